@@ -1,0 +1,162 @@
+/*
+ * sida_b200.h -- C ABI of the B200-native SiDA serving hot path.
+ *
+ * One shared library (paper_2310_18859_b200/_sida_b200.so, sm_100a) exports
+ * the entry points below. Conventions:
+ *   - callers own every buffer; nothing here allocates device memory
+ *     (workspace sizes are queried with the *_workspace_bytes helpers);
+ *   - every launch takes an explicit stream (a cudaStream_t passed as void*);
+ *   - calls are re-entrant across distinct streams and buffers;
+ *   - status codes map onto the reference exception taxonomy
+ *     (ref pkg/src/sida/errors.py:4-13): no exception crosses the ABI,
+ *     the Python mirror raises the matching type. sida_last_error() returns
+ *     the calling thread's message for the last non-zero status.
+ *
+ * Reference interfaces each export replaces are cited per function
+ * ("ref" = /root/reference/pkg/src/sida/).
+ */
+#ifndef SIDA_B200_H
+#define SIDA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  SIDA_OK = 0,
+  SIDA_ERR_CONTRACT = 1,    /* -> ContractError   (ref errors.py:4)  */
+  SIDA_ERR_COVERAGE = 2,    /* -> CoverageError   (ref errors.py:8)  */
+  SIDA_ERR_UNSERVABLE = 3,  /* -> UnservableError (ref errors.py:12) */
+  SIDA_ERR_CUDA = 4,        /* CUDA runtime / launch failure          */
+  SIDA_ERR_UNSUPPORTED = 5  /* shape/arch outside the kernel's contract */
+};
+
+/* Library identity and the device check (fails unless cc 10.0 / sm_100). */
+int sida_abi_version(void);
+const char* sida_last_error(void);
+int sida_device_check(int device);
+
+/* ---------------------------------------------------------------------
+ * (1) Hash-function predictor, fp64.
+ * Replaces ref predictor.py:373-399 (build_hash_table) over
+ * PredictorNet.forward (predictor.py:234-259) + softmax/topk_rows
+ * (numkit.py:28-33, 87-93), batched over every sequence of a batch.
+ *
+ * params: float64, packed in this order (row-major, x@W convention):
+ *   compress_w (d,cd) compress_b (cd)
+ *   lstm1_wx (cd,4H) lstm1_wh (H,4H) lstm1_b (4H)
+ *   lstm2_wx (H,4H)  lstm2_wh (H,4H) lstm2_b (4H)
+ *   attn_wq (H,H) attn_wk (H,H) attn_wv (H,H)
+ *   head_w (L,H,K) head_b (L,K)
+ * tok_emb (vocab,d) / pos_emb (max_len,d): the bf16 embedding tables of the
+ *   MoE model (embed = tok_emb[t] + pos_emb[pos], summed in fp64;
+ *   ref moe.py:206-218). emb_f64 (n_tokens, d), optional, replaces the
+ *   tables for a caller-supplied embed_fn (ref predictor.py:377).
+ * tokens: int32 (n_tokens), seq_off: int32 (n_seq+1) exclusive offsets.
+ * Outputs, global-token layout (L, n_tokens, topk) (ref moe.py:14-16):
+ *   ids int32, alpha float64 (softmax probability at the id, not
+ *   renormalised), alpha_f32 optional float32 copy for the FFN epilogue.
+ * ------------------------------------------------------------------- */
+size_t sida_hash_param_count(int d, int cd, int H, int L, int K);
+size_t sida_hash_workspace_bytes(int n_tokens, int n_seq, int max_len, int d, int cd, int H,
+                                 int L, int K);
+int sida_hash_forward(const double* params, const uint16_t* tok_emb, const uint16_t* pos_emb,
+                      const double* emb_f64, const int32_t* tokens, const int32_t* seq_off, int n_seq, int n_tokens,
+                      int max_len, int d, int cd, int H, int L, int K, int topk,
+                      int32_t* ids, double* alpha, float* alpha_f32,
+                      void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------------
+ * (3) Token permute + histogram (SURVEY §8(a) A13 contract), all layers.
+ * ids: int32 (L, n_rows) with n_rows = n_tokens*k, row = token*k + rank.
+ * Outputs per layer: hist (L,K), off (L,K+1), perm (L,n_rows) stable by
+ * row within expert, inv (L,n_rows) with inv[perm[p]] = p; alpha_perm
+ * (optional, L x n_rows float32) = alpha_rows[perm[p]].
+ * Replaces the implicit grouping of ref moe.py:253-256 (w1[ids] gather).
+ * ------------------------------------------------------------------- */
+size_t sida_permute_workspace_bytes(int n_layers, int n_rows, int num_experts);
+int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, int num_experts,
+                      const float* alpha_rows, int32_t* hist, int32_t* off, int32_t* perm,
+                      int32_t* inv, float* alpha_perm, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/* x_perm[p, :] = bf16(x[perm[p] / k, :]), x float32 (n_tokens, d), 128-bit
+ * coalesced. (The row gather half of A13.) */
+int sida_gather_rows_bf16(const float* x, const int32_t* perm, int n_rows, int k, int d,
+                          uint16_t* x_perm, void* stream);
+
+/* ---------------------------------------------------------------------
+ * (4) Expert FFN over permuted rows, bf16 tcgen05/TMEM/TMA grouped GEMM.
+ * Replaces ref moe.py:235-262 (moe_apply): per expert e,
+ *   f = relu(X_e W1_e + b1_e) W2_e + b2_e, out[row_map[p]] = alpha[p]*f (+ resid)
+ * Weights live in HBM slots of one arena (slot stride slot_stride bytes):
+ *   [0, h*d*2)        W1^T  (h, d) bf16, K-major
+ *   [w2_off, +d*h*2)  W2^T  (d, h) bf16, K-major,  w2_off = h*d*2
+ *   [b1_off, +h*2)    b1 (h) bf16,                 b1_off = 2*h*d*2
+ *   [b2_off, +d*2)    b2 (d) bf16,                 b2_off = b1_off + h*2
+ * expert_slot (K) int32 maps expert -> slot (-1 = not resident: such an
+ * expert must have no rows or the call fails with SIDA_ERR_CONTRACT on the
+ * device-side check flag). expert_list (n_list, optional) restricts the
+ * launch to a subset of experts (layers whose working set exceeds the budget
+ * run in waves).
+ * row_map (n_rows, optional; identity if NULL): output row of permuted row p.
+ * alpha (n_rows, optional; 1 if NULL), resid (optional, indexed like out).
+ * out: float32, row stride d. hidden: bf16 workspace (n_rows, h).
+ * Requires d % 64 == 0, h % 64 == 0.
+ * ------------------------------------------------------------------- */
+size_t sida_slot_bytes(int d, int h);
+int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h, const int32_t* off,
+                          int num_experts, const int32_t* expert_slot, const int32_t* expert_list,
+                          int n_list, const void* arena, size_t slot_stride, int n_slots,
+                          const int32_t* row_map, const float* alpha, const float* resid,
+                          float* out, uint16_t* hidden, int32_t* err_flag, void* stream);
+
+/* fp32 FMA check path: same contraction with float32 weights in the
+ * reference layout w1 (K,d,h), b1 (K,h), w2 (K,h,d), b2 (K,d); x_perm
+ * float32; hidden float32 workspace (n_rows, h). */
+int sida_grouped_ffn_f32(const float* x_perm, int n_rows, int d, int h, const int32_t* off,
+                         int num_experts, const float* w1, const float* b1, const float* w2,
+                         const float* b2, const int32_t* row_map, const float* alpha,
+                         const float* resid, float* out, float* hidden, void* stream);
+
+/* k > 1 combine: out[t] = resid[t] + sum_{r=0..k-1} y[t*k + r] (ranks in
+ * order, ref moe.py:252-262). */
+int sida_combine_ranks(const float* y, const float* resid, int n_tokens, int k, int d, float* out,
+                       void* stream);
+
+/* ---------------------------------------------------------------------
+ * (2) Expert streaming: one pinned-host expert image -> one HBM slot on the
+ * copy stream, ordered after wait_event (the slot's last reader) and
+ * followed by done_event. Replaces the simulated transfer of ref
+ * offload.py:207-222 + pipeline.py:141-146,229-254.
+ * ------------------------------------------------------------------- */
+int sida_expert_copy(void* dst_slot, const void* src_pinned, size_t bytes, void* copy_stream,
+                     void* wait_event, void* done_event);
+
+/* Pack one expert from the reference layout (float64 w1 (d,h), b1 (h),
+ * w2 (h,d), b2 (d)) into the slot image above (host memory, bf16 RNE).
+ * dst must hold sida_slot_bytes(d,h) bytes. */
+int sida_pack_expert_host(const double* w1, const double* b1, const double* w2, const double* b2,
+                          int d, int h, void* dst);
+
+
+/* ---------------------------------------------------------------------
+ * (2) Residency planner (host, native): ref offload.py:118-204 with the
+ * budget in whole expert slots. required: uint8 (L, K) bitmap of the experts
+ * each layer of the batch needs (ref predictor.py:96-100). fifo_in: resident
+ * keys (layer*K + expert) in arrival order. steps (capacity >= L*K*2 +
+ * fifo_len): key for a load, -(key+1) for an eviction, in execution order;
+ * group_off (L+1) delimits each layer's group; prefetchable (L) per group.
+ * Needs no GPU.
+ * ------------------------------------------------------------------- */
+int sida_plan_placement(const uint8_t* required, int n_layers, int num_experts, int budget_slots,
+                        const int32_t* fifo_in, int fifo_len, int32_t* steps, int steps_capacity,
+                        int32_t* group_off, uint8_t* prefetchable);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIDA_B200_H */

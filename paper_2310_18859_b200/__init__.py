@@ -1,0 +1,34 @@
+"""SiDA data-aware MoE serving hot path, B200-native (sm_100a).
+
+Public names mirror the hot-path subset of the reference package's API
+(ref pkg/src/sida/__init__.py:1-50): the hash-function predictor, the
+expert hash table, the FIFO residency planner and the two-worker serving
+loop. Compute runs in the hand-written CUDA library `_sida_b200.so`
+(include/sida_b200.h); there is no CPU fallback.
+"""
+
+from .errors import ContractError, CoverageError, NativeLibraryError, TrainingDiverged, UnservableError
+from .moe import ActivationTrace, BatchLayout, MoEConfig, MoEModel, Rng, SequenceBatch, model_forward
+from .predictor import (
+    DeviceTable,
+    ExpertHashTable,
+    PredictorConfig,
+    PredictorHasher,
+    PredictorNet,
+    build_hash_table,
+)
+from .offload import (
+    ExpertStore,
+    MemoryBudget,
+    PlacementPlan,
+    PlanGroup,
+    ResidencyState,
+    apply_group_inplace,
+    apply_plan,
+    effective_utilization,
+    memory_reduction,
+    plan_placement,
+)
+from .pipeline import HashTableQueue, ServingReport, serve_sida
+
+__version__ = "0.1.0"

@@ -1,0 +1,105 @@
+"""ctypes binding of the sm_100a C ABI (include/sida_b200.h).
+
+This is the only place Python crosses into native code. There is no CPU
+fallback: if the library is missing or the device is not an sm_100 part,
+``lib()`` raises ``NativeLibraryError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from .errors import ContractError, CoverageError, NativeLibraryError, UnservableError
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "_sida_b200.so")
+
+OK, ERR_CONTRACT, ERR_COVERAGE, ERR_UNSERVABLE, ERR_CUDA, ERR_UNSUPPORTED = range(6)
+
+_vp, _i, _sz = C.c_void_p, C.c_int, C.c_size_t
+
+# name -> (restype, argtypes); mirrors include/sida_b200.h one-to-one.
+SIGNATURES = {
+    "sida_abi_version": (_i, []),
+    "sida_last_error": (C.c_char_p, []),
+    "sida_device_check": (_i, [_i]),
+    "sida_hash_param_count": (_sz, [_i, _i, _i, _i, _i]),
+    "sida_hash_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),
+    "sida_hash_forward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i,
+                               _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sida_permute_workspace_bytes": (_sz, [_i, _i, _i]),
+    "sida_permute_hist": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sida_gather_rows_bf16": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    "sida_slot_bytes": (_sz, [_i, _i]),
+    "sida_grouped_ffn_bf16": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _i, _vp, _sz, _i, _vp, _vp,
+                                   _vp, _vp, _vp, _vp, _vp]),
+    "sida_grouped_ffn_f32": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp, _vp, _vp]),
+    "sida_combine_ranks": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    "sida_expert_copy": (_i, [_vp, _vp, _sz, _vp, _vp, _vp]),
+    "sida_pack_expert_host": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp]),
+    "sida_plan_placement": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp]),
+}
+
+_lock = threading.Lock()
+_handle = None
+_device_checked: set[int] = set()
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load the library and bind every signature (no device needed)."""
+    global _handle
+    with _lock:
+        if _handle is not None:
+            return _handle
+        if not os.path.exists(path):
+            raise NativeLibraryError(
+                f"{path} not found: build it with `python -m paper_2310_18859_b200.build`")
+        try:
+            h = C.CDLL(path)
+        except OSError as exc:  # pragma: no cover - depends on the box
+            raise NativeLibraryError(f"cannot load {path}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        _handle = h
+        return h
+
+
+def lib(device: int | None = None) -> C.CDLL:
+    """The loaded library, after checking the CUDA device is sm_100."""
+    h = load()
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("no CUDA device: the SiDA B200 path has no CPU fallback")
+    dev = torch.cuda.current_device() if device is None else device
+    if dev not in _device_checked:
+        check(h.sida_device_check(dev))
+        _device_checked.add(dev)
+    return h
+
+
+def check(status: int) -> None:
+    if status == OK:
+        return
+    msg = (load().sida_last_error() or b"").decode(errors="replace")
+    if status == ERR_COVERAGE:
+        raise CoverageError(msg)
+    if status == ERR_CONTRACT:
+        raise ContractError(msg)
+    if status == ERR_UNSERVABLE:
+        raise UnservableError(msg)
+    raise NativeLibraryError(f"[status {status}] {msg}")
+
+
+def ptr(t) -> int | None:
+    """Device/host address of a tensor (None for None)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(stream) -> int:
+    return stream.cuda_stream

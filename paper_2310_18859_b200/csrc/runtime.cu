@@ -1,0 +1,116 @@
+// Status plumbing, device check, expert streaming and host-side slot packing.
+//
+// sida_expert_copy is the B200 replacement of the simulated transfer in
+// ref offload.py:207-222 + pipeline.py:141-146 (a sleep): a real
+// cudaMemcpyAsync from pinned host DRAM into an HBM slot on the dedicated copy
+// stream, ordered after the slot's last reader and followed by a done event
+// the compute stream waits on.
+#include <stdarg.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace sida {
+
+static thread_local char g_err[512] = {0};
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+}  // namespace sida
+
+extern "C" int sida_abi_version(void) { return 1; }
+
+extern "C" const char* sida_last_error(void) { return sida::g_err; }
+
+extern "C" int sida_device_check(int device) {
+  cudaDeviceProp prop;
+  SIDA_CUDA(cudaGetDeviceProperties(&prop, device));
+  SIDA_REQUIRE(prop.major == 10 && prop.minor == 0, SIDA_ERR_UNSUPPORTED,
+               "device %d is sm_%d%d (%s); this library is built for sm_100a only", device,
+               prop.major, prop.minor, prop.name);
+  return SIDA_OK;
+}
+
+extern "C" size_t sida_slot_bytes(int d, int h) {
+  size_t raw = (2ull * d * h + h + d) * 2ull;
+  return sida::align_up(raw, 256);
+}
+
+extern "C" int sida_expert_copy(void* dst_slot, const void* src_pinned, size_t bytes,
+                                void* copy_stream, void* wait_event, void* done_event) {
+  SIDA_REQUIRE(dst_slot && src_pinned, SIDA_ERR_CONTRACT, "null copy endpoint");
+  cudaStream_t s = sida::as_stream(copy_stream);
+  if (wait_event) SIDA_CUDA(cudaStreamWaitEvent(s, reinterpret_cast<cudaEvent_t>(wait_event), 0));
+  SIDA_CUDA(cudaMemcpyAsync(dst_slot, src_pinned, bytes, cudaMemcpyHostToDevice, s));
+  if (done_event) SIDA_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(done_event), s));
+  return SIDA_OK;
+}
+
+static inline uint16_t host_bf16(double v) {
+  float f = static_cast<float>(v);  // RNE double -> float
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+extern "C" int sida_pack_expert_host(const double* w1, const double* b1, const double* w2,
+                                     const double* b2, int d, int h, void* dst) {
+  SIDA_REQUIRE(w1 && b1 && w2 && b2 && dst, SIDA_ERR_CONTRACT, "null pointer in pack");
+  uint16_t* out = static_cast<uint16_t*>(dst);
+  uint16_t* w1t = out;                    // (h, d): w1t[n][k] = w1[k][n]
+  uint16_t* w2t = out + (size_t)h * d;    // (d, h): w2t[n][k] = w2[k][n]
+  uint16_t* ob1 = out + 2ull * h * d;
+  uint16_t* ob2 = ob1 + h;
+  for (int k = 0; k < d; ++k)
+    for (int n = 0; n < h; ++n) w1t[(size_t)n * d + k] = host_bf16(w1[(size_t)k * h + n]);
+  for (int k = 0; k < h; ++k)
+    for (int n = 0; n < d; ++n) w2t[(size_t)n * h + k] = host_bf16(w2[(size_t)k * d + n]);
+  for (int n = 0; n < h; ++n) ob1[n] = host_bf16(b1[n]);
+  for (int n = 0; n < d; ++n) ob2[n] = host_bf16(b2[n]);
+  size_t used = (2ull * d * h + h + d) * 2ull;
+  memset(static_cast<char*>(dst) + used, 0, sida_slot_bytes(d, h) - used);
+  return SIDA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// k > 1 rank combine: out[t] = resid[t] + sum_r y[t*k + r], ranks in order
+// (ref moe.py:252-262 accumulates rank outputs in order then adds x).
+__global__ void combine_ranks_kernel(const float4* __restrict__ y, const float4* __restrict__ resid,
+                                     int n_tokens, int k, int d4, float4* __restrict__ out) {
+  long total = (long)n_tokens * d4;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
+       i += (long)gridDim.x * blockDim.x) {
+    long t = i / d4;
+    int c = static_cast<int>(i - t * d4);
+    float4 acc = y[(t * k) * d4 + c];
+    for (int r = 1; r < k; ++r) {
+      float4 v = y[(t * k + r) * d4 + c];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (resid) {
+      float4 x = resid[t * d4 + c];
+      acc.x = x.x + acc.x; acc.y = x.y + acc.y; acc.z = x.z + acc.z; acc.w = x.w + acc.w;
+    }
+    out[t * d4 + c] = acc;
+  }
+}
+
+extern "C" int sida_combine_ranks(const float* y, const float* resid, int n_tokens, int k, int d,
+                                  float* out, void* stream) {
+  SIDA_REQUIRE(d % 4 == 0 && k >= 1 && n_tokens >= 0, SIDA_ERR_UNSUPPORTED,
+               "combine needs d %% 4 == 0 (d=%d) and k >= 1", d);
+  if (n_tokens == 0) return SIDA_OK;
+  long total = (long)n_tokens * (d / 4);
+  int blocks = (int)std::min<long>((total + 255) / 256, sida::kNumSMs * 8);
+  combine_ranks_kernel<<<blocks, 256, 0, sida::as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(y), reinterpret_cast<const float4*>(resid), n_tokens, k,
+      d / 4, reinterpret_cast<float4*>(out));
+  SIDA_LAUNCH_CHECK();
+  return SIDA_OK;
+}

@@ -1,0 +1,441 @@
+"""B200 MoE model: host mirror of the forward half of ref pkg/src/sida/moe.py.
+
+Same public names as the reference (`MoEConfig`, `SequenceBatch`,
+`ActivationTrace`, `MoEModel`, `model_forward`), but the model lives on the
+GPU and runs a whole batch per layer instead of one sequence at a time:
+
+  embed          tok_emb[t] + pos_emb[pos] from bf16 tables (ref moe.py:206-218)
+  attention_mix  single-head non-causal mixing (ref moe.py:220-233); cuBLAS
+                 bf16 via torch for now (SURVEY §8(f) row 1 makes it a kernel)
+  moe_apply      the SiDA hot path: permuted-row gather + tcgen05 grouped FFN
+                 with the alpha/unpermute/residual epilogue (ref moe.py:235-262)
+  pool_classify  per-sequence mean and linear head (ref moe.py:264-266)
+
+Memory layout: the residual stream x is float32
+(n_tokens, d); expert weights never live in this object's device memory --
+each (layer, expert) is one pinned host "slot image" (W1^T, W2^T, b1, b2 in
+bf16, sida_slot_bytes(d, h) bytes) streamed into HBM slots by
+``offload.ExpertStore``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ContractError
+
+
+@dataclass
+class MoEConfig:
+    """ref moe.py:40-59 (same fields, defaults and validation)."""
+
+    vocab_size: int = 512
+    d_model: int = 64
+    num_layers: int = 2
+    num_experts: int = 32
+    expert_hidden: int = 128
+    max_seq_len: int = 64
+    routing_k: int = 1
+    num_classes: int = 4
+
+    def __post_init__(self):
+        for name in ("vocab_size", "d_model", "num_layers", "num_experts", "expert_hidden",
+                     "max_seq_len", "routing_k", "num_classes"):
+            if getattr(self, name) < 1:
+                raise ContractError(f"{name} must be >= 1")
+        if self.routing_k > self.num_experts:
+            raise ContractError("routing_k must not exceed num_experts")
+
+
+@dataclass
+class SequenceBatch:
+    """ref moe.py:62-80."""
+
+    batch_id: int
+    sequences: list
+    labels: list | None = None
+
+    @property
+    def lengths(self) -> list[int]:
+        return [len(s) for s in self.sequences]
+
+    @property
+    def num_tokens(self) -> int:
+        return sum(self.lengths)
+
+
+@dataclass
+class ActivationTrace:
+    """ref moe.py:83-105 (external mode: probs is None)."""
+
+    lengths: list[int]
+    selected: np.ndarray
+    alphas: np.ndarray
+    probs: np.ndarray | None
+
+    @property
+    def num_layers(self) -> int:
+        return self.selected.shape[0]
+
+    @property
+    def offsets(self) -> list[int]:
+        out = [0]
+        for n in self.lengths:
+            out.append(out[-1] + n)
+        return out
+
+
+class Rng:
+    """Deterministic PCG64 stream over SeedSequence(seed), the generator of
+    ref numkit.py:172-209, so `MoEModel(cfg, Rng(s))` draws the reference's
+    weights bit-for-bit."""
+
+    algorithm = "pcg64"
+
+    def __init__(self, seed: int, _seq: np.random.SeedSequence | None = None):
+        self.seed = int(seed)
+        self._seq = _seq if _seq is not None else np.random.SeedSequence(self.seed)
+        self._gen = np.random.Generator(np.random.PCG64(self._seq))
+
+    def split(self, n: int) -> list["Rng"]:
+        return [Rng(self.seed, _seq=c) for c in self._seq.spawn(n)]
+
+    def integers(self, low, high=None, size=None):
+        return self._gen.integers(low, high=high, size=size)
+
+    def normal(self, loc=0.0, scale=1.0, size=None):
+        return self._gen.normal(loc=loc, scale=scale, size=size)
+
+    def uniform(self, low=0.0, high=1.0, size=None):
+        return self._gen.uniform(low=low, high=high, size=size)
+
+    def random(self, size=None):
+        return self._gen.random(size=size)
+
+    def choice(self, a, size=None, replace=True, p=None):
+        return self._gen.choice(a, size=size, replace=replace, p=p)
+
+    def permutation(self, x):
+        return self._gen.permutation(x)
+
+
+def to_bf16(a: np.ndarray, device=None) -> torch.Tensor:
+    """float64 -> float32 (RNE) -> bfloat16 (RNE): the one rounding recipe the
+    GPU model and the parity oracle share (tests/test_oracle_golden.py)."""
+    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(torch.float32)
+    t = t.to(torch.bfloat16)
+    return t if device is None else t.to(device)
+
+
+def _default_device():
+    if not torch.cuda.is_available():
+        raise _lib.NativeLibraryError("MoEModel needs a CUDA (sm_100a) device")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class BatchLayout:
+    """A batch's concatenated global token axis on the device (ref moe.py:14-16)."""
+
+    def __init__(self, lengths: list[int], tokens: torch.Tensor, device):
+        self.lengths = [int(n) for n in lengths]
+        self.n_seq = len(self.lengths)
+        self.n_tokens = int(sum(self.lengths))
+        self.max_len = max(self.lengths)
+        self.uniform = all(n == self.max_len for n in self.lengths)
+        off = np.zeros(self.n_seq + 1, dtype=np.int64)
+        np.cumsum(self.lengths, out=off[1:])
+        self.offsets = off
+        self.tokens = tokens  # int32 (n_tokens,) on device
+        self.seq_off = torch.from_numpy(off.astype(np.int32)).to(device, non_blocking=True)
+        seq_id = np.repeat(np.arange(self.n_seq), self.lengths)
+        pos = np.arange(self.n_tokens) - off[seq_id]
+        self.pos = torch.from_numpy(pos).to(device, non_blocking=True)
+        self.seq_id = torch.from_numpy(seq_id).to(device, non_blocking=True)
+        self.len_t = torch.tensor(self.lengths, dtype=torch.float32).to(device, non_blocking=True)
+        if not self.uniform:
+            pad = np.full((self.n_seq, self.max_len), self.n_tokens, dtype=np.int64)
+            for i, n in enumerate(self.lengths):
+                pad[i, :n] = np.arange(off[i], off[i] + n)
+            self.pad_index = torch.from_numpy(pad.reshape(-1)).to(device, non_blocking=True)
+            mask = np.zeros((self.n_seq, 1, self.max_len), dtype=np.float32)
+            for i, n in enumerate(self.lengths):
+                mask[i, 0, n:] = -np.inf
+            self.key_mask = torch.from_numpy(mask).to(device, non_blocking=True)
+            self.valid_rows = torch.from_numpy(
+                np.concatenate([np.arange(i * self.max_len, i * self.max_len + n)
+                                for i, n in enumerate(self.lengths)])).to(device, non_blocking=True)
+
+    @classmethod
+    def from_batch(cls, model: "MoEModel", batch: SequenceBatch) -> "BatchLayout":
+        toks = model.validate_tokens(batch)
+        pinned = torch.from_numpy(toks).pin_memory()
+        return cls(batch.lengths, pinned.to(model.device, non_blocking=True), model.device)
+
+
+def reference_init(config: MoEConfig, rng: Rng) -> dict[str, np.ndarray]:
+    """Draw the parameters in the order of ref moe.py:158-181."""
+    c = config
+    d, h, ne = c.d_model, c.expert_hidden, c.num_experts
+    p: dict[str, np.ndarray] = {}
+    p["tok_emb"] = rng.normal(0.0, 1.0 / np.sqrt(d), (c.vocab_size, d))
+    p["pos_emb"] = rng.normal(0.0, 1.0 / np.sqrt(d), (c.max_seq_len, d))
+    for layer in range(c.num_layers):
+        pre = f"block{layer}."
+        for name in ("wq", "wk", "wv", "wo"):
+            p[pre + name] = rng.normal(0.0, np.sqrt(1.0 / d), (d, d))
+        p[pre + "w_r"] = rng.normal(0.0, np.sqrt(1.0 / d), (d, ne))
+        p[pre + "w1"] = rng.normal(0.0, np.sqrt(2.0 / (d + h)), (ne, d, h))
+        p[pre + "b1"] = np.zeros((ne, h))
+        p[pre + "w2"] = rng.normal(0.0, np.sqrt(2.0 / (d + h)), (ne, h, d))
+        p[pre + "b2"] = np.zeros((ne, d))
+    p["wc"] = rng.normal(0.0, np.sqrt(1.0 / d), (d, c.num_classes))
+    return p
+
+
+class MoEModel:
+    """Embeddings, mixing attention, experts (as pinned slot images), head.
+
+    ``MoEModel(config, rng)`` draws the reference's weights (ref moe.py:158)
+    and holds them at bf16; ``MoEModel(config, params=...)`` takes a reference
+    parameter dict; ``MoEModel.synthetic(config, seed)`` draws Switch-shaped
+    random weights directly on the GPU for shapes whose float64 reference
+    init would not fit host RAM (not reference-identical).
+    """
+
+    def __init__(self, config: MoEConfig, rng: Rng | None = None, *, params=None, device=None):
+        self.config = config
+        self.device = torch.device(device) if device is not None else _default_device()
+        self.slot_stride = int(_lib.load().sida_slot_bytes(config.d_model, config.expert_hidden))
+        self.expert_images = None  # pinned uint8 (L*K, slot_stride)
+        if params is None and rng is None:
+            rng = Rng(0)
+        if params is None:
+            params = reference_init(config, rng)
+        self._load_params(params)
+
+    # -- construction -----------------------------------------------------------------
+    def _alloc_images(self):
+        c = self.config
+        self.expert_images = torch.empty((c.num_layers * c.num_experts, self.slot_stride),
+                                         dtype=torch.uint8).pin_memory()
+
+    def _load_params(self, params):
+        c = self.config
+        dev = self.device
+        self.tok_emb = to_bf16(params["tok_emb"], dev)
+        self.pos_emb = to_bf16(params["pos_emb"], dev)
+        self.wqkv, self.wo, self.w_r = [], [], []
+        for layer in range(c.num_layers):
+            pre = f"block{layer}."
+            self.wqkv.append(torch.cat([to_bf16(params[pre + n]) for n in ("wq", "wk", "wv")],
+                                       dim=1).to(dev))
+            self.wo.append(to_bf16(params[pre + "wo"], dev))
+            self.w_r.append(to_bf16(params[pre + "w_r"]).float().to(dev))
+        self.wc = to_bf16(params["wc"]).float().to(dev)
+        self._alloc_images()
+        h = _lib.load()
+        for layer in range(c.num_layers):
+            pre = f"block{layer}."
+            w1, b1 = params[pre + "w1"], params[pre + "b1"]
+            w2, b2 = params[pre + "w2"], params[pre + "b2"]
+            for e in range(c.num_experts):
+                arrs = [np.ascontiguousarray(a[e], dtype=np.float64) for a in (w1, b1, w2, b2)]
+                dst = self.expert_images[layer * c.num_experts + e]
+                _lib.check(h.sida_pack_expert_host(*(a.ctypes.data for a in arrs), c.d_model,
+                                                   c.expert_hidden, dst.data_ptr()))
+
+    @classmethod
+    def synthetic(cls, config: MoEConfig, seed: int = 0, device=None) -> "MoEModel":
+        """Random-init Switch-shaped weights drawn on the GPU (same scales as
+        ref moe.py:163-179: N(0,1/sqrt d) embeddings, N(0,sqrt(1/d)) mixing,
+        N(0,sqrt(2/(d+h))) experts, zero biases), rounded to bf16."""
+        self = cls.__new__(cls)
+        self.config = c = config
+        self.device = torch.device(device) if device is not None else _default_device()
+        self.slot_stride = int(_lib.load().sida_slot_bytes(c.d_model, c.expert_hidden))
+        g = torch.Generator(device=self.device)
+        g.manual_seed(int(seed))
+        d, hh = c.d_model, c.expert_hidden
+
+        def randn(shape, std, dtype=torch.bfloat16):
+            return (torch.randn(shape, generator=g, device=self.device, dtype=torch.float32)
+                    * std).to(dtype)
+
+        self.tok_emb = randn((c.vocab_size, d), 1.0 / math.sqrt(d))
+        self.pos_emb = randn((c.max_seq_len, d), 1.0 / math.sqrt(d))
+        self.wqkv = [randn((d, 3 * d), math.sqrt(1.0 / d)) for _ in range(c.num_layers)]
+        self.wo = [randn((d, d), math.sqrt(1.0 / d)) for _ in range(c.num_layers)]
+        self.w_r = [randn((d, c.num_experts), math.sqrt(1.0 / d)).float()
+                    for _ in range(c.num_layers)]
+        self.wc = randn((d, c.num_classes), math.sqrt(1.0 / d)).float()
+        self._alloc_images()
+        s_dh = math.sqrt(2.0 / (d + hh))
+        n_el = 2 * d * hh
+        for i in range(c.num_layers * c.num_experts):
+            img = torch.zeros(self.slot_stride // 2, dtype=torch.bfloat16, device=self.device)
+            img[:n_el] = randn((n_el,), s_dh)
+            self.expert_images[i].copy_(img.view(torch.uint8))
+        torch.cuda.synchronize(self.device)
+        return self
+
+    # -- parameter bookkeeping (ref moe.py:188-198) ---------------------------------
+    def expert_bytes_each(self) -> int:
+        """Bytes one expert occupies in an HBM slot (bf16 image)."""
+        return self.slot_stride
+
+    def total_expert_bytes(self) -> int:
+        return self.expert_bytes_each() * self.config.num_layers * self.config.num_experts
+
+    def non_expert_bytes(self) -> int:
+        n = self.tok_emb.numel() + self.pos_emb.numel()
+        n += sum(t.numel() for t in self.wqkv) + sum(t.numel() for t in self.wo)
+        return 2 * n + 4 * (self.wc.numel() + sum(t.numel() for t in self.w_r))
+
+    def expert_image(self, layer: int, expert: int) -> torch.Tensor:
+        return self.expert_images[layer * self.config.num_experts + expert]
+
+    # -- forward pieces -------------------------------------------------------------
+    def validate_tokens(self, batch: SequenceBatch) -> np.ndarray:
+        """ref moe.py:208-217 checks, for a whole batch; returns int32 tokens."""
+        c = self.config
+        if not batch.sequences:
+            raise ContractError("empty batch")
+        for s in batch.sequences:
+            n = len(s)
+            if n == 0:
+                raise ContractError("empty sequence")
+            if n > c.max_seq_len:
+                raise ContractError(f"sequence length {n} exceeds max_seq_len {c.max_seq_len}")
+        toks = np.concatenate([np.asarray(s, dtype=np.int64) for s in batch.sequences])
+        if toks.min() < 0 or toks.max() >= c.vocab_size:
+            raise ContractError("token id out of vocabulary")
+        return toks.astype(np.int32)
+
+    def embed(self, tokens) -> np.ndarray:
+        """One sequence's input embeddings, float64 of the bf16 tables
+        (ref moe.py:206-218). The GPU hasher recognises this bound method and
+        reads the tables on the device instead of calling it."""
+        toks = self.validate_tokens(SequenceBatch(0, [tokens])).astype(np.int64)
+        te = self.tok_emb.index_select(0, torch.from_numpy(toks).to(self.device)).double()
+        return (te + self.pos_emb[: toks.size].double()).cpu().numpy()
+
+    def embed_layout(self, lay: BatchLayout) -> torch.Tensor:
+        """float32 (n_tokens, d): tok_emb[t] + pos_emb[pos] (exact in fp32)."""
+        return (self.tok_emb.index_select(0, lay.tokens.long()).float()
+                + self.pos_emb.index_select(0, lay.pos).float())
+
+    def attention_mix(self, layer: int, x: torch.Tensor, lay: BatchLayout) -> torch.Tensor:
+        """x + softmax(q k^T / sqrt(d)) v W_o per sequence (ref moe.py:220-233)."""
+        d = self.config.d_model
+        qkv = x.to(torch.bfloat16) @ self.wqkv[layer]
+        if lay.uniform:
+            qkv = qkv.view(lay.n_seq, lay.max_len, 3 * d)
+        else:
+            qkv = torch.cat([qkv, qkv.new_zeros(1, 3 * d)]).index_select(0, lay.pad_index)
+            qkv = qkv.view(lay.n_seq, lay.max_len, 3 * d)
+        q, k, v = qkv.split(d, dim=2)
+        scores = torch.bmm(q, k.transpose(1, 2)).float() * (1.0 / math.sqrt(d))
+        if not lay.uniform:
+            scores = scores + lay.key_mask
+        attn = torch.softmax(scores, dim=-1).to(torch.bfloat16)
+        ctx = torch.bmm(attn, v).reshape(-1, d)
+        if not lay.uniform:
+            ctx = ctx.index_select(0, lay.valid_rows)
+        return x + (ctx @ self.wo[layer]).float()
+
+    def pool_classify(self, x: torch.Tensor, lay: BatchLayout) -> torch.Tensor:
+        """(n_seq, C): per-sequence mean then the classifier (ref moe.py:264-266)."""
+        if lay.uniform:
+            pooled = x.view(lay.n_seq, lay.max_len, -1).mean(dim=1)
+        else:
+            sums = x.new_zeros(lay.n_seq, x.shape[1]).index_add_(0, lay.seq_id, x)
+            pooled = sums / lay.len_t[:, None]
+        return pooled @ self.wc
+
+    def moe_apply_rows(self, layer_tables, x: torch.Tensor, k: int, arena, slot_row: torch.Tensor,
+                       expert_list: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                       y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """The SiDA expert FFN for one layer over the whole batch.
+
+        ``layer_tables`` = (off (K+1,), perm (R,), alpha_perm (R,)) of this
+        layer from sida_permute_hist; ``slot_row`` (K,) int32 expert -> slot.
+        k == 1: out[t] = x[t] + alpha * f(x[t]) written by the GEMM2
+        epilogue directly (unpermute + residual fused). k > 1: the epilogue
+        writes alpha_r f_r into row t*k+r of ``y`` and sida_combine_ranks adds
+        the ranks in order plus the residual (ref moe.py:252-262).
+        """
+        c = self.config
+        h = _lib.lib()
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        sh = st.cuda_stream
+        off, perm, alpha_perm = layer_tables
+        n_tok = x.shape[0]
+        rows = n_tok * k
+        x_perm = torch.empty((rows, c.d_model), dtype=torch.bfloat16, device=self.device)
+        hidden = torch.empty((rows, c.expert_hidden), dtype=torch.bfloat16, device=self.device)
+        _lib.check(h.sida_gather_rows_bf16(x.data_ptr(), perm.data_ptr(), rows, k, c.d_model,
+                                           x_perm.data_ptr(), sh))
+        err = arena.err_flag
+        n_list = 0 if expert_list is None else int(expert_list.numel())
+        if out is None:
+            out = torch.empty_like(x)
+        if k == 1:
+            target, resid = out, x
+        else:
+            target = y if y is not None else torch.empty((rows, c.d_model), dtype=torch.float32,
+                                                         device=self.device)
+            resid = None
+        _lib.check(h.sida_grouped_ffn_bf16(
+            x_perm.data_ptr(), rows, c.d_model, c.expert_hidden, off.data_ptr(), c.num_experts,
+            slot_row.data_ptr(), _lib.ptr(expert_list), n_list, arena.base_ptr,
+            arena.slot_stride, arena.n_slots, perm.data_ptr(), alpha_perm.data_ptr(),
+            _lib.ptr(resid), target.data_ptr(), hidden.data_ptr(), err.data_ptr(), sh))
+        return target if k == 1 else target
+
+    def combine(self, y: torch.Tensor, x: torch.Tensor, k: int, out: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+        h = _lib.lib()
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        if out is None:
+            out = torch.empty_like(x)
+        _lib.check(h.sida_combine_ranks(y.data_ptr(), x.data_ptr(), x.shape[0], k,
+                                        self.config.d_model, out.data_ptr(), st.cuda_stream))
+        return out
+
+
+def model_forward(model: MoEModel, batch: SequenceBatch, mode: str = "external", table=None,
+                  timings: dict | None = None, store=None):
+    """Forward a whole batch in external (hash-table) mode (ref moe.py:408-442).
+
+    Returns (logits numpy (B, C), ActivationTrace). Every expert the table
+    names is made resident in ``store`` (default: a store holding all
+    experts) before its layer runs. Router mode is SURVEY §8(f) "next".
+    """
+    from .offload import ExpertStore  # local import: offload depends on moe
+
+    if mode != "external":
+        raise ContractError(f"mode {mode!r} is not on the SiDA hot path (external only)")
+    if table is None:
+        raise ContractError("external mode requires a hash table")
+    if store is None:
+        store = ExpertStore.full(model)
+    dev_table = table.on_device(model)
+    if dev_table.n_tokens != batch.num_tokens or table.lengths != batch.lengths:
+        raise ContractError("hash table does not cover the requested tokens")
+    if dev_table.num_layers < model.config.num_layers:
+        raise ContractError(f"missing hash entry for (layer {dev_table.num_layers}, token 0)")
+    lay = BatchLayout(batch.lengths, dev_table.tokens_for(model, batch), model.device)
+    x = model.embed_layout(lay)
+    torch.cuda.current_stream(model.device).wait_event(dev_table.ready)
+    for layer in range(model.config.num_layers):
+        x = model.attention_mix(layer, x, lay)
+        x = store.run_layer(model, layer, x, dev_table)
+    logits = model.pool_classify(x, lay).cpu().numpy().astype(np.float64)
+    trace = ActivationTrace(lengths=batch.lengths, selected=table.ids, alphas=table.alphas,
+                            probs=None)
+    return logits, trace

@@ -1,0 +1,343 @@
+"""Expert residency: the reference planner API over a real HBM slot arena.
+
+Mirrors ref pkg/src/sida/offload.py (`MemoryBudget`, `ResidencyState`,
+`PlanGroup`, `PlacementPlan`, `plan_placement`, `apply_group_inplace`,
+`apply_plan`, `effective_utilization`, `memory_reduction`). Decisions come
+from the native planner (`sida_plan_placement`, csrc/planner.cpp) and are
+identical to the reference's FIFO victim classes; `ExpertStore` executes them
+for real: one HBM arena of ``n_slots`` expert slots, pinned host expert
+images, and `cudaMemcpyAsync` copies on a dedicated copy stream, each
+ordered after the last kernel that read the slot it overwrites (the
+simulated `time.sleep` transfers of ref pipeline.py:141-146 become real
+copies overlapped with the previous layer's compute).
+"""
+
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ContractError, UnservableError
+
+Key = tuple[int, int]  # (layer, expert id)
+
+
+@dataclass
+class MemoryBudget:
+    """ref offload.py:36-46. ``fast_tier_bytes`` is the HBM expert budget;
+    the bandwidth/latency pair only feeds the reported cost model."""
+
+    fast_tier_bytes: int
+    bandwidth_bytes_per_s: float = 16e9
+    per_transfer_latency_s: float = 50e-6
+
+    def __post_init__(self):
+        if self.bandwidth_bytes_per_s <= 0:
+            raise ContractError("bandwidth must be positive")
+        if self.fast_tier_bytes < 0:
+            raise ContractError("fast tier budget must be non-negative")
+
+
+@dataclass
+class ResidencyState:
+    """ref offload.py:49-67."""
+
+    resident: dict = field(default_factory=dict)
+    fifo_order: list = field(default_factory=list)
+    used_bytes: int = 0
+
+    def copy(self) -> "ResidencyState":
+        return ResidencyState(dict(self.resident), list(self.fifo_order), self.used_bytes)
+
+    def fingerprint(self) -> tuple:
+        return (tuple(self.fifo_order), self.used_bytes)
+
+    def check(self) -> None:
+        if sorted(self.fifo_order) != sorted(self.resident):
+            raise ContractError("fifo_order is not a permutation of resident")
+        if self.used_bytes != sum(self.resident.values()):
+            raise ContractError("used_bytes does not match resident sizes")
+
+
+@dataclass
+class PlanGroup:
+    """ref offload.py:70-91."""
+
+    layer: int
+    steps: list
+    prefetchable: bool
+    transfer_s: float
+
+    @property
+    def loads(self) -> list:
+        return [k for op, k in self.steps if op == "load"]
+
+    @property
+    def evictions(self) -> list:
+        return [k for op, k in self.steps if op == "evict"]
+
+
+@dataclass
+class PlacementPlan:
+    """ref offload.py:94-111."""
+
+    groups: list
+    budget_bytes: int
+    expert_bytes: int
+    source_fingerprint: tuple
+
+    @property
+    def loads(self) -> list:
+        return [k for g in self.groups for k in g.loads]
+
+    @property
+    def evictions(self) -> list:
+        return [k for g in self.groups for k in g.evictions]
+
+    @property
+    def estimated_transfer_s(self) -> float:
+        return sum(g.transfer_s for g in self.groups)
+
+
+def plan_placement(table, state: ResidencyState, budget: MemoryBudget,
+                   expert_bytes: int) -> PlacementPlan:
+    """Per-layer load/evict groups (ref offload.py:118-140), computed by the
+    native planner. ``table`` is anything with ``required_by_layer()``."""
+    if expert_bytes > budget.fast_tier_bytes:
+        raise UnservableError(
+            f"expert of {expert_bytes} bytes exceeds budget {budget.fast_tier_bytes}")
+    required = [set(int(e) for e in s) for s in table.required_by_layer()]
+    n_layers = len(required)
+    keys = list(state.fifo_order)
+    if any(state.resident.get(k) != expert_bytes for k in keys) or len(keys) != len(state.resident):
+        raise ContractError("residency state holds experts of another size")
+    max_e = max([e for s in required for e in s] + [k[1] for k in keys] + [0])
+    K = max_e + 1
+    req = np.zeros((max(n_layers, 1), K), dtype=np.uint8)
+    for layer, s in enumerate(required):
+        if s:
+            req[layer, sorted(s)] = 1
+    fifo = np.array([l * K + e for l, e in keys], dtype=np.int32)
+    cap = 2 * n_layers * K + len(keys) + 1
+    steps = np.empty(cap, dtype=np.int32)
+    goff = np.empty(n_layers + 1, dtype=np.int32)
+    pref = np.empty(max(n_layers, 1), dtype=np.uint8)
+    budget_slots = budget.fast_tier_bytes // expert_bytes
+    _lib.check(_lib.load().sida_plan_placement(
+        req.ctypes.data, n_layers, K, int(budget_slots), fifo.ctypes.data, len(keys),
+        steps.ctypes.data, cap, goff.ctypes.data, pref.ctypes.data))
+    groups = []
+    for layer in range(n_layers):
+        raw = steps[goff[layer] : goff[layer + 1]]
+        st = [("load", divmod(int(v), K)) if v >= 0 else ("evict", divmod(int(-v - 1), K))
+              for v in raw]
+        n_loads = int(np.count_nonzero(raw >= 0))
+        groups.append(PlanGroup(
+            layer=layer, steps=st, prefetchable=bool(pref[layer]),
+            transfer_s=n_loads * expert_bytes / budget.bandwidth_bytes_per_s
+            + budget.per_transfer_latency_s * n_loads))
+    return PlacementPlan(groups=groups, budget_bytes=budget.fast_tier_bytes,
+                         expert_bytes=expert_bytes, source_fingerprint=state.fingerprint())
+
+
+def apply_group_inplace(state: ResidencyState, group: PlanGroup, budget_bytes: int,
+                        expert_bytes: int) -> None:
+    """ref offload.py:207-222 (bookkeeping half; copies are ExpertStore's)."""
+    for op, key in group.steps:
+        if op == "evict":
+            if key not in state.resident:
+                raise ContractError(f"plan/state mismatch: evicting non-resident {key}")
+            state.used_bytes -= state.resident.pop(key)
+            state.fifo_order.remove(key)
+        else:
+            if key in state.resident:
+                raise ContractError(f"plan/state mismatch: loading resident {key}")
+            if state.used_bytes + expert_bytes > budget_bytes:
+                raise ContractError("plan exceeds budget mid-application")
+            state.resident[key] = expert_bytes
+            state.fifo_order.append(key)
+            state.used_bytes += expert_bytes
+
+
+def apply_plan(state: ResidencyState, plan: PlacementPlan) -> tuple[ResidencyState, float]:
+    """ref offload.py:225-237."""
+    if plan.source_fingerprint != state.fingerprint():
+        raise ContractError("plan/state mismatch: plan was computed from a different state")
+    new = state.copy()
+    for group in plan.groups:
+        apply_group_inplace(new, group, plan.budget_bytes, plan.expert_bytes)
+    new.check()
+    return new, plan.estimated_transfer_s
+
+
+def effective_utilization(state: ResidencyState, activated: set) -> float:
+    """ref offload.py:281-289."""
+    missing = [k for k in activated if k not in state.resident]
+    if missing:
+        raise ContractError(f"activated experts not resident: {missing[:3]}")
+    if state.used_bytes == 0:
+        return 1.0
+    return sum(state.resident[k] for k in activated) / state.used_bytes
+
+
+def memory_reduction(table, model) -> float:
+    """ref offload.py:292-300."""
+    required = table.required_experts()
+    return 1.0 - len(required) * model.expert_bytes_each() / model.total_expert_bytes()
+
+
+# ------------------------------------------------------------------------------------
+@dataclass
+class Wave:
+    """Experts of one layer computed together: loads to enqueue first, then
+    the FFN over ``experts`` using the expert->slot map ``slot_row``."""
+
+    layer: int
+    loads: list
+    experts: list
+    slot_row: np.ndarray
+
+
+class ExpertStore:
+    """HBM slot arena + pinned expert images + copy stream.
+
+    Slots are assigned lowest-free-first; a load into a slot waits (on the copy
+    stream) for the event recorded after the last FFN that read the slot.
+    """
+
+    _full_cache: dict = {}
+
+    def __init__(self, model, n_slots: int, copy_stream=None):
+        if n_slots < 1:
+            raise UnservableError("budget cannot hold a single expert")
+        self.model = model
+        self.n_slots = int(n_slots)
+        self.slot_stride = model.slot_stride
+        dev = model.device
+        self.arena = torch.empty(self.n_slots * self.slot_stride, dtype=torch.uint8, device=dev)
+        self.base_ptr = self.arena.data_ptr()
+        self.err_flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.copy_stream = copy_stream or torch.cuda.Stream(device=dev)
+        self.slot_of: dict = {}
+        self._free = list(range(self.n_slots))
+        self._reader: list = [None] * self.n_slots
+        self.n_loads = 0
+        self.bytes_loaded = 0
+        self.peak_slots = 0
+
+    @classmethod
+    def full(cls, model) -> "ExpertStore":
+        """One store per model holding every expert (model_forward's default)."""
+        key = id(model)
+        st = cls._full_cache.get(key)
+        if st is None or st.model is not model:
+            c = model.config
+            st = cls(model, c.num_layers * c.num_experts)
+            cls._full_cache[key] = st
+        return st
+
+    @classmethod
+    def for_budget(cls, model, budget: MemoryBudget) -> "ExpertStore":
+        return cls(model, budget.fast_tier_bytes // model.expert_bytes_each())
+
+    # -- bookkeeping --------------------------------------------------------------
+    def take_slot(self, key: Key) -> int:
+        if key in self.slot_of:
+            raise ContractError(f"plan/state mismatch: loading resident {key}")
+        if not self._free:
+            raise ContractError("plan exceeds budget mid-application")
+        slot = heapq.heappop(self._free)
+        self.slot_of[key] = slot
+        self.peak_slots = max(self.peak_slots, len(self.slot_of))
+        return slot
+
+    def free_slot(self, key: Key) -> None:
+        slot = self.slot_of.pop(key, None)
+        if slot is None:
+            raise ContractError(f"plan/state mismatch: evicting non-resident {key}")
+        heapq.heappush(self._free, slot)
+
+    def slot_row(self, layer: int, experts) -> np.ndarray:
+        row = np.full(self.model.config.num_experts, -1, dtype=np.int32)
+        for e in experts:
+            row[e] = self.slot_of[(layer, e)]
+        return row
+
+    # -- copy engine ---------------------------------------------------------------
+    def enqueue_loads(self, loads) -> torch.cuda.Event | None:
+        """H2D copies for [(key, slot)], each after its slot's last reader."""
+        if not loads:
+            return None
+        h = _lib.lib()
+        cs = self.copy_stream
+        for (layer, e), slot in loads:
+            ev = self._reader[slot]
+            if ev is not None:
+                cs.wait_event(ev)
+            src = self.model.expert_image(layer, e)
+            _lib.check(h.sida_expert_copy(self.base_ptr + slot * self.slot_stride, src.data_ptr(),
+                                          self.slot_stride, cs.cuda_stream, None, None))
+            self.n_loads += 1
+            self.bytes_loaded += self.slot_stride
+        done = torch.cuda.Event()
+        done.record(cs)
+        return done
+
+    def mark_read(self, slot_row: np.ndarray, event: torch.cuda.Event) -> None:
+        for s in slot_row[slot_row >= 0]:
+            self._reader[int(s)] = event
+
+    # -- one layer, every required expert resident (model_forward path) ---------------
+    def run_layer(self, model, layer: int, x: torch.Tensor, dev_table, stream=None):
+        st = stream or torch.cuda.current_stream(model.device)
+        table_hist = dev_table.hist
+        dev_table.ready.synchronize()
+        st.wait_event(dev_table.ready)
+        need = [int(e) for e in np.nonzero(table_hist[layer].cpu().numpy())[0]]
+        loads = [((layer, e), self.take_slot((layer, e))) for e in need
+                 if (layer, e) not in self.slot_of]
+        done = self.enqueue_loads(loads)
+        wave = Wave(layer, loads, need, self.slot_row(layer, need))
+        return run_waves(model, [wave], x, dev_table, self, st, pre_done=[done])
+
+
+def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=None,
+              issue=None):
+    """Execute one layer as a sequence of waves on ``stream``: wait for each
+    wave's copies, run the grouped FFN over its experts, record the reader
+    event. ``issue(wave)`` (optional) enqueues a wave's copies just in time and
+    returns their done event."""
+    c = model.config
+    k = dev_table.k
+    layer = waves[0].layer
+    tables = dev_table.layer(layer)
+    out = torch.empty_like(x)
+    y = None
+    if k > 1:
+        y = torch.empty((x.shape[0] * k, c.d_model), dtype=torch.float32, device=x.device)
+    multi = len(waves) > 1
+    for i, wave in enumerate(waves):
+        done = issue(wave) if issue is not None else (pre_done[i] if pre_done else None)
+        if done is not None:
+            stream.wait_event(done)
+        if not wave.experts:
+            continue
+        with torch.cuda.stream(stream):
+            row = torch.from_numpy(wave.slot_row).pin_memory().to(x.device, non_blocking=True)
+            elist = None
+            if multi:
+                elist = torch.from_numpy(np.asarray(wave.experts, dtype=np.int32)).pin_memory().to(
+                    x.device, non_blocking=True)
+            model.moe_apply_rows(tables, x, k, store, row, expert_list=elist, out=out, y=y,
+                                 stream=stream)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        store.mark_read(wave.slot_row, ev)
+    if k > 1:
+        with torch.cuda.stream(stream):
+            out = model.combine(y, x, k, out=out, stream=stream)
+    return out

@@ -1,0 +1,335 @@
+"""SiDA hash function on the GPU: host mirror of the inference half of
+ref pkg/src/sida/predictor.py.
+
+`build_hash_table` keeps the reference signature (ref predictor.py:373) but
+runs every sequence of the batch in one fp64 kernel chain
+(`sida_hash_forward`) and immediately permutes every layer's (token, rank)
+rows by expert (`sida_permute_hist`) on the same stream.
+The resulting `ExpertHashTable` is device-resident; its numpy views
+(`ids`, `alphas`) are fetched lazily -- boundary (iv) of SURVEY §3.
+"""
+
+from __future__ import annotations
+
+import json
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import ContractError
+from .moe import MoEModel, Rng, SequenceBatch
+
+
+@dataclass
+class PredictorConfig:
+    """ref predictor.py:41-58 (training fields kept for API parity)."""
+
+    compress_dim: int = 24
+    lstm_hidden: int = 48
+    lstm_layers: int = 2
+    top_t: int = 30
+    lambda_ce: float = 0.005
+    lr: float = 5e-5
+    batch_size: int = 64
+    max_steps: int = 2000
+
+    def __post_init__(self):
+        if self.lstm_layers != 2:
+            raise ContractError("the predictor trunk is fixed at 2 LSTM layers")
+        if self.top_t < 1:
+            raise ContractError("top_t must be >= 1")
+        if self.lambda_ce < 0:
+            raise ContractError("lambda_ce must be >= 0")
+
+
+PARAM_ORDER = ("compress_w", "compress_b", "lstm1_wx", "lstm1_wh", "lstm1_b", "lstm2_wx",
+               "lstm2_wh", "lstm2_b", "attn_wq", "attn_wk", "attn_wv", "head_w", "head_b")
+
+
+class PredictorNet:
+    """Compress FC -> 2-layer LSTM -> sparsemax attention -> residual -> heads
+    (ref predictor.py:129-164); parameters float64, packed once on the device
+    in the order sida_hash_forward expects (include/sida_b200.h)."""
+
+    def __init__(self, config: PredictorConfig, d_model: int, num_moe_layers: int,
+                 num_experts: int, rng: Rng | None = None, *, params=None):
+        self.config = config
+        self.d_model = d_model
+        self.num_moe_layers = num_moe_layers
+        self.num_experts = num_experts
+        if params is None:
+            params = self._init(rng if rng is not None else Rng(0))
+        self.params = params
+        self._packed = {}
+
+    def _init(self, rng: Rng) -> dict[str, np.ndarray]:
+        cd, hid = self.config.compress_dim, self.config.lstm_hidden
+
+        def xavier(n_in, n_out, shape):
+            return rng.normal(0.0, np.sqrt(2.0 / (n_in + n_out)), shape)
+
+        p = {"compress_w": xavier(self.d_model, cd, (self.d_model, cd)),
+             "compress_b": np.zeros(cd)}
+        for i, n_in in ((1, cd), (2, hid)):
+            s = 1.0 / np.sqrt(hid)
+            p[f"lstm{i}_wx"] = rng.uniform(-s, s, (n_in, 4 * hid))
+            p[f"lstm{i}_wh"] = rng.uniform(-s, s, (hid, 4 * hid))
+            b = np.zeros(4 * hid)
+            b[hid : 2 * hid] = 1.0
+            p[f"lstm{i}_b"] = b
+        for name in ("attn_wq", "attn_wk", "attn_wv"):
+            p[name] = xavier(hid, hid, (hid, hid))
+        p["head_w"] = xavier(hid, self.num_experts,
+                             (self.num_moe_layers, hid, self.num_experts))
+        p["head_b"] = np.zeros((self.num_moe_layers, self.num_experts))
+        return p
+
+    def param_bytes(self) -> int:
+        return sum(v.size for v in self.params.values()) * 8
+
+    def packed(self, device) -> torch.Tensor:
+        key = str(device)
+        if key not in self._packed:
+            flat = np.concatenate([np.ascontiguousarray(self.params[n], dtype=np.float64).ravel()
+                                   for n in PARAM_ORDER])
+            c = self.config
+            want = _lib.load().sida_hash_param_count(self.d_model, c.compress_dim, c.lstm_hidden,
+                                                     self.num_moe_layers, self.num_experts)
+            if flat.size != want:
+                raise ContractError(f"predictor params hold {flat.size} values, expected {want}")
+            self._packed[key] = torch.from_numpy(flat).to(device)
+        return self._packed[key]
+
+
+class DeviceTable:
+    """Device half of an ExpertHashTable: ids/alphas plus the per-layer
+    permutation (hist, off, perm, inv, alpha_perm) and the event after which
+    all of it is valid on any stream."""
+
+    def __init__(self, ids, alpha, alpha_f32, n_tokens, k, tokens=None):
+        self.ids = ids              # int32 (L, N, k)
+        self.alpha = alpha          # float64 (L, N, k)
+        self.alpha_f32 = alpha_f32  # float32 (L, N, k)
+        self.num_layers = ids.shape[0]
+        self.n_tokens = n_tokens
+        self.k = k
+        self.tokens = tokens        # int32 device tokens when built by the GPU hasher
+        self.hist = self.off = self.perm = self.inv = self.alpha_perm = None
+        self.ready = torch.cuda.Event()
+
+    def permute(self, num_experts: int, stream) -> None:
+        h = _lib.lib()
+        L, rows = self.num_layers, self.n_tokens * self.k
+        dev = self.ids.device
+        self.hist = torch.empty((L, num_experts), dtype=torch.int32, device=dev)
+        self.off = torch.empty((L, num_experts + 1), dtype=torch.int32, device=dev)
+        self.perm = torch.empty((L, rows), dtype=torch.int32, device=dev)
+        self.inv = torch.empty((L, rows), dtype=torch.int32, device=dev)
+        self.alpha_perm = torch.empty((L, rows), dtype=torch.float32, device=dev)
+        ws_bytes = h.sida_permute_workspace_bytes(L, rows, num_experts)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        _lib.check(h.sida_permute_hist(
+            self.ids.data_ptr(), L, rows, num_experts, self.alpha_f32.data_ptr(),
+            self.hist.data_ptr(), self.off.data_ptr(), self.perm.data_ptr(), self.inv.data_ptr(),
+            self.alpha_perm.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream))
+        ws.record_stream(stream)
+        self.ready.record(stream)
+
+    def use_on(self, stream) -> None:
+        """Mark the table's buffers as in use on ``stream`` (caching-allocator
+        safety when the table was built on another stream)."""
+        for t in (self.ids, self.alpha, self.alpha_f32, self.hist, self.off, self.perm, self.inv,
+                  self.alpha_perm, self.tokens):
+            if t is not None:
+                t.record_stream(stream)
+
+    def layer(self, layer: int):
+        return self.off[layer], self.perm[layer], self.alpha_perm[layer]
+
+    def tokens_for(self, model: MoEModel, batch: SequenceBatch) -> torch.Tensor:
+        if self.tokens is None:
+            toks = model.validate_tokens(batch)
+            self.tokens = torch.from_numpy(toks).pin_memory().to(model.device, non_blocking=True)
+        return self.tokens
+
+
+class ExpertHashTable:
+    """Predicted (expert id, alpha) per (layer, token) for one batch
+    (ref predictor.py:61-126). Constructed either from numpy arrays (the
+    reference's form) or by the GPU hasher, in which case the arrays live on
+    the device and the numpy views are fetched on first access."""
+
+    def __init__(self, batch_id: int, lengths: list[int], ids=None, alphas=None, *,
+                 device_table: DeviceTable | None = None):
+        self.batch_id = int(batch_id)
+        self.lengths = [int(n) for n in lengths]
+        self._ids = None if ids is None else np.asarray(ids, dtype=np.int64)
+        self._alphas = None if alphas is None else np.asarray(alphas, dtype=np.float64)
+        self._dev = device_table
+        self._hist = None
+        if self._ids is None and self._dev is None:
+            raise ContractError("hash table needs ids or a device table")
+
+    # -- numpy view (boundary iv) ----------------------------------------------------
+    @property
+    def ids(self) -> np.ndarray:
+        if self._ids is None:
+            self._dev.ready.synchronize()
+            self._ids = self._dev.ids.cpu().numpy().astype(np.int64)
+        return self._ids
+
+    @property
+    def alphas(self) -> np.ndarray:
+        if self._alphas is None:
+            self._dev.ready.synchronize()
+            self._alphas = self._dev.alpha.cpu().numpy()
+        return self._alphas
+
+    @property
+    def num_layers(self) -> int:
+        return self._dev.num_layers if self._dev is not None else self._ids.shape[0]
+
+    @property
+    def eval_top_k(self) -> int:
+        return self._dev.k if self._dev is not None else self._ids.shape[2]
+
+    @property
+    def num_tokens(self) -> int:
+        return self._dev.n_tokens if self._dev is not None else self._ids.shape[1]
+
+    def sequence_slice(self, offset: int, t_len: int):
+        if offset + t_len > self.num_tokens:
+            raise ContractError("hash table does not cover the requested tokens")
+        return self.ids[:, offset : offset + t_len], self.alphas[:, offset : offset + t_len]
+
+    def histogram(self) -> np.ndarray:
+        """(L, K) per-layer expert counts (device hist when available)."""
+        if self._hist is None:
+            if self._dev is not None and self._dev.hist is not None:
+                self._dev.ready.synchronize()
+                self._hist = self._dev.hist.cpu().numpy()
+            else:
+                K = int(self.ids.max()) + 1
+                self._hist = np.stack([np.bincount(self.ids[l].ravel(), minlength=K)
+                                       for l in range(self.num_layers)])
+        return self._hist
+
+    def required_experts(self) -> set[tuple[int, int]]:
+        """ref predictor.py:89-94."""
+        return {(l, int(e)) for l, row in enumerate(self.histogram()) for e in np.nonzero(row)[0]}
+
+    def required_by_layer(self) -> list[set[int]]:
+        """ref predictor.py:96-100 (sorted sets of the experts each layer needs)."""
+        return [{int(e) for e in np.nonzero(row)[0]} for row in self.histogram()]
+
+    def to_json(self) -> str:
+        """ref predictor.py:102-112."""
+        entries = []
+        ids, al = self.ids, self.alphas
+        for layer in range(ids.shape[0]):
+            for tok in range(ids.shape[1]):
+                entries.append([layer, tok, [[int(e), float(a)]
+                                             for e, a in zip(ids[layer, tok], al[layer, tok])]])
+        return json.dumps({"batch_id": self.batch_id, "lengths": self.lengths, "entries": entries})
+
+    @classmethod
+    def from_json(cls, text: str) -> "ExpertHashTable":
+        """ref predictor.py:114-126."""
+        obj = json.loads(text)
+        lengths = [int(x) for x in obj["lengths"]]
+        layers = 1 + max(e[0] for e in obj["entries"])
+        k = len(obj["entries"][0][2])
+        ids = np.zeros((layers, sum(lengths), k), dtype=np.int64)
+        alphas = np.zeros((layers, sum(lengths), k))
+        for layer, tok, pairs in obj["entries"]:
+            ids[layer, tok] = [p[0] for p in pairs]
+            alphas[layer, tok] = [p[1] for p in pairs]
+        return cls(int(obj["batch_id"]), lengths, ids, alphas)
+
+    # -- device view -----------------------------------------------------------------
+    def on_device(self, model: MoEModel, stream=None) -> DeviceTable:
+        """The device table (uploading + permuting a host-built table once)."""
+        if self._dev is None:
+            st = stream or torch.cuda.current_stream(model.device)
+            ids = self._ids
+            K = model.config.num_experts
+            if ids.size and (ids.min() < 0 or ids.max() >= K):
+                raise ContractError("expert index out of range")
+            if self._alphas is None or np.any(self._alphas < 0):
+                raise ContractError("scaling factors must be non-negative")
+            with torch.cuda.stream(st):
+                d_ids = torch.from_numpy(ids.astype(np.int32)).to(model.device)
+                d_al = torch.from_numpy(self._alphas).to(model.device)
+                dt = DeviceTable(d_ids, d_al, d_al.float(), ids.shape[1], ids.shape[2])
+                dt.permute(K, st)
+            self._dev = dt
+        return self._dev
+
+
+def build_hash_table(predictor: PredictorNet, batch: SequenceBatch, eval_top_k: int, embed_fn,
+                     stream=None) -> ExpertHashTable:
+    """Top-k expert ids and alphas per (layer, token) (ref predictor.py:373-399).
+
+    ``embed_fn`` is normally ``model.embed`` of a GPU `MoEModel`: the kernel
+    then reads the model's bf16 embedding tables directly. Any other callable
+    is evaluated on the host per sequence and its float64 embeddings are
+    uploaded. Alphas are the raw softmax probabilities at the ids."""
+    if eval_top_k < 1:
+        raise ContractError("eval_top_k must be >= 1")
+    if eval_top_k > predictor.num_experts:
+        raise ContractError(f"k={eval_top_k} out of range for width-{predictor.num_experts} rows")
+    model = getattr(embed_fn, "__self__", None)
+    use_tables = isinstance(model, MoEModel) and getattr(embed_fn, "__name__", "") == "embed"
+    device = model.device if use_tables else torch.device("cuda", torch.cuda.current_device())
+    h = _lib.lib()
+    st = stream or torch.cuda.current_stream(device)
+    lengths = batch.lengths
+    if not lengths or min(lengths) < 1:
+        raise ContractError("empty sequence")
+    n_tok, n_seq, max_len = sum(lengths), len(lengths), max(lengths)
+    c = predictor.config
+    L, K = predictor.num_moe_layers, predictor.num_experts
+    off = np.zeros(n_seq + 1, dtype=np.int32)
+    np.cumsum(lengths, out=off[1:])
+    with torch.cuda.stream(st):
+        seq_off = torch.from_numpy(off).pin_memory().to(device, non_blocking=True)
+        tokens = None
+        emb = None
+        if use_tables:
+            toks = model.validate_tokens(batch)
+            tokens = torch.from_numpy(toks).pin_memory().to(device, non_blocking=True)
+        else:
+            host = np.concatenate([np.asarray(embed_fn(s), dtype=np.float64) for s in batch.sequences])
+            if host.shape != (n_tok, predictor.d_model) or not np.all(np.isfinite(host)):
+                raise ContractError("predictor input must be finite (T, d_model) embeddings")
+            emb = torch.from_numpy(host).to(device)
+        ids = torch.empty((L, n_tok, eval_top_k), dtype=torch.int32, device=device)
+        alpha = torch.empty((L, n_tok, eval_top_k), dtype=torch.float64, device=device)
+        alpha_f32 = torch.empty((L, n_tok, eval_top_k), dtype=torch.float32, device=device)
+        ws_bytes = h.sida_hash_workspace_bytes(n_tok, n_seq, max_len, predictor.d_model,
+                                               c.compress_dim, c.lstm_hidden, L, K)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+        params = predictor.packed(device)
+        _lib.check(h.sida_hash_forward(
+            params.data_ptr(), _lib.ptr(model.tok_emb) if use_tables else None,
+            _lib.ptr(model.pos_emb) if use_tables else None, _lib.ptr(emb), _lib.ptr(tokens),
+            seq_off.data_ptr(), n_seq, n_tok, max_len, predictor.d_model, c.compress_dim,
+            c.lstm_hidden, L, K, eval_top_k, ids.data_ptr(), alpha.data_ptr(),
+            alpha_f32.data_ptr(), ws.data_ptr(), ws_bytes, st.cuda_stream))
+        dt = DeviceTable(ids, alpha, alpha_f32, n_tok, eval_top_k, tokens=tokens)
+        dt.permute(K, st)
+    return ExpertHashTable(batch.batch_id, lengths, device_table=dt)
+
+
+class PredictorHasher:
+    """Binds a predictor to an embedding source (ref predictor.py:402-410)."""
+
+    def __init__(self, predictor: PredictorNet, embed_fn, stream=None):
+        self.predictor = predictor
+        self.embed_fn = embed_fn
+        self.stream = stream
+
+    def build_table(self, batch: SequenceBatch, eval_top_k: int) -> ExpertHashTable:
+        return build_hash_table(self.predictor, batch, eval_top_k, self.embed_fn, self.stream)

@@ -1,0 +1,303 @@
+"""GPU parity of the hot-path kernels against the oracle (run on a B200).
+
+Bars (BASELINE.json north star): ids and permutation indices bit-exact;
+bf16 layer outputs within rtol 2e-2 and the fp32 check path within 1e-4 of
+the float64 oracle, both with an absolute floor of the same fraction of the
+output's RMS (written per test below).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from oracle import moe as omoe
+from oracle import permute as operm
+from oracle import predictor as opred
+
+pytestmark = pytest.mark.gpu
+
+
+def _lib():
+    from paper_2310_18859_b200 import _lib
+
+    return _lib, _lib.lib()
+
+
+def close_rms(got, ref, rtol):
+    """|got - ref| <= rtol * |ref| + rtol * rms(ref), elementwise."""
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    rms = float(np.sqrt(np.mean(ref ** 2))) or 1.0
+    err = np.abs(got - ref) - rtol * np.abs(ref)
+    worst = float(err.max() / rms)
+    assert worst <= rtol, f"max excess error {worst:.3e} * rms > rtol {rtol}"
+
+
+# ----------------------------------------------------------------------------- permute
+def _permute_gpu(ids_np, K):
+    from paper_2310_18859_b200.predictor import DeviceTable
+
+    L, N, k = ids_np.shape
+    dev = torch.device("cuda")
+    ids = torch.from_numpy(ids_np.astype(np.int32)).to(dev)
+    alpha = torch.rand((L, N, k), dtype=torch.float64, device=dev)
+    dt = DeviceTable(ids, alpha, alpha.float(), N, k)
+    dt.permute(K, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    return dt
+
+
+@pytest.mark.parametrize("L,N,k,K,skew", [
+    (1, 1, 1, 1, 0.0), (2, 1, 3, 4, 0.0), (2, 37, 1, 8, 0.0), (3, 1000, 2, 8, 3.0),
+    (12, 8192, 1, 128, 1.5), (2, 5000, 3, 256, 0.0), (1, 4096 * 3 + 17, 1, 7, 0.5),
+    (2, 20000, 1, 1, 0.0)])
+def test_permute_hist_bit_exact(cuda_device, L, N, k, K, skew):
+    g = np.random.default_rng(L * 1000 + N + K)
+    if skew > 0:
+        p = 1.0 / np.arange(1, K + 1) ** skew
+        ids = g.choice(K, size=(L, N, k), p=p / p.sum())
+    else:
+        ids = g.integers(0, K, size=(L, N, k))
+    dt = _permute_gpu(ids, K)
+    hist, off, perm, inv = operm.permute_all(ids, K)
+    np.testing.assert_array_equal(dt.hist.cpu().numpy(), hist)
+    np.testing.assert_array_equal(dt.off.cpu().numpy(), off)
+    np.testing.assert_array_equal(dt.perm.cpu().numpy(), perm)
+    np.testing.assert_array_equal(dt.inv.cpu().numpy(), inv)
+    ap = dt.alpha_perm.cpu().numpy()
+    af = dt.alpha_f32.reshape(L, -1).cpu().numpy()
+    np.testing.assert_array_equal(ap, np.take_along_axis(af, perm, axis=1))
+
+
+def test_permute_matches_reference_fixture(cuda_device):
+    g = load_golden("c0")
+    ids = g["ids_k1"]
+    dt = _permute_gpu(ids, 8)
+    for layer in range(ids.shape[0]):
+        np.testing.assert_array_equal(dt.perm[layer].cpu().numpy(), g[f"perm_k1_l{layer}"])
+        np.testing.assert_array_equal(dt.hist[layer].cpu().numpy(), g[f"hist_k1_l{layer}"])
+
+
+def test_permute_max_size_properties(cuda_device):
+    """C4 maximum: 262,144 tokens x 12 layers, K=256 -- size-independent
+    properties (stable sortedness, inverse, histogram sum)."""
+    L, N, K = 12, 262144, 256
+    ids = torch.randint(0, K, (L, N, 1), device="cuda", dtype=torch.int32)
+    from paper_2310_18859_b200.predictor import DeviceTable
+
+    a = torch.rand((L, N, 1), device="cuda", dtype=torch.float64)
+    dt = DeviceTable(ids, a, a.float(), N, 1)
+    dt.permute(K, torch.cuda.current_stream())
+    flat = ids.reshape(L, N).long()
+    perm = dt.perm.long()
+    e_sorted = torch.gather(flat, 1, perm)
+    key = e_sorted * N + perm  # stable order <=> strictly increasing (expert, row)
+    assert bool((key[:, 1:] > key[:, :-1]).all())
+    ar = torch.arange(N, device="cuda").expand(L, N)
+    assert bool((torch.gather(dt.inv.long(), 1, perm) == ar).all())
+    assert bool((dt.off[:, -1] == N).all())
+    ref_hist = torch.stack([torch.bincount(flat[l], minlength=K) for l in range(L)])
+    assert bool((dt.hist.long() == ref_hist).all())
+
+
+def test_gather_rows(cuda_device):
+    _l, h = _lib()
+    N, k, d = 3000, 2, 768
+    x = torch.randn(N, d, device="cuda")
+    perm = torch.randperm(N * k, device="cuda", dtype=torch.int64).int()
+    out = torch.empty((N * k, d), dtype=torch.bfloat16, device="cuda")
+    _l.check(h.sida_gather_rows_bf16(x.data_ptr(), perm.data_ptr(), N * k, k, d, out.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream))
+    ref = x[perm.long() // k].bfloat16()
+    assert torch.equal(out, ref)
+
+
+# ------------------------------------------------------------------------ expert FFN
+def _moe_setup(d, hdim, K, L=1, seed=0):
+    from paper_2310_18859_b200.moe import MoEConfig, MoEModel
+
+    shape = omoe.MoEShape(vocab_size=64, d_model=d, num_layers=L, num_experts=K,
+                          expert_hidden=hdim, max_seq_len=16)
+    params = omoe.bf16_params(omoe.init_params(shape, seed))
+    # non-zero biases so the epilogue bias path is exercised
+    g = np.random.default_rng(seed + 1)
+    for l in range(L):
+        params[f"block{l}.b1"] = omoe.round_bf16(g.normal(0, 0.05, (K, hdim)))
+        params[f"block{l}.b2"] = omoe.round_bf16(g.normal(0, 0.05, (K, d)))
+    cfg = MoEConfig(**shape.__dict__)
+    model = MoEModel(cfg, params=params)
+    return shape, params, model
+
+
+def _ids_for(N, k, K, g, skew=True):
+    if k == 1 and skew:
+        p = 1.0 / np.arange(1, K + 1) ** 1.2
+        p[K // 2] = 0.0  # one empty expert
+        ids = g.choice(K, size=(1, N, 1), p=p / p.sum())
+        ids[0, 0, 0] = K // 2 if K > 2 else ids[0, 0, 0]  # ... holding exactly one row
+        return ids
+    return np.stack([np.stack([g.permutation(K)[:k] for _ in range(N)])])[None][0]
+
+
+@pytest.mark.parametrize("d,hdim,K,N,k", [
+    (64, 128, 4, 300, 1), (256, 1024, 8, 1024, 1), (768, 3072, 8, 2048, 1),
+    (128, 256, 8, 700, 2), (768, 3072, 4, 257, 3)])
+def test_grouped_ffn_bf16_vs_oracle(cuda_device, d, hdim, K, N, k):
+    from paper_2310_18859_b200.offload import ExpertStore
+    from paper_2310_18859_b200.predictor import ExpertHashTable
+
+    shape, params, model = _moe_setup(d, hdim, K)
+    g = np.random.default_rng(d + N)
+    ids = _ids_for(N, k, K, g)
+    alphas = g.uniform(0.05, 1.0, size=ids.shape)
+    x = g.normal(0, 1.0, (N, d))
+    table = ExpertHashTable(0, [N], ids, alphas)
+    dt = table.on_device(model)
+    store = ExpertStore.full(model)
+    xt = torch.from_numpy(x).float().cuda()
+    out = store.run_layer(model, 0, xt, dt).cpu().numpy()
+    ref = omoe.moe_apply_grouped(params, 0, x.astype(np.float32).astype(np.float64), ids[0],
+                                 alphas[0])
+    close_rms(out, ref, 2e-2)
+    # the FFN part alone (out - x) must also meet the bar
+    close_rms(out - x.astype(np.float32), ref - x.astype(np.float32), 2e-2)
+    assert store.err_flag.item() == 0
+
+
+@pytest.mark.parametrize("d,hdim,K,N,k", [(32, 64, 8, 300, 1), (256, 1024, 8, 513, 2)])
+def test_grouped_ffn_f32_check_path(cuda_device, d, hdim, K, N, k):
+    _l, h = _lib()
+    shape = omoe.MoEShape(vocab_size=8, d_model=d, num_layers=1, num_experts=K,
+                          expert_hidden=hdim, max_seq_len=4)
+    params = omoe.bf16_params(omoe.init_params(shape, 3))
+    g = np.random.default_rng(5)
+    ids = _ids_for(N, k, K, g)
+    alphas = g.uniform(0.05, 1.0, size=ids.shape)
+    x = g.normal(0, 1.0, (N, d)).astype(np.float32).astype(np.float64)
+    hist, off, perm, inv = operm.permute_layer(ids[0], K)
+    dev = "cuda"
+    xp = torch.from_numpy(x[perm // k]).float().to(dev)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).float().to(dev)  # noqa: E731
+    w1, b1, w2, b2 = (t(params[f"block0.{n}"]) for n in ("w1", "b1", "w2", "b2"))
+    rows = N * k
+    y = torch.empty((rows, d), device=dev)
+    hid = torch.empty((rows, hdim), device=dev)
+    ap = t(alphas[0].reshape(-1)[perm])
+    pm = torch.from_numpy(perm.astype(np.int32)).to(dev)
+    offt = torch.from_numpy(off.astype(np.int32)).to(dev)
+    xt = t(x)
+    s = torch.cuda.current_stream().cuda_stream
+    _l.check(h.sida_grouped_ffn_f32(xp.data_ptr(), rows, d, hdim, offt.data_ptr(), K,
+                                    w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
+                                    pm.data_ptr(), ap.data_ptr(), None, y.data_ptr(),
+                                    hid.data_ptr(), s))
+    out = torch.empty((N, d), device=dev)
+    _l.check(h.sida_combine_ranks(y.data_ptr(), xt.data_ptr(), N, k, d, out.data_ptr(), s))
+    ref = omoe.moe_apply_grouped(params, 0, x, ids[0], alphas[0])
+    close_rms(out.cpu().numpy(), ref, 1e-4)
+
+
+def test_ffn_rejects_nonresident_expert(cuda_device):
+    """An expert with rows but no slot raises the device error flag."""
+    from paper_2310_18859_b200.offload import ExpertStore, Wave, run_waves
+    from paper_2310_18859_b200.predictor import ExpertHashTable
+
+    shape, params, model = _moe_setup(64, 128, 4)
+    ids = np.zeros((1, 10, 1), dtype=np.int64)
+    dt = ExpertHashTable(0, [10], ids, np.ones(ids.shape)).on_device(model)
+    store = ExpertStore(model, 2)
+    wave = Wave(0, [], [0], np.full(4, -1, dtype=np.int32))
+    x = torch.zeros((10, 64), device="cuda")
+    torch.cuda.current_stream().wait_event(dt.ready)
+    run_waves(model, [wave], x, dt, store, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert store.err_flag.item() == 1
+
+
+# ------------------------------------------------------------------------------- hash
+def _hash_fixture(name):
+    import json
+    import os
+
+    from conftest import GOLDEN
+    from paper_2310_18859_b200.moe import MoEConfig, MoEModel, SequenceBatch
+    from paper_2310_18859_b200.predictor import PredictorConfig, PredictorNet
+
+    meta = json.load(open(os.path.join(GOLDEN, name + ".json")))
+    cfg = MoEConfig(**meta["config"])
+    shape = omoe.MoEShape(**meta["config"])
+    params = omoe.bf16_params(omoe.init_params(shape, 0))
+    model = MoEModel(cfg, params=params)
+    pcfg = PredictorConfig(**meta["predictor"])
+    pshape = opred.PredictorShape(cfg.d_model, cfg.num_layers, cfg.num_experts, **meta["predictor"])
+    net = PredictorNet(pcfg, cfg.d_model, cfg.num_layers, cfg.num_experts,
+                       params=opred.init_params(pshape, 1))
+    g = load_golden(name)
+    seqs = np.split(g["tokens"], np.cumsum(g["lengths"])[:-1])
+    return meta, model, net, SequenceBatch(0, list(seqs)), g, params, shape
+
+
+@pytest.mark.parametrize("name", ["tiny", "c0"])
+def test_hash_ids_bit_exact_vs_reference_fixture(cuda_device, name):
+    from paper_2310_18859_b200.predictor import build_hash_table
+
+    meta, model, net, batch, g, _, _ = _hash_fixture(name)
+    for k in meta["ks"]:
+        table = build_hash_table(net, batch, k, model.embed)
+        np.testing.assert_array_equal(table.ids, g[f"ids_k{k}"])
+        np.testing.assert_allclose(table.alphas, g[f"alphas_k{k}"], rtol=1e-12, atol=0)
+
+
+def test_hash_with_callable_embed_fn(cuda_device):
+    """A non-model embed_fn (ref tests use lambdas) goes through the f64 upload path."""
+    from paper_2310_18859_b200.moe import SequenceBatch
+    from paper_2310_18859_b200.predictor import PredictorConfig, PredictorNet, build_hash_table
+
+    pshape = opred.PredictorShape(6, 2, 5, compress_dim=4, lstm_hidden=8)
+    pp = opred.init_params(pshape, 2)
+    net = PredictorNet(PredictorConfig(compress_dim=4, lstm_hidden=8), 6, 2, 5, params=pp)
+    rows = {t: np.random.default_rng(t).normal(0, 1, 6) for t in range(6)}
+    embed = lambda toks: np.stack([rows[int(t)] for t in toks])  # noqa: E731
+    seqs = [np.array([1, 2, 3]), np.array([5]), np.array([0, 4, 4, 2, 1, 3, 5])]
+    table = build_hash_table(net, SequenceBatch(3, seqs), 3, embed)
+    ids, al = opred.build_hash_table(pp, seqs, 3, embed)
+    np.testing.assert_array_equal(table.ids, ids)
+    np.testing.assert_allclose(table.alphas, al, rtol=1e-12)
+    np.testing.assert_allclose(table.alphas.sum(axis=2), 1.0, atol=1e-9)  # full width
+
+
+@pytest.mark.parametrize("L,K,T,B,k", [(12, 128, 128, 6, 1), (12, 8, 96, 4, 2), (2, 256, 512, 2, 3)])
+def test_hash_ids_bit_exact_vs_oracle_switch_shapes(cuda_device, L, K, T, B, k):
+    """Switch-base predictor heads (K = 8 / 128 / 256, 12 layers), up to T=512."""
+    from paper_2310_18859_b200.moe import MoEConfig, MoEModel, SequenceBatch
+    from paper_2310_18859_b200.predictor import PredictorConfig, PredictorNet, build_hash_table
+
+    d = 768
+    cfg = MoEConfig(vocab_size=1000, d_model=d, num_layers=L, num_experts=K, expert_hidden=64,
+                    max_seq_len=T)
+    g = torch.Generator().manual_seed(L * K)
+    tok = (torch.randn(cfg.vocab_size, d, generator=g) / np.sqrt(d)).double().numpy()
+    pos = (torch.randn(T, d, generator=g) / np.sqrt(d)).double().numpy()
+    params = {"tok_emb": omoe.round_bf16(tok), "pos_emb": omoe.round_bf16(pos),
+              "wc": np.zeros((d, 4))}
+    for l in range(L):
+        for n in ("wq", "wk", "wv", "wo"):
+            params[f"block{l}.{n}"] = np.zeros((d, d))
+        params[f"block{l}.w_r"] = np.zeros((d, K))
+        params[f"block{l}.w1"] = np.zeros((K, d, 64))
+        params[f"block{l}.b1"] = np.zeros((K, 64))
+        params[f"block{l}.w2"] = np.zeros((K, 64, d))
+        params[f"block{l}.b2"] = np.zeros((K, d))
+    model = MoEModel(cfg, params=params)
+    pshape = opred.PredictorShape(d, L, K)
+    pp = opred.init_params(pshape, 7)
+    net = PredictorNet(PredictorConfig(), d, L, K, params=pp)
+    rng = np.random.default_rng(9)
+    lens = [T] + [int(rng.integers(1, T + 1)) for _ in range(B - 1)]
+    seqs = [rng.integers(0, cfg.vocab_size, size=n) for n in lens]
+    table = build_hash_table(net, SequenceBatch(0, seqs), k, model.embed)
+    emb = lambda t: params["tok_emb"][t] + params["pos_emb"][: len(t)]  # noqa: E731
+    ids, al = opred.build_hash_table(pp, seqs, k, emb)
+    mism = int((table.ids != ids).sum())
+    assert mism == 0, f"{mism} id mismatches"
+    np.testing.assert_allclose(table.alphas, al, rtol=1e-11)

@@ -1,0 +1,104 @@
+"""Native residency planner (csrc/planner.cpp via offload.plan_placement)
+against the reference's own plans (tests/golden/planner.json) and against the
+oracle restatement on randomized multi-batch workloads (ref
+tests/test_offload.py:150-170 style, state-for-state)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import offload as ooff
+from paper_2310_18859_b200.errors import ContractError, UnservableError
+from paper_2310_18859_b200.offload import (
+    MemoryBudget,
+    ResidencyState,
+    apply_plan,
+    effective_utilization,
+    plan_placement,
+)
+
+
+class FakeTable:
+    def __init__(self, layers):
+        self.layers = [set(s) for s in layers]
+
+    def required_by_layer(self):
+        return self.layers
+
+    def required_experts(self):
+        return {(l, e) for l, s in enumerate(self.layers) for e in s}
+
+
+def test_replays_reference_plans():
+    cases = json.load(open(os.path.join(GOLDEN, "planner.json")))
+    for case in cases:
+        eb = case["expert_bytes"]
+        budget = MemoryBudget(case["slots"] * eb, bandwidth_bytes_per_s=case["bandwidth"],
+                              per_transfer_latency_s=case["latency"])
+        state = ResidencyState()
+        for b in case["batches"]:
+            plan = plan_placement(FakeTable(b["required"]), state, budget, eb)
+            assert len(plan.groups) == len(b["groups"])
+            for mine, ref in zip(plan.groups, b["groups"]):
+                assert [[op, list(k)] for op, k in mine.steps] == ref["steps"]
+                assert mine.prefetchable == ref["prefetchable"]
+                assert mine.transfer_s == pytest.approx(ref["transfer_s"], rel=1e-12)
+            state, secs = apply_plan(state, plan)
+            assert secs == pytest.approx(b["seconds"], rel=1e-12)
+            assert [list(k) for k in state.fifo_order] == b["fifo_after"]
+
+
+def test_random_workload_matches_oracle_state_for_state():
+    g = np.random.default_rng(11)
+    eb = 7
+    for trial in range(60):
+        L, K = int(g.integers(1, 6)), int(g.integers(1, 12))
+        slots = int(g.integers(1, L * K + 3))
+        budget = MemoryBudget(slots * eb)
+        state = ResidencyState()
+        res, fifo, used = {}, [], 0
+        for _ in range(int(g.integers(1, 20))):
+            req = [set(g.integers(0, K, size=int(g.integers(0, K + 1))).tolist()) for _ in range(L)]
+            plan = plan_placement(FakeTable(req), state, budget, eb)
+            ref = ooff.plan(req, res, fifo, used, slots * eb, eb)
+            assert [g_.steps for g_ in plan.groups] == [r["steps"] for r in ref]
+            assert [g_.prefetchable for g_ in plan.groups] == [r["prefetchable"] for r in ref]
+            for r in ref:
+                used = ooff.apply_group(res, fifo, used, r, slots * eb, eb)
+            state, _ = apply_plan(state, plan)
+            assert state.fifo_order == fifo
+            assert state.used_bytes <= slots * eb
+
+
+def test_full_budget_never_evicts():
+    req = [{0, 1, 2}, {0, 3}, {1}]
+    plan = plan_placement(FakeTable(req), ResidencyState(), MemoryBudget(100 * 10), 10)
+    assert plan.evictions == [] and len(plan.loads) == 6
+
+
+def test_within_layer_swap_is_not_prefetchable():
+    plan = plan_placement(FakeTable([{0, 1, 2}]), ResidencyState(), MemoryBudget(20), 10)
+    assert plan.groups[0].prefetchable is False
+    assert plan.evictions == [(0, 0)]
+
+
+def test_unservable_and_contract_errors():
+    with pytest.raises(UnservableError):
+        plan_placement(FakeTable([{0}]), ResidencyState(), MemoryBudget(5), 10)
+    state = ResidencyState({(0, 1): 3}, [(0, 1)], 3)
+    with pytest.raises(ContractError):
+        plan_placement(FakeTable([{0}]), state, MemoryBudget(100), 10)
+    plan = plan_placement(FakeTable([{0}]), ResidencyState(), MemoryBudget(100), 10)
+    other = ResidencyState({(0, 5): 10}, [(0, 5)], 10)
+    with pytest.raises(ContractError):
+        apply_plan(other, plan)
+
+
+def test_effective_utilization():
+    state = ResidencyState({(0, 1): 10, (0, 2): 10}, [(0, 1), (0, 2)], 20)
+    assert effective_utilization(state, {(0, 1)}) == 0.5
+    with pytest.raises(ContractError):
+        effective_utilization(state, {(1, 1)})
