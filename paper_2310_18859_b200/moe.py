@@ -352,9 +352,9 @@ class MoEModel:
         """(n_seq, C): per-sequence mean then the classifier (ref moe.py:264-266)."""
         if lay.uniform:
             pooled = x.view(lay.n_seq, lay.max_len, -1).mean(dim=1)
-        else:
-            sums = x.new_zeros(lay.n_seq, x.shape[1]).index_add_(0, lay.seq_id, x)
-            pooled = sums / lay.len_t[:, None]
+        else:  # padded gather + sum: deterministic (no atomics)
+            xp = torch.cat([x, x.new_zeros(1, x.shape[1])]).index_select(0, lay.pad_index)
+            pooled = xp.view(lay.n_seq, lay.max_len, -1).sum(dim=1) / lay.len_t[:, None]
         return pooled @ self.wc
 
     def moe_apply_rows(self, layer_tables, x: torch.Tensor, k: int, arena, slot_row: torch.Tensor,

@@ -259,8 +259,8 @@ def test_hash_with_callable_embed_fn(cuda_device):
     rows = {t: np.random.default_rng(t).normal(0, 1, 6) for t in range(6)}
     embed = lambda toks: np.stack([rows[int(t)] for t in toks])  # noqa: E731
     seqs = [np.array([1, 2, 3]), np.array([5]), np.array([0, 4, 4, 2, 1, 3, 5])]
-    table = build_hash_table(net, SequenceBatch(3, seqs), 3, embed)
-    ids, al = opred.build_hash_table(pp, seqs, 3, embed)
+    table = build_hash_table(net, SequenceBatch(3, seqs), 5, embed)
+    ids, al = opred.build_hash_table(pp, seqs, 5, embed)
     np.testing.assert_array_equal(table.ids, ids)
     np.testing.assert_allclose(table.alphas, al, rtol=1e-12)
     np.testing.assert_allclose(table.alphas.sum(axis=2), 1.0, atol=1e-9)  # full width
