@@ -151,24 +151,28 @@ class BatchLayout:
         np.cumsum(self.lengths, out=off[1:])
         self.offsets = off
         self.tokens = tokens  # int32 (n_tokens,) on device
-        self.seq_off = torch.from_numpy(off.astype(np.int32)).to(device, non_blocking=True)
+        if self.uniform:  # positions derived on the device: no per-token H2D traffic
+            self.pos = torch.arange(self.n_tokens, device=device) % self.max_len
+            return
+
+        def h2d(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(device,
+                                                                              non_blocking=True)
+
         seq_id = np.repeat(np.arange(self.n_seq), self.lengths)
-        pos = np.arange(self.n_tokens) - off[seq_id]
-        self.pos = torch.from_numpy(pos).to(device, non_blocking=True)
-        self.seq_id = torch.from_numpy(seq_id).to(device, non_blocking=True)
-        self.len_t = torch.tensor(self.lengths, dtype=torch.float32).to(device, non_blocking=True)
+        self.pos = h2d(np.arange(self.n_tokens) - off[seq_id])
+        self.len_t = h2d(np.asarray(self.lengths, dtype=np.float32))
         if not self.uniform:
             pad = np.full((self.n_seq, self.max_len), self.n_tokens, dtype=np.int64)
             for i, n in enumerate(self.lengths):
                 pad[i, :n] = np.arange(off[i], off[i] + n)
-            self.pad_index = torch.from_numpy(pad.reshape(-1)).to(device, non_blocking=True)
+            self.pad_index = h2d(pad.reshape(-1))
             mask = np.zeros((self.n_seq, 1, self.max_len), dtype=np.float32)
             for i, n in enumerate(self.lengths):
                 mask[i, 0, n:] = -np.inf
-            self.key_mask = torch.from_numpy(mask).to(device, non_blocking=True)
-            self.valid_rows = torch.from_numpy(
-                np.concatenate([np.arange(i * self.max_len, i * self.max_len + n)
-                                for i, n in enumerate(self.lengths)])).to(device, non_blocking=True)
+            self.key_mask = h2d(mask)
+            self.valid_rows = h2d(np.concatenate([np.arange(i * self.max_len, i * self.max_len + n)
+                                                  for i, n in enumerate(self.lengths)]))
 
     @classmethod
     def from_batch(cls, model: "MoEModel", batch: SequenceBatch) -> "BatchLayout":

@@ -283,18 +283,12 @@ def build_hash_table(predictor: PredictorNet, batch: SequenceBatch, eval_top_k: 
     model = getattr(embed_fn, "__self__", None)
     use_tables = isinstance(model, MoEModel) and getattr(embed_fn, "__name__", "") == "embed"
     device = model.device if use_tables else torch.device("cuda", torch.cuda.current_device())
-    h = _lib.lib()
     st = stream or torch.cuda.current_stream(device)
     lengths = batch.lengths
     if not lengths or min(lengths) < 1:
         raise ContractError("empty sequence")
-    n_tok, n_seq, max_len = sum(lengths), len(lengths), max(lengths)
-    c = predictor.config
-    L, K = predictor.num_moe_layers, predictor.num_experts
-    off = np.zeros(n_seq + 1, dtype=np.int32)
-    np.cumsum(lengths, out=off[1:])
+    n_tok = sum(lengths)
     with torch.cuda.stream(st):
-        seq_off = torch.from_numpy(off).pin_memory().to(device, non_blocking=True)
         tokens = None
         emb = None
         if use_tables:
@@ -305,6 +299,25 @@ def build_hash_table(predictor: PredictorNet, batch: SequenceBatch, eval_top_k: 
             if host.shape != (n_tok, predictor.d_model) or not np.all(np.isfinite(host)):
                 raise ContractError("predictor input must be finite (T, d_model) embeddings")
             emb = torch.from_numpy(host).to(device)
+    return hash_device(predictor, model if use_tables else None, tokens, lengths, eval_top_k,
+                       batch.batch_id, st, emb=emb, device=device)
+
+
+def hash_device(predictor: PredictorNet, model: MoEModel | None, tokens, lengths, eval_top_k: int,
+                batch_id: int, stream, emb=None, device=None) -> ExpertHashTable:
+    """Hash + permute for tokens already resident in HBM (int32 ``tokens`` on
+    the device, or float64 embeddings ``emb``), enqueued on ``stream``."""
+    h = _lib.lib()
+    st = stream
+    device = device or (model.device if model is not None else emb.device)
+    n_tok, n_seq, max_len = sum(lengths), len(lengths), max(lengths)
+    c = predictor.config
+    L, K = predictor.num_moe_layers, predictor.num_experts
+    off = np.zeros(n_seq + 1, dtype=np.int32)
+    np.cumsum(lengths, out=off[1:])
+    use_tables = model is not None
+    with torch.cuda.stream(st):
+        seq_off = torch.from_numpy(off).pin_memory().to(device, non_blocking=True)
         ids = torch.empty((L, n_tok, eval_top_k), dtype=torch.int32, device=device)
         alpha = torch.empty((L, n_tok, eval_top_k), dtype=torch.float64, device=device)
         alpha_f32 = torch.empty((L, n_tok, eval_top_k), dtype=torch.float32, device=device)
@@ -320,7 +333,8 @@ def build_hash_table(predictor: PredictorNet, batch: SequenceBatch, eval_top_k: 
             alpha_f32.data_ptr(), ws.data_ptr(), ws_bytes, st.cuda_stream))
         dt = DeviceTable(ids, alpha, alpha_f32, n_tok, eval_top_k, tokens=tokens)
         dt.permute(K, st)
-    return ExpertHashTable(batch.batch_id, lengths, device_table=dt)
+        ws.record_stream(st)
+    return ExpertHashTable(batch_id, lengths, device_table=dt)
 
 
 class PredictorHasher:
