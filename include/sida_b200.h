@@ -114,6 +114,12 @@ int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h, cons
                           const int32_t* row_map, const float* alpha, const float* resid,
                           float* out, uint16_t* hidden, int32_t* err_flag, void* stream);
 
+/* Observability: per-CTA cycle counters of the last sida_grouped_ffn_bf16
+ * call when the process runs with SIDA_GEMM_PROF=1 (producer wait, MMA wait
+ * on epilogue / on TMA, MMA loop, epilogue wait, epilogue loop, tiles).
+ * out: uint64 [2 GEMMs][148 CTAs][8]. Synchronises the device. */
+int sida_debug_gemm_prof(unsigned long long* out);
+
 /* fp32 FMA check path: same contraction with float32 weights in the
  * reference layout w1 (K,d,h), b1 (K,h), w2 (K,h,d), b2 (K,d); x_perm
  * float32; hidden float32 workspace (n_rows, h). */

@@ -4,21 +4,32 @@
 // (GEMM2) epilogues fused. Replaces ref moe.py:235-262 (moe_apply), whose
 // per-token gathered einsum is the reference's dominant cost.
 //
-// One launch = one GEMM over every (expert, 128-row tile, BN-col tile) of a
-// layer. Rows are the permuted (token, rank) rows of sida_permute_hist, so
-// each expert's rows are contiguous: tile (e, m) covers rows
-// off[e] + 128m ... The B operand (W1^T or W2^T) is addressed in the HBM
-// slot arena through a 3-D tensor map (k, n, slot) -- the residency engine
-// moves experts between slots without rebuilding descriptors.
+// One launch = one GEMM over every (expert, row tile, BN-col tile) of a layer.
+// Rows are the permuted (token, rank) rows of sida_permute_hist, so each
+// expert's rows are contiguous: tile (e, m) covers rows off[e] + TM*m ... The
+// B operand (W1^T or W2^T) is addressed in the HBM slot arena through a 3-D
+// tensor map (k, n, slot): the residency engine moves experts between slots
+// without rebuilding descriptors.
 //
-// CTA = 6 warps:  warp 0  TMA producer (one elected lane)
-//                 warp 1  TMEM allocator + MMA issuer (one elected lane)
-//                 warps 2-5 epilogue: TMEM -> registers -> global
-// Pipelines: smem ring of kStages {A,B} stages (full/empty mbarriers),
-// double-buffered TMEM accumulator (tmem_full/tmem_empty mbarriers) so the
-// epilogue of tile i overlaps the MMAs of tile i+1.
+// Two CTA-group modes (template CG):
+//   CG=1  one CTA per 128-row tile (small per-expert row counts)
+//   CG=2  a CTA pair (cluster of 2 on one TPC) per 256-row tile:
+//         tcgen05.mma.cta_group::2 (M=256) issued by the leader CTA, each CTA
+//         TMA-loading its own 128 rows of A and half of the B tile, so per SM
+//         the smem fill per MMA is 2/3 of CG=1 and the L2 reads of B halve.
+//
+// CTA = 10 warps: warp 0    TMA producer (one elected lane)
+//                 warp 1    TMEM allocator + MMA issuer (one lane, leader CTA)
+//                 warps 2-9 epilogue, two per TMEM lane quarter (each half of
+//                           the tile's columns): TMEM -> registers -> swizzled
+//                           smem transpose -> coalesced global stores
+// Pipelines: smem ring of {A,B} stages (full/empty mbarriers); double-buffered
+// TMEM accumulator (tmem_full/tmem_empty) so the epilogue of tile i overlaps
+// the MMAs of tile i+1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -27,12 +38,30 @@
 namespace sida {
 namespace sm100 {
 
-constexpr int BM = 128;       // UMMA M (cta_group::1), one TMEM lane per row
+constexpr int BM = 128;       // rows per CTA (one TMEM lane per row)
 constexpr int BK = 64;        // 64 bf16 = 128 B = one SWIZZLE_128B row
 constexpr int UMMA_K = 16;    // K per tcgen05.mma for kind::f16
-constexpr int kStages = 4;
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kMaxListed = 512;
+constexpr int kSmemBudget = 222 * 1024;
+
+// Per-warp epilogue staging tile: 32 rows x 32 columns of the output type.
+template <int STAGE>
+__host__ __device__ constexpr int stage_tile_bytes() { return 32 * 32 * (STAGE == 1 ? 2 : 4); }
+
+template <int BN, int STAGE, int CG>
+__host__ __device__ constexpr int stages_for() {
+  return (kSmemBudget - 1024 - kEpiWarps * stage_tile_bytes<STAGE>() - 8 * 1024) /
+                     (BM * BK * 2 + (BN / CG) * BK * 2) > 8
+             ? 8
+             : (kSmemBudget - 1024 - kEpiWarps * stage_tile_bytes<STAGE>() - 8 * 1024) /
+                   (BM * BK * 2 + (BN / CG) * BK * 2);
+}
+
+__host__ __device__ constexpr uint32_t pow2_cols(uint32_t c) {
+  return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
 
 struct GemmParams {
   int n_rows, kdim, ndim;
@@ -44,18 +73,41 @@ struct GemmParams {
   const uint8_t* arena;
   size_t slot_stride;
   size_t bias_off;             // byte offset of this GEMM's bias inside a slot (bf16)
-  int stage;                   // 1: hidden = relu(acc + b1) bf16; 2: fp32 scatter epilogue
-  uint16_t* hidden;            // stage 1 output (n_rows, ndim)
-  const int32_t* row_map;      // stage 2
+  uint16_t* hidden;            // GEMM1 output (n_rows, ndim) bf16
+  const int32_t* row_map;      // GEMM2: output row of permuted row p
   const float* alpha;
   const float* resid;
   float* out;
   int32_t* err_flag;
+  unsigned long long* prof;    // optional per-CTA cycle counters (sida_debug_gemm_prof)
 };
+
+// prof slots per CTA: producer wait(empty), MMA wait(tmem_empty), MMA wait(full),
+// MMA loop total, epilogue wait(tmem_full), epilogue loop total, tiles
+constexpr int kProfSlots = 8;
+__device__ __forceinline__ unsigned long long clk() { return clock64(); }
 
 // ---------------------------------------------------------------- PTX shims
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// shared::cluster address of the same smem object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -68,8 +120,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+// arrive on the barrier at shared::cluster address `caddr` (possibly remote)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr)
+               : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -86,22 +140,54 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 }
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
 }
 
+// TMA tile loads; `mbar` is a shared::cluster address (the leader CTA's
+// barrier in CG=2, so both CTAs' bytes land on one transaction count).
+template <int CG>
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1,
+                                            uint32_t mbar) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(mbar), "r"(c0), "r"(c1)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(mbar), "r"(c0), "r"(c1)
+        : "memory");
+}
+
+template <int CG>
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, int c0, int c1,
-                                            int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
+                                            int c2, uint32_t mbar) {
+  if constexpr (CG == 1)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(mbar), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -111,10 +197,19 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// MMA completion -> mbarrier arrive (CG=2: on the same barrier of both CTAs)
+template <int CG>
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+  if constexpr (CG == 1)
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+  else
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(static_cast<uint16_t>(0x3))
+        : "memory");
 }
 
 // K-major operand tile, 128-byte rows, SWIZZLE_128B, 8-row core groups 1024 B
@@ -128,23 +223,31 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// kind::f16 instruction descriptor: bf16 A/B, f32 D, both K-major, M=128.
-template <int BN>
+// kind::f16 instruction descriptor: bf16 A/B, f32 D, both K-major.
+template <int M, int N>
 __device__ __forceinline__ constexpr uint32_t idesc_bf16() {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(BN >> 3) << 17) |
-         (static_cast<uint32_t>(BM >> 4) << 24);
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+template <int CG>
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                           uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  if constexpr (CG == 1)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* v) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -155,7 +258,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // one cvt.rn.bf16x2.f32
+  return *reinterpret_cast<uint32_t*>(&v);
 }
 
 // ------------------------------------------------------------ tile schedule
@@ -163,9 +274,10 @@ struct TileInfo {
   int expert, row0, row_end, ncol0, slot;
 };
 
+// Tile t -> (expert, first row of the TM-row tile, column tile).
 __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int32_t* s_prefix,
                                                 const int32_t* s_expert, int n_list,
-                                                const GemmParams& p, int BN) {
+                                                const GemmParams& p, int BN, int TM) {
   const int mt = t / n_ntiles, nt = t - mt * n_ntiles;
   int lo = 0, hi = n_list - 1;
   while (lo < hi) {
@@ -175,27 +287,32 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int32
   TileInfo ti;
   ti.expert = s_expert[lo];
   const int seg0 = p.off[ti.expert];
-  ti.row0 = seg0 + (mt - s_prefix[lo]) * BM;
+  ti.row0 = seg0 + (mt - s_prefix[lo]) * TM;
   ti.row_end = p.off[ti.expert + 1];
   ti.ncol0 = nt * BN;
   ti.slot = p.expert_slot[ti.expert];
   return ti;
 }
 
-template <int BN>
+template <int BN, int STAGE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const GemmParams p) {
+  constexpr int TM = BM * CG;                    // rows per tile (per CTA pair)
+  constexpr int BNL = BN / CG;                   // B rows this CTA loads
   constexpr uint32_t kABytes = BM * BK * 2;
-  constexpr uint32_t kBBytes = BN * BK * 2;
-  constexpr uint32_t kTmemCols = 2 * BN;
+  constexpr uint32_t kBBytes = BNL * BK * 2;
+  constexpr uint32_t kTmemCols = pow2_cols(2 * BN);
+  constexpr int kStages = stages_for<BN, STAGE, CG>();
+  constexpr int kTile = stage_tile_bytes<STAGE>();
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kStages * kBBytes);
+  uint8_t* sOut = sB + kStages * kBBytes;  // kEpiWarps staging tiles
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + kEpiWarps * kTile);
   uint64_t* full = bars;
   uint64_t* empty = bars + kStages;
   uint64_t* tmem_full = bars + 2 * kStages;
@@ -206,6 +323,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_list = p.expert_list ? p.n_list : p.num_experts;
+  const uint32_t rank = CG == 1 ? 0u : cluster_rank();
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;  // CTA pairs walk tiles together
 
   if (threadIdx.x == 0) {
     int acc = 0;
@@ -213,7 +333,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const int e = p.expert_list ? p.expert_list[i] : i;
       s_expert[i] = e;
       s_prefix[i] = acc;
-      acc += ceil_div(p.off[e + 1] - p.off[e], BM);
+      acc += ceil_div(p.off[e + 1] - p.off[e], TM);
     }
     s_prefix[n_list] = acc;
     for (int i = 0; i < kStages; ++i) {
@@ -222,7 +342,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 128);
+      mbar_init(&tmem_empty[i], CG * kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -232,13 +352,20 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(s_tmem)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(s_tmem)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(s_tmem)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
 
@@ -247,134 +374,222 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int n_kblocks = p.kdim / BK;
 
   if (warp == 0) {
+    // ===== TMA producer (both CTAs): own 128 rows of A, own BN/CG rows of B
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN);
+      unsigned long long w_empty = 0;
+      for (int t = unit; t < total; t += n_units) {
+        const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
         if (ti.slot < 0) continue;
         for (int kb = 0; kb < n_kblocks; ++kb) {
+          const unsigned long long c0 = p.prof ? clk() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], kABytes + kBBytes);
-          tma_load_2d(sA + stage * kABytes, &tmA, kb * BK, ti.row0, &full[stage]);
-          tma_load_3d(sB + stage * kBBytes, &tmB, kb * BK, ti.ncol0, ti.slot, &full[stage]);
+          if (p.prof) w_empty += clk() - c0;
+          const uint32_t fb = CG == 1 ? smem_u32(&full[stage]) : map_rank(smem_u32(&full[stage]), 0);
+          if (leader) mbar_expect_tx(&full[stage], CG * (kABytes + kBBytes));
+          tma_load_2d<CG>(sA + stage * kABytes, &tmA, kb * BK, ti.row0 + rank * BM, fb);
+          tma_load_3d<CG>(sB + stage * kBBytes, &tmB, kb * BK, ti.ncol0 + rank * BNL, ti.slot, fb);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
+      if (p.prof) p.prof[blockIdx.x * kProfSlots + 0] = w_empty;
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16<BN>();
+    // ===== MMA issuer (single thread of the leader CTA)
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_bf16<TM, BN>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN);
+      unsigned long long w_epi = 0, w_tma = 0, n_tiles = 0;
+      const unsigned long long m0 = p.prof ? clk() : 0;
+      for (int t = unit; t < total; t += n_units) {
+        const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
         if (ti.slot < 0) {
           atomicExch(p.err_flag, 1);
           continue;
         }
-        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        ++n_tiles;
+        const unsigned long long c0 = p.prof ? clk() : 0;
+        if constexpr (CG == 1) mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        else mbar_wait_cluster(&tmem_empty[acc], acc_phase ^ 1);
+        if (p.prof) w_epi += clk() - c0;
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * (kTmemCols / 2);
         for (int kb = 0; kb < n_kblocks; ++kb) {
+          const unsigned long long c1 = p.prof ? clk() : 0;
           mbar_wait(&full[stage], phase);
+          if (p.prof) w_tma += clk() - c1;
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * kABytes);
           const uint32_t b0 = smem_u32(sB + stage * kBBytes);
 #pragma unroll
           for (int k = 0; k < BK / UMMA_K; ++k) {
-            umma_bf16(d_tmem, sw128_desc(a0 + k * UMMA_K * 2), sw128_desc(b0 + k * UMMA_K * 2),
-                      idesc, (kb | k) != 0);
+            umma_bf16<CG>(d_tmem, sw128_desc(a0 + k * UMMA_K * 2),
+                          sw128_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0);
           }
-          tc_commit(&empty[stage]);
+          tc_commit<CG>(&empty[stage]);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tmem_full[acc]);
+        tc_commit<CG>(&tmem_full[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      if (p.prof) {
+        unsigned long long* pr = p.prof + blockIdx.x * kProfSlots;
+        pr[1] = w_epi;
+        pr[2] = w_tma;
+        pr[3] = clk() - m0;
+        pr[6] = n_tiles;
       }
     }
   } else {
-    // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 == tile rows
+    // ===== epilogue. Warp w owns TMEM lanes 32*(w%4)..+31 (this CTA's tile
+    // rows) and one half of the columns, in 32-column chunks. Per chunk:
+    // tcgen05.ld (next chunk's load in flight), + bias, activation / alpha,
+    // write the 32x32 sub-tile row-per-lane into a swizzled smem tile, then
+    // re-read it column-chunk-per-lane so each global access covers whole row
+    // segments (GEMM1: 8 rows x 64 B, GEMM2: 4 rows x 128 B per instruction).
     const int quarter = warp & 3;
-    const int r_in_tile = quarter * 32 + lane;
+    const int half = (warp - 2) >> 2;
+    constexpr int kHalfCols = BN / 2;
+    constexpr int kChunks = kHalfCols / 32;
+    uint8_t* stile = sOut + (warp - 2) * kTile;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN);
+    unsigned long long w_full = 0;
+    const unsigned long long e0 = p.prof ? clk() : 0;
+    for (int t = unit; t < total; t += n_units) {
+      const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
       if (ti.slot < 0) continue;
-      mbar_wait(&tmem_full[acc], acc_phase);
-      tc_fence_after();
-      const int row = ti.row0 + r_in_tile;
-      const bool valid = row < ti.row_end;
+      const int qrow0 = ti.row0 + rank * BM + quarter * 32;  // first row of this warp's quarter
+      const int my_row = qrow0 + lane;
+      const bool valid = my_row < ti.row_end;
       const uint16_t* bias = reinterpret_cast<const uint16_t*>(
           p.arena + static_cast<size_t>(ti.slot) * p.slot_stride + p.bias_off);
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * BN;
       float a_scale = 1.f;
-      size_t orow = static_cast<size_t>(row);
-      if (p.stage == 2 && valid) {
-        if (p.alpha) a_scale = p.alpha[row];
-        if (p.row_map) orow = static_cast<size_t>(p.row_map[row]);
+      int orow = my_row;
+      if (STAGE == 2 && valid) {
+        if (p.alpha) a_scale = p.alpha[my_row];
+        if (p.row_map) orow = p.row_map[my_row];
       }
-#pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t v[32];
-        tmem_ld32(t_row + c * 32, v);
-        const int col0 = ti.ncol0 + c * 32;
-        if (!valid) continue;
-        if (p.stage == 1) {
-          uint4* dst = reinterpret_cast<uint4*>(p.hidden + orow * p.ndim + col0);
+      const int cbase = ti.ncol0 + half * kHalfCols;
+      const unsigned long long c2 = p.prof ? clk() : 0;
+      mbar_wait(&tmem_full[acc], acc_phase);
+      if (p.prof) w_full += clk() - c2;
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
+                             acc * (kTmemCols / 2) + half * kHalfCols;
+      uint32_t v[2][32];
+      tmem_ld32_nowait(t_row, v[0]);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float f[8];
+      for (int c = 0; c < kChunks; ++c) {
+        const int col0 = cbase + c * 32;
+        const uint4* bvec = reinterpret_cast<const uint4*>(bias + col0);
+        uint4 braw[4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              f[j] = fmaxf(__uint_as_float(v[q * 8 + j]) + bf16_to_f32(bias[col0 + q * 8 + j]), 0.f);
-            uint4 o;
-            o.x = pack_bf16x2(f[0], f[1]);
-            o.y = pack_bf16x2(f[2], f[3]);
-            o.z = pack_bf16x2(f[4], f[5]);
-            o.w = pack_bf16x2(f[6], f[7]);
-            dst[q] = o;
-          }
-        } else {
-          float4* dst = reinterpret_cast<float4*>(p.out + orow * p.ndim + col0);
-          const float4* res = p.resid ? reinterpret_cast<const float4*>(p.resid + orow * p.ndim + col0)
-                                      : nullptr;
+        for (int q = 0; q < 4; ++q) braw[q] = __ldg(bvec + q);
+        tmem_wait_ld();
+        if (c + 1 < kChunks) tmem_ld32_nowait(t_row + (c + 1) * 32, v[(c + 1) & 1]);
+        const uint32_t* vv = v[c & 1];
+        float f[32];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            float4 o;
-            o.x = (__uint_as_float(v[q * 4 + 0]) + bf16_to_f32(bias[col0 + q * 4 + 0])) * a_scale;
-            o.y = (__uint_as_float(v[q * 4 + 1]) + bf16_to_f32(bias[col0 + q * 4 + 1])) * a_scale;
-            o.z = (__uint_as_float(v[q * 4 + 2]) + bf16_to_f32(bias[col0 + q * 4 + 2])) * a_scale;
-            o.w = (__uint_as_float(v[q * 4 + 3]) + bf16_to_f32(bias[col0 + q * 4 + 3])) * a_scale;
-            if (res) {
-              const float4 x = res[q];
-              o.x = x.x + o.x; o.y = x.y + o.y; o.z = x.z + o.z; o.w = x.w + o.w;
-            }
-            dst[q] = o;
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t w[4] = {braw[q].x, braw[q].y, braw[q].z, braw[q].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            f[q * 8 + 2 * j] = __uint_as_float(vv[q * 8 + 2 * j]) + __uint_as_float(w[j] << 16);
+            f[q * 8 + 2 * j + 1] =
+                __uint_as_float(vv[q * 8 + 2 * j + 1]) + __uint_as_float(w[j] & 0xFFFF0000u);
           }
         }
+        if (STAGE == 1) {
+          // row-per-lane write: row r = lane, 4 x 16 B chunks, chunk' = q ^ ((r>>1)&3)
+          uint4* srow = reinterpret_cast<uint4*>(stile + lane * 64);
+          const int sw = (lane >> 1) & 3;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 o;
+            o.x = bf16x2_rn(fmaxf(f[q * 8 + 0], 0.f), fmaxf(f[q * 8 + 1], 0.f));
+            o.y = bf16x2_rn(fmaxf(f[q * 8 + 2], 0.f), fmaxf(f[q * 8 + 3], 0.f));
+            o.z = bf16x2_rn(fmaxf(f[q * 8 + 4], 0.f), fmaxf(f[q * 8 + 5], 0.f));
+            o.w = bf16x2_rn(fmaxf(f[q * 8 + 6], 0.f), fmaxf(f[q * 8 + 7], 0.f));
+            srow[q ^ sw] = o;
+          }
+          __syncwarp();
+          // read back: lane -> (row = i*8 + lane/4, chunk = lane%4)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r = i * 8 + (lane >> 2), q = lane & 3;
+            const uint4 val = reinterpret_cast<const uint4*>(stile + r * 64)[q ^ ((r >> 1) & 3)];
+            if (qrow0 + r < ti.row_end)
+              *reinterpret_cast<uint4*>(p.hidden + static_cast<size_t>(qrow0 + r) * p.ndim +
+                                        col0 + q * 8) = val;
+          }
+          __syncwarp();
+        } else {
+          // row-per-lane write of alpha*(acc+b2): 8 x 16 B chunks, chunk' = q ^ (r & 7)
+          uint4* srow = reinterpret_cast<uint4*>(stile + lane * 128);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4 o = make_float4(f[q * 4 + 0] * a_scale, f[q * 4 + 1] * a_scale,
+                                   f[q * 4 + 2] * a_scale, f[q * 4 + 3] * a_scale);
+            srow[q ^ (lane & 7)] = *reinterpret_cast<uint4*>(&o);
+          }
+          __syncwarp();
+          // read back: lane -> (row = i*4 + lane/8, chunk = lane%8); residual
+          // and unpermute (row_map) applied per row segment
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + (lane >> 3), q = lane & 7;
+            const int orow_r = __shfl_sync(0xffffffffu, orow, r);
+            const uint4 raw = reinterpret_cast<const uint4*>(stile + r * 128)[q ^ (r & 7)];
+            if (qrow0 + r < ti.row_end) {
+              float4 o = *reinterpret_cast<const float4*>(&raw);
+              const size_t at = static_cast<size_t>(orow_r) * p.ndim + col0 + q * 4;
+              if (p.resid) {
+                const float4 x = __ldg(reinterpret_cast<const float4*>(p.resid + at));
+                o.x = x.x + o.x; o.y = x.y + o.y; o.z = x.z + o.z; o.w = x.w + o.w;
+              }
+              *reinterpret_cast<float4*>(p.out + at) = o;
+            }
+          }
+          __syncwarp();
+        }
       }
+      // this warp's TMEM reads are done: release the accumulator (leader's barrier)
       tc_fence_before();
-      mbar_arrive(&tmem_empty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t eb = smem_u32(&tmem_empty[acc]);
+        mbar_arrive_cluster(CG == 1 ? eb : map_rank(eb, 0));
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (p.prof && warp == 2 && lane == 0) {
+      p.prof[blockIdx.x * kProfSlots + 4] = w_full;
+      p.prof[blockIdx.x * kProfSlots + 5] = clk() - e0;
     }
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 1) __syncthreads(); else cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols));
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols));
   }
 }
 
-template <int BN>
+template <int BN, int STAGE, int CG>
 constexpr size_t smem_bytes() {
-  return 1024 + kStages * (BM * BK * 2 + BN * BK * 2) + (2 * kStages + 4) * 8 + 16 +
+  return 1024 + stages_for<BN, STAGE, CG>() * (BM * BK * 2 + (BN / CG) * BK * 2) +
+         kEpiWarps * stage_tile_bytes<STAGE>() + (2 * stages_for<BN, STAGE, CG>() + 4) * 8 + 16 +
          (2 * kMaxListed + 2) * 4;
 }
 
@@ -422,39 +637,100 @@ static int make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
   return SIDA_OK;
 }
 
-template <int BN>
+template <int BN, int STAGE, int CG>
 static int launch_gemm(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
                        int n_listed, cudaStream_t s) {
+  auto kern = grouped_gemm_kernel<BN, STAGE, CG>;
   static bool configured = false;
   if (!configured) {
-    SIDA_CUDA(cudaFuncSetAttribute(grouped_gemm_kernel<BN>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_bytes<BN>()));
+    SIDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_bytes<BN, STAGE, CG>()));
     configured = true;
   }
   CUtensorMap ta, tb;
   int st = make_map_2d(&ta, a_base, p.kdim, p.n_rows, BM);
   if (st) return st;
-  st = make_map_3d(&tb, b_base, p.kdim, p.ndim, n_slots, p.slot_stride, BN);
+  st = make_map_3d(&tb, b_base, p.kdim, p.ndim, n_slots, p.slot_stride, BN / CG);
   if (st) return st;
-  const int max_tiles = (ceil_div(p.n_rows, BM) + n_listed) * (p.ndim / BN);
-  const int grid = std::max(1, std::min(max_tiles, kNumSMs));
-  grouped_gemm_kernel<BN><<<grid, kThreads, smem_bytes<BN>(), s>>>(ta, tb, p);
-  SIDA_LAUNCH_CHECK();
+  const int max_tiles = (ceil_div(p.n_rows, BM * CG) + n_listed) * (p.ndim / BN);
+  const int units = std::max(1, std::min(max_tiles, kNumSMs / CG));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem_bytes<BN, STAGE, CG>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return SIDA_OK;
 }
 
+template <int STAGE, int CG>
+static int dispatch_bn(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
+                       int n_listed, cudaStream_t s) {
+  // N tile: 256 for wide outputs; 192 when it splits N into more tiles with no
+  // remainder (d = 768 -> 4 tiles: better wave quantisation on 148 SMs)
+  if (p.ndim % 256 == 0 && p.ndim >= 2048)
+    return launch_gemm<256, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
+  if (p.ndim % 192 == 0) return launch_gemm<192, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
+  if (p.ndim % 256 == 0) return launch_gemm<256, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
+  if (p.ndim % 128 == 0) return launch_gemm<128, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
+  return launch_gemm<64, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
+}
+
+// CTA-pair (M=256) tiles when experts hold enough rows to fill them.
+template <int STAGE>
 static int dispatch_gemm(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
-                         int n_listed, cudaStream_t s) {
-  if (p.ndim % 256 == 0) return launch_gemm<256>(a_base, b_base, n_slots, p, n_listed, s);
-  if (p.ndim % 128 == 0) return launch_gemm<128>(a_base, b_base, n_slots, p, n_listed, s);
-  return launch_gemm<64>(a_base, b_base, n_slots, p, n_listed, s);
+                         int n_listed, int cg, cudaStream_t s) {
+  if (cg == 2) return dispatch_bn<STAGE, 2>(a_base, b_base, n_slots, p, n_listed, s);
+  return dispatch_bn<STAGE, 1>(a_base, b_base, n_slots, p, n_listed, s);
 }
 
 }  // namespace sm100
 }  // namespace sida
 
 using namespace sida;
+
+static unsigned long long* g_prof = nullptr;  // [2 GEMMs][148 CTAs][kProfSlots]
+
+static unsigned long long* prof_buffer(int gemm) {
+  static int enabled = -1;
+  if (enabled < 0) enabled = getenv("SIDA_GEMM_PROF") != nullptr;
+  if (!enabled) return nullptr;
+  if (!g_prof) {
+    const size_t bytes = 2ull * kNumSMs * sm100::kProfSlots * sizeof(unsigned long long);
+    if (cudaMalloc(&g_prof, bytes) != cudaSuccess) return nullptr;
+    cudaMemset(g_prof, 0, bytes);
+  }
+  return g_prof + (size_t)gemm * kNumSMs * sm100::kProfSlots;
+}
+
+// Observability: copy the per-CTA cycle counters of the last FFN call
+// (enabled by SIDA_GEMM_PROF=1) into out[2][148][8]; synchronises the device.
+extern "C" int sida_debug_gemm_prof(unsigned long long* out) {
+  SIDA_REQUIRE(g_prof, SIDA_ERR_UNSUPPORTED, "run with SIDA_GEMM_PROF=1 to collect counters");
+  SIDA_CUDA(cudaDeviceSynchronize());
+  SIDA_CUDA(cudaMemcpy(out, g_prof, 2ull * kNumSMs * sm100::kProfSlots * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost));
+  return SIDA_OK;
+}
+
+// CTA-group choice: SIDA_FFN_CG=1|2 forces it; default pairs (M=256 tiles)
+// once the average expert holds >= 1024 rows (padding waste < 1/8).
+static int choose_cg(int n_rows, int listed) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("SIDA_FFN_CG");
+    forced = e ? atoi(e) : 0;
+  }
+  if (forced == 1 || forced == 2) return forced;
+  return n_rows >= 1024 * listed ? 2 : 1;
+}
 
 extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h,
                                      const int32_t* off, int num_experts,
@@ -478,18 +754,20 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   cudaStream_t s = as_stream(stream);
   const uint8_t* ar = static_cast<const uint8_t*>(arena);
   const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
+  const int cg = choose_cg(n_rows, listed);
 
   sm100::GemmParams p1{};
   p1.n_rows = n_rows; p1.kdim = d; p1.ndim = h;
   p1.off = off; p1.num_experts = num_experts; p1.expert_slot = expert_slot;
   p1.expert_list = expert_list; p1.n_list = n_list;
   p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
-  p1.stage = 1; p1.hidden = hidden; p1.err_flag = err_flag;
-  int st = sm100::dispatch_gemm(x_perm, ar, n_slots, p1, listed, s);
+  p1.hidden = hidden; p1.err_flag = err_flag; p1.prof = prof_buffer(0);
+  int st = sm100::dispatch_gemm<1>(x_perm, ar, n_slots, p1, listed, cg, s);
   if (st) return st;
 
   sm100::GemmParams p2 = p1;
-  p2.kdim = h; p2.ndim = d; p2.bias_off = b2_off; p2.stage = 2;
+  p2.kdim = h; p2.ndim = d; p2.bias_off = b2_off;
   p2.row_map = row_map; p2.alpha = alpha; p2.resid = resid; p2.out = out;
-  return sm100::dispatch_gemm(hidden, ar + w2_off, n_slots, p2, listed, s);
+  p2.prof = prof_buffer(1);
+  return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, listed, cg, s);
 }

@@ -1,0 +1,80 @@
+"""Run one MoE layer's grouped FFN at the bench shape (for ncu / timing).
+
+    python tools/ffn_probe.py [--tokens 32768] [--experts 8] [--iters 20]
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2310_18859_b200 import MoEConfig, MoEModel  # noqa: E402
+from paper_2310_18859_b200.offload import ExpertStore  # noqa: E402
+from paper_2310_18859_b200.predictor import DeviceTable  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--tokens", type=int, default=32768)
+p.add_argument("--experts", type=int, default=8)
+p.add_argument("--d", type=int, default=768)
+p.add_argument("--h", type=int, default=3072)
+p.add_argument("--iters", type=int, default=20)
+a = p.parse_args()
+cfg = MoEConfig(vocab_size=64, d_model=a.d, num_layers=1, num_experts=a.experts,
+                expert_hidden=a.h, max_seq_len=16)
+model = MoEModel.synthetic(cfg, 0)
+store = ExpertStore.full(model)
+N, K = a.tokens, a.experts
+ids = torch.randint(0, K, (1, N, 1), device="cuda", dtype=torch.int32)
+al = torch.rand((1, N, 1), device="cuda", dtype=torch.float64)
+dt = DeviceTable(ids, al, al.float(), N, 1)
+dt.permute(K, torch.cuda.current_stream())
+x = torch.randn(N, a.d, device="cuda")
+torch.cuda.synchronize()
+dt.ready.synchronize()
+hist = dt.hist.cpu().numpy()
+out = store.run_layer(model, 0, x, dt)  # loads experts
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+from paper_2310_18859_b200.offload import Wave, run_waves  # noqa: E402
+need = list(range(K))
+wave = Wave(0, [], need, store.slot_row(0, need))
+for _ in range(3):
+    run_waves(model, [wave], x, dt, store, torch.cuda.current_stream())
+torch.cuda.synchronize()
+e0.record()
+for _ in range(a.iters):
+    run_waves(model, [wave], x, dt, store, torch.cuda.current_stream())
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.iters
+fl = 4.0 * N * a.d * a.h
+print(f"ffn layer: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s  (N={N}, K={K}, d={a.d}, h={a.h})")
+if os.environ.get("SIDA_GEMM_PROF"):
+    from paper_2310_18859_b200 import _lib
+    buf = np.zeros((2, 148, 8), dtype=np.uint64)
+    _lib.check(_lib.load().sida_debug_gemm_prof(buf.ctypes.data))
+    names = ["prod_wait_empty", "mma_wait_epi", "mma_wait_tma", "mma_total", "epi_wait_full",
+             "epi_total", "tiles"]
+    for gi in range(2):
+        b = buf[gi].astype(np.float64)
+        tot = b[:, 3].mean()
+        print(f"GEMM{gi + 1}: " + ", ".join(f"{n}={b[:, i].mean():.0f}" for i, n in enumerate(names))
+              + f"  | mma waits epi {b[:, 1].mean() / tot:.1%} tma {b[:, 2].mean() / tot:.1%}")
+# cuBLAS reference on the same shapes (dense bmm, no gather/epilogue fusion)
+E = K
+xs = torch.randn(E, N // E, a.d, device="cuda", dtype=torch.bfloat16)
+w1 = torch.randn(E, a.d, a.h, device="cuda", dtype=torch.bfloat16)
+w2 = torch.randn(E, a.h, a.d, device="cuda", dtype=torch.bfloat16)
+for _ in range(3):
+    torch.bmm(torch.bmm(xs, w1), w2)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(a.iters):
+    hh = torch.bmm(xs, w1)
+    torch.bmm(hh, w2)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / a.iters
+print(f"cuBLAS bmm pair: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s")
