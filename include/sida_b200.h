@@ -61,13 +61,32 @@ int sida_device_check(int device);
  *   renormalised), alpha_f32 optional float32 copy for the FFN epilogue.
  * ------------------------------------------------------------------- */
 size_t sida_hash_param_count(int d, int cd, int H, int L, int K);
+
+/* Per-model folding tables (float64, sida_hash_tables_count doubles): the
+ * compress FC and layer-1 input projection are linear in the embedding, so
+ * TX = (tok_emb Wc) Wx1 (vocab x 4H), PX = (pos_emb Wc) Wx1 (max_len x 4H),
+ * cX = bc Wx1, plus [Wq|Wk|Wv] packed (H x 3H) and the heads packed (H x L*K). tok_emb/pos_emb may be NULL
+ * with vocab = max_len = 0 (caller-embedding path). Run once per model. */
+size_t sida_hash_tables_count(int vocab, int max_len, int H, int L, int K);
+int sida_hash_prepare(const double* params, const uint16_t* tok_emb, const uint16_t* pos_emb,
+                      int vocab, int max_len, int d, int cd, int H, int L, int K, double* tables,
+                      void* stream);
+
 size_t sida_hash_workspace_bytes(int n_tokens, int n_seq, int max_len, int d, int cd, int H,
                                  int L, int K);
-int sida_hash_forward(const double* params, const uint16_t* tok_emb, const uint16_t* pos_emb,
-                      const double* emb_f64, const int32_t* tokens, const int32_t* seq_off, int n_seq, int n_tokens,
-                      int max_len, int d, int cd, int H, int L, int K, int topk,
-                      int32_t* ids, double* alpha, float* alpha_f32,
-                      void* workspace, size_t workspace_bytes, void* stream);
+/* tables/vocab/table_max_len: from sida_hash_prepare. emb_f64 (n_tokens, d),
+ * optional: caller-supplied embeddings (ref predictor.py:377 embed_fn) instead
+ * of tokens. Requires H <= 48, cd <= 64, max_len <= 512, K <= 1024. */
+int sida_hash_forward(const double* params, const double* tables, int vocab, int table_max_len,
+                      const double* emb_f64, const int32_t* tokens, const int32_t* seq_off,
+                      int n_seq, int n_tokens, int max_len, int d, int cd, int H, int L, int K,
+                      int topk, int32_t* ids, double* alpha, float* alpha_f32, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* Observability: summed per-warp cycles of the last hash attention launch by
+ * phase (scores, sort, support, ctx, heads, setup) when run with
+ * SIDA_HASH_PROF=1. Synchronises the device. */
+int sida_debug_hash_prof(unsigned long long* out);
 
 /* ---------------------------------------------------------------------
  * (3) Token permute + histogram (SURVEY §8(a) A13 contract), all layers.

@@ -27,8 +27,11 @@ SIGNATURES = {
     "sida_device_check": (_i, [_i]),
     "sida_hash_param_count": (_sz, [_i, _i, _i, _i, _i]),
     "sida_hash_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),
-    "sida_hash_forward": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i,
-                               _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sida_hash_tables_count": (_sz, [_i, _i, _i, _i, _i]),
+    "sida_hash_prepare": (_i, [_vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _vp, _vp]),
+    "sida_hash_forward": (_i, [_vp, _vp, _i, _i, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _i, _i,
+                               _i, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sida_debug_hash_prof": (_i, [_vp]),
     "sida_permute_workspace_bytes": (_sz, [_i, _i, _i]),
     "sida_permute_hist": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "sida_gather_rows_bf16": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),

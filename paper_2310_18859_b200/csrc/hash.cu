@@ -4,17 +4,28 @@
 // (predictor.py:234-259). Runs in float64 like the reference so the top-k ids
 // are bit-identical (SURVEY.md §7 "Bit-exact ids").
 //
-//   embed_xw1   emb = tok_emb[t] + pos_emb[pos] (fp64 of bf16 tables,
-//               ref moe.py:218), comp = emb Wc + bc, xw1 = comp Wx1
-//   lstm<H>     recurrence over each sequence (ref predictor.py:174-196):
-//               gates = (xw_t + h Wh) + b, blocks i|f|g|o, Wh column per
-//               thread in registers, S sequences per CTA
-//   rows_gemm   xw2 = h1 Wx2, q/k/v = h2 W{q,k,v}
-//   attn_heads  one warp per token: scores q.k (no 1/sqrt(H), :249),
-//               per-row sparsemax by bitonic sort in smem (numkit.py:42-60),
-//               ctx + h2 residual (:251-252), L heads, softmax over K,
-//               top-k with ties to the lower index (numkit.py:87-93)
+// Per-vocabulary folding (sida_hash_prepare, once per model + predictor):
+// the layer-1 LSTM input x_t Wx1 = (emb_t Wc + bc) Wx1 is linear in the
+// embedding emb_t = tok_emb[t] + pos_emb[p] (ref moe.py:218), so it splits
+// into  TX[t] + PX[p] + bc Wx1  with TX = (tok_emb Wc) Wx1 (vocab x 4H) and
+// PX = (pos_emb Wc) Wx1 (max_len x 4H), both computed once in fp64. Per batch
+// the compress FC and the input projection become two table rows.
+//
+//   lstm<H,S>   recurrence over each sequence (ref predictor.py:174-196):
+//               gates = (x_t Wx + h Wh) + b, blocks i|f|g|o, the Wh column of
+//               each gate in registers, four independent FMA chains
+//   rows_gemm   xw2 = h1 Wx2 and qkv = h2 [Wq|Wk|Wv], smem-tiled, 4x6
+//               register blocking
+//   attn_heads  CTA per (sequence, 32-query block): K staged in smem
+//               (transposed), one warp per query row: scores q.k (no
+//               1/sqrt(H), :249), sparsemax by an smem bitonic sort
+//               (numkit.py:42-60), ctx over the support + h2 residual
+//               (:251-252), all L heads, softmax over K and top-k with ties to
+//               the lower index (numkit.py:87-93)
+#include <stdlib.h>
+
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 
@@ -23,7 +34,8 @@ namespace hash {
 
 constexpr int kMaxLen = 512;     // T_max supported by the smem sparsemax
 constexpr int kMaxK = 1024;      // experts per layer
-constexpr int kAttnWarps = 4;
+constexpr int kAttnWarps = 8;
+constexpr int kRowsPerBlk = 64;  // query rows per attention CTA (K/V staged once)
 
 struct Dims {
   int d, cd, H, L, K;
@@ -74,27 +86,25 @@ __device__ __forceinline__ double sigmoid_d(double x) {
   return e / (1.0 + e);
 }
 
-// One warp per token: embedding (fp64 sum of bf16 tables), compress FC, and
-// the layer-1 input projection xw1 = comp @ Wx1.
+// One warp per row: out[row] = ((src[row] (+ pos_src[pos]) ) Wc (+ bc)) Wx1.
+// Modes: table rows (bf16 source, no bias: vocabulary / position folding) or
+// caller embeddings (fp64 source, with bias: the embed_fn path).
 __global__ void __launch_bounds__(256)
-embed_xw1_kernel(const uint16_t* __restrict__ tok_emb, const uint16_t* __restrict__ pos_emb,
-                 const double* __restrict__ emb_f64, const int32_t* __restrict__ tokens, const int32_t* __restrict__ seq_off, int n_seq,
-                 int n_tokens, Dims dm, ParamPtrs w, double* __restrict__ xw) {
+project_rows_kernel(const uint16_t* __restrict__ tab_bf16, const double* __restrict__ emb_f64,
+                    int n_rows, Dims dm, const double* __restrict__ cw,
+                    const double* __restrict__ cb, const double* __restrict__ wx1,
+                    double* __restrict__ out) {
   __shared__ double s_comp[8][64];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int n = blockIdx.x * 8 + wib;
-  if (n >= n_tokens) return;
-  const int sq = seq_of(seq_off, n_seq, n);
-  const int pos = n - seq_off[sq];
-  const uint16_t* te = tok_emb ? tok_emb + (size_t)tokens[n] * dm.d : nullptr;
-  const uint16_t* pe = tok_emb ? pos_emb + (size_t)pos * dm.d : nullptr;
-  const double* ee = emb_f64 ? emb_f64 + (size_t)n * dm.d : nullptr;
+  if (n >= n_rows) return;
   double part[64];
 #pragma unroll
   for (int c = 0; c < 64; ++c) part[c] = 0.0;
   for (int j = lane; j < dm.d; j += 32) {
-    const double e = ee ? ee[j] : (double)bf16_to_f32(te[j]) + (double)bf16_to_f32(pe[j]);
-    const double* row = w.cw + (size_t)j * dm.cd;
+    const double e = tab_bf16 ? (double)bf16_to_f32(tab_bf16[(size_t)n * dm.d + j])
+                              : emb_f64[(size_t)n * dm.d + j];
+    const double* row = cw + (size_t)j * dm.cd;
 #pragma unroll
     for (int c = 0; c < 64; ++c)
       if (c < dm.cd) part[c] = fma(e, row[c], part[c]);
@@ -103,24 +113,38 @@ embed_xw1_kernel(const uint16_t* __restrict__ tok_emb, const uint16_t* __restric
   for (int c = 0; c < 64; ++c) {
     if (c < dm.cd) {
       const double s = warp_sum(part[c]);
-      if (lane == 0) s_comp[wib][c] = s + w.cb[c];
+      if (lane == 0) s_comp[wib][c] = cb ? s + cb[c] : s;
     }
   }
   __syncwarp();
   const int G = 4 * dm.H;
   for (int g = lane; g < G; g += 32) {
     double acc = 0.0;
-    for (int c = 0; c < dm.cd; ++c) acc = fma(s_comp[wib][c], w.wx1[(size_t)c * G + g], acc);
-    xw[(size_t)n * G + g] = acc;
+    for (int c = 0; c < dm.cd; ++c) acc = fma(s_comp[wib][c], wx1[(size_t)c * G + g], acc);
+    out[(size_t)n * G + g] = acc;
   }
 }
 
-// LSTM recurrence. blockDim = 4H; thread g owns gate column g of Wh (in
-// registers); S sequences per CTA share the weights.
-template <int MAXH, int S>
+// cX[g] = sum_c bc[c] Wx1[c][g] (the bias part of the folded input projection)
+__global__ void bias_project_kernel(const double* __restrict__ cb, const double* __restrict__ wx1,
+                                    int cd, int G, double* __restrict__ out) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= G) return;
+  double acc = 0.0;
+  for (int c = 0; c < cd; ++c) acc = fma(cb[c], wx1[(size_t)c * G + g], acc);
+  out[g] = acc;
+}
+
+// LSTM recurrence. blockDim = 4*MAXH; thread g owns gate column g of Wh (in
+// registers); S sequences per CTA share the weights. Layer-1 input comes from
+// the folded tables (FOLD) or a materialised x Wx (xw).
+template <int MAXH, int S, bool FOLD>
 __global__ void __launch_bounds__(4 * MAXH)
-lstm_kernel(const double* __restrict__ xw, const double* __restrict__ wh, const double* __restrict__ b,
-            const int32_t* __restrict__ seq_off, int n_seq, int H, double* __restrict__ h_out) {
+lstm_kernel(const double* __restrict__ xw, const double* __restrict__ tokx,
+            const double* __restrict__ posx, const double* __restrict__ cx,
+            const int32_t* __restrict__ tokens, const double* __restrict__ wh,
+            const double* __restrict__ b, const int32_t* __restrict__ seq_off, int n_seq, int H,
+            double* __restrict__ h_out) {
   __shared__ double s_h[S][MAXH];
   __shared__ double s_gate[S][4 * MAXH];
   const int G = 4 * H;
@@ -130,6 +154,7 @@ lstm_kernel(const double* __restrict__ xw, const double* __restrict__ wh, const 
 #pragma unroll
   for (int i = 0; i < MAXH; ++i) wcol[i] = (g < G && i < H) ? wh[(size_t)i * G + g] : 0.0;
   const double bg = g < G ? b[g] : 0.0;
+  const double cg = (FOLD && g < G) ? cx[g] : 0.0;
   int len[S], base[S];
   int tmax = 0;
 #pragma unroll
@@ -139,31 +164,51 @@ lstm_kernel(const double* __restrict__ xw, const double* __restrict__ wh, const 
     len[s] = sq < n_seq ? seq_off[sq + 1] - seq_off[sq] : 0;
     tmax = max(tmax, len[s]);
   }
-  // cell-update role: thread -> (sequence us, unit uj)
-  const int us = g / MAXH, uj = g % MAXH;
+  const int us = g / MAXH, uj = g % MAXH;  // cell-update role: (sequence, unit)
   double c_state = 0.0;
   for (int i = threadIdx.x; i < S * MAXH; i += blockDim.x) (&s_h[0][0])[i] = 0.0;
   __syncthreads();
+  // x_t Wx does not depend on h: its load for step t+1 is issued during step
+  // t so the (random-row) table / L2 latency leaves the recurrence's path
+  auto load_x = [&](int s, int t) -> double {
+    if (g >= G || t >= len[s]) return 0.0;
+    const int n = base[s] + t;
+    if (FOLD) return (tokx[(size_t)tokens[n] * G + g] + posx[(size_t)t * G + g]) + cg;
+    return xw[(size_t)n * G + g];
+  };
+  double xnext[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) xnext[s] = load_x(s, 0);
   for (int t = 0; t < tmax; ++t) {
+    double xcur[S];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      xcur[s] = xnext[s];
+      xnext[s] = load_x(s, t + 1);
+    }
     if (g < G) {
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         if (t < len[s]) {
-          double acc = 0.0;
+          const double x = xcur[s];
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
 #pragma unroll
-          for (int i = 0; i < MAXH; ++i)
-            if (i < H) acc = fma(s_h[s][i], wcol[i], acc);
-          s_gate[s][g] = (xw[(size_t)(base[s] + t) * G + g] + acc) + bg;
+          for (int i = 0; i < MAXH; i += 4) {
+            if (i < H) a0 = fma(s_h[s][i], wcol[i], a0);
+            if (i + 1 < H) a1 = fma(s_h[s][i + 1], wcol[i + 1], a1);
+            if (i + 2 < H) a2 = fma(s_h[s][i + 2], wcol[i + 2], a2);
+            if (i + 3 < H) a3 = fma(s_h[s][i + 3], wcol[i + 3], a3);
+          }
+          const double pre = (x + ((a0 + a1) + (a2 + a3))) + bg;
+          // gate nonlinearity on the gate's own thread: i, f, o sigmoid; g tanh
+          s_gate[s][g] = (g >= 2 * H && g < 3 * H) ? tanh(pre) : sigmoid_d(pre);
         }
       }
     }
     __syncthreads();
     if (us < S && uj < H && t < len[us]) {
       const double* gt = s_gate[us];
-      const double ig = sigmoid_d(gt[uj]);
-      const double fg = sigmoid_d(gt[H + uj]);
-      const double gg = tanh(gt[2 * H + uj]);
-      const double og = sigmoid_d(gt[3 * H + uj]);
+      const double ig = gt[uj], fg = gt[H + uj], gg = gt[2 * H + uj], og = gt[3 * H + uj];
       c_state = fg * c_state + ig * gg;
       const double hv = og * tanh(c_state);
       s_h[us][uj] = hv;
@@ -173,165 +218,549 @@ lstm_kernel(const double* __restrict__ xw, const double* __restrict__ wh, const 
   }
 }
 
-// C (N x M) = A (N x Kd) @ B (Kd x M), fp64; B staged in smem.
+// C (N x M) = A (N x Kd) @ B (Kd x M), fp64. Block = 64 rows; A and B in smem;
+// 256 threads as a 16 x 16 grid, each 4 rows x (M/16) columns.
+constexpr int kRG_Rows = 64;
 __global__ void __launch_bounds__(256)
 rows_gemm_kernel(const double* __restrict__ A, int n_rows, int Kd, const double* __restrict__ B,
                  int M, double* __restrict__ C) {
-  extern __shared__ double s_b[];
-  for (int i = threadIdx.x; i < Kd * M; i += blockDim.x) s_b[i] = B[i];
-  __syncthreads();
-  const int rows_per_block = 16;
-  const int r0 = blockIdx.x * rows_per_block;
-  for (int i = threadIdx.x; i < rows_per_block * M; i += blockDim.x) {
-    const int r = r0 + i / M, m = i % M;
-    if (r >= n_rows) break;
-    const double* a = A + (size_t)r * Kd;
-    double acc = 0.0;
-    for (int k = 0; k < Kd; ++k) acc = fma(a[k], s_b[k * M + m], acc);
-    C[(size_t)r * M + m] = acc;
-  }
-}
-
-// In-smem bitonic sort, descending, of n (power of two) doubles by one warp.
-__device__ void warp_bitonic_desc(double* v, int n) {
-  const int lane = threadIdx.x & 31;
-  for (int size = 2; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = lane; i < n / 2; i += 32) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool desc = ((lo & size) == 0);
-        const double a = v[lo], b = v[hi];
-        if (desc ? (a < b) : (a > b)) {
-          v[lo] = b;
-          v[hi] = a;
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
-
-// One warp per token: scores, sparsemax, ctx, residual, L heads, softmax,
-// top-k. Smem per warp: scores[kMaxLen], sorted[kMaxLen], resid[64], z[kMaxK].
-__global__ void __launch_bounds__(32 * kAttnWarps)
-attn_heads_kernel(const double* __restrict__ q, const double* __restrict__ k,
-                  const double* __restrict__ v, const double* __restrict__ h2,
-                  const int32_t* __restrict__ seq_off, int n_seq, int n_tokens, Dims dm,
-                  const double* __restrict__ hw, const double* __restrict__ hb, int topk,
-                  int32_t* __restrict__ ids, double* __restrict__ alpha,
-                  float* __restrict__ alpha_f32) {
   extern __shared__ double smem_d[];
+  double* s_b = smem_d;                  // Kd x M
+  double* s_a = smem_d + (size_t)Kd * M; // 64 x (Kd + 1)
+  const int r0 = blockIdx.x * kRG_Rows;
+  for (int i = threadIdx.x; i < Kd * M; i += blockDim.x) s_b[i] = B[i];
+  for (int i = threadIdx.x; i < kRG_Rows * Kd; i += blockDim.x) {
+    const int r = i / Kd, k = i % Kd;
+    s_a[r * (Kd + 1) + k] = (r0 + r < n_rows) ? A[(size_t)(r0 + r) * Kd + k] : 0.0;
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int ncol = (M + 15) / 16;  // <= 12
+  double acc[4][12];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 12; ++j) acc[i][j] = 0.0;
+  for (int k = 0; k < Kd; ++k) {
+    double a[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = s_a[(ty * 4 + i) * (Kd + 1) + k];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      if (j < ncol && tx + 16 * j < M) {
+        const double bv = s_b[k * M + tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[i][j] = fma(a[i], bv, acc[i][j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = r0 + ty * 4 + i;
+    if (r >= n_rows) continue;
+#pragma unroll
+    for (int j = 0; j < 12; ++j)
+      if (j < ncol && tx + 16 * j < M) C[(size_t)r * M + tx + 16 * j] = acc[i][j];
+  }
+}
+
+// Top-k helper: (value desc, index asc) arg-max over a group of W lanes.
+__device__ __forceinline__ void seg_argmax(double& best, int& bi, int W) {
+  for (int o = W >> 1; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+  }
+}
+
+struct AttnArgs {
+  const double* qkv;   // (N, 3H): q | k | v
+  const double* h2;    // (N, H)
+  const int32_t* seq_off;
+  const int32_t* blk_off;  // (n_seq+1) prefix of ceil(len/kRowsPerBlk)
+  int n_seq, n_tokens;
+  Dims dm;
+  const double* hw;
+  const double* hb;
+  int topk;
+  int32_t* ids;
+  double* alpha;
+  float* alpha_f32;
+  unsigned long long* prof;  // optional per-warp phase cycles (SIDA_HASH_PROF)
+  int ts;  // keys/values staged in smem per sequence (0: read them from L2)
+};
+
+constexpr int kMaxZ = kMaxLen / 32;  // score registers per lane
+constexpr int kResPitch = 49;         // smem pitch (doubles) of a residual row: conflict-free
+
+// Record the selected (id, probability) of rank r for (layer, token n).
+__device__ __forceinline__ void emit(const AttnArgs& a, int l, int n, int r, int id, double p) {
+  const size_t at = ((size_t)l * a.n_tokens + n) * a.topk + r;
+  a.ids[at] = id;
+  a.alpha[at] = p;
+  if (a.alpha_f32) a.alpha_f32[at] = (float)p;
+}
+
+// Heads for small K: one thread per (row, layer); the K logits stay in
+// registers; softmax over K (ref numkit.py:28-33) then top-k on the
+// probabilities, descending, ties to the lower index (numkit.py:87-93).
+template <int KB>
+__device__ void heads_small(const AttnArgs& a, const double* s_res, int rows, int n0) {
+  const int H = a.dm.H, K = a.dm.K, L = a.dm.L;
+  for (int pr = threadIdx.x; pr < rows * L; pr += blockDim.x) {
+    const int r = pr / L, l = pr % L;
+    const double* res = s_res + r * kResPitch;
+    const double* W = a.hw + (size_t)l * H * K;
+    double z[KB];
+#pragma unroll
+    for (int e = 0; e < KB; ++e) z[e] = 0.0;
+    for (int i = 0; i < H; ++i) {
+      const double ri = res[i];
+      const double* wr = W + (size_t)i * K;
+#pragma unroll
+      for (int e = 0; e < KB; ++e)
+        if (e < K) z[e] = fma(ri, wr[e], z[e]);
+    }
+    double zmax = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < KB; ++e)
+      if (e < K) {
+        z[e] += a.hb[(size_t)l * K + e];
+        zmax = fmax(zmax, z[e]);
+      }
+    double ssum = 0.0;
+#pragma unroll
+    for (int e = 0; e < KB; ++e)
+      if (e < K) {
+        z[e] = exp(z[e] - zmax);
+        ssum += z[e];
+      }
+#pragma unroll
+    for (int e = 0; e < KB; ++e)
+      if (e < K) z[e] = z[e] / ssum;
+    for (int rk = 0; rk < a.topk; ++rk) {
+      double best = -1.0;
+      int bi = 0;
+#pragma unroll
+      for (int e = 0; e < KB; ++e)
+        if (e < K && z[e] > best) { best = z[e]; bi = e; }
+      emit(a, l, n0 + r, rk, bi, best);
+#pragma unroll
+      for (int e = 0; e < KB; ++e)
+        if (e == bi) z[e] = -2.0;  // removed from later ranks
+    }
+  }
+}
+
+// Heads for large K: one warp per (row, layer), lanes over experts, MZ
+// logits per lane in registers.
+template <int MZ>
+__device__ void heads_large(const AttnArgs& a, const double* s_res, int rows, int n0) {
+  const int H = a.dm.H, K = a.dm.K, L = a.dm.L;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  double* s_sc = smem_d + (size_t)wib * (2 * kMaxLen + 64 + dm.K);
-  double* s_srt = s_sc + kMaxLen;
-  double* s_res = s_srt + kMaxLen;
-  double* s_z = s_res + 64;
-  const int H = dm.H;
-  for (int n = blockIdx.x * kAttnWarps + wib; n < n_tokens; n += gridDim.x * kAttnWarps) {
-    const int sq = seq_of(seq_off, n_seq, n);
-    const int base = seq_off[sq], T = seq_off[sq + 1] - base;
-    // q_n -> smem, then each lane owns score columns j = lane, lane+32, ...
-    if (lane < H) s_res[lane] = q[(size_t)n * H + lane];
-    if (lane + 32 < H) s_res[lane + 32] = q[(size_t)n * H + lane + 32];
-    __syncwarp();
-    int P = 1;
-    while (P < T) P <<= 1;
-    for (int j = lane; j < P; j += 32) {
-      if (j < T) {
-        const double* kr = k + (size_t)(base + j) * H;
-        double sc = 0.0;
-        for (int i = 0; i < H; ++i) sc = fma(s_res[i], kr[i], sc);
-        s_sc[j] = sc;
-        s_srt[j] = sc;
-      } else {
-        s_srt[j] = -INFINITY;
-      }
-    }
-    __syncwarp();
-    warp_bitonic_desc(s_srt, P);
-    // running sum S_k of the sorted row (stored in place), support count
-    // k_z = #{k : 1 + k z_(k) > S_k}, tau = (S_{k_z} - 1) / k_z (ref numkit.py:52-59)
-    double carry = 0.0;
-    int kz = 0;
-    for (int c0 = 0; c0 < T; c0 += 32) {
-      const int idx = c0 + lane;
-      const double z = idx < T ? s_srt[idx] : 0.0;
-      double incl = z;
+  for (int pr = wib; pr < rows * L; pr += kAttnWarps) {
+    const int r = pr / L, l = pr % L;
+    const double* res = s_res + r * kResPitch;
+    const double* W = a.hw + (size_t)l * H * K;
+    double z[MZ];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const double t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      const double S = carry + incl;
-      const bool sup = idx < T && (1.0 + (double)(idx + 1) * z > S);
-      kz += __popc(__ballot_sync(0xffffffffu, sup));
-      if (idx < T) s_srt[idx] = S;
-      carry = __shfl_sync(0xffffffffu, S, 31);
+    for (int m = 0; m < MZ; ++m) z[m] = 0.0;
+    for (int i = 0; i < H; ++i) {
+      const double ri = res[i];
+      const double* wr = W + (size_t)i * K + lane;
+#pragma unroll
+      for (int m = 0; m < MZ; ++m)
+        if (lane + 32 * m < K) z[m] = fma(ri, wr[32 * m], z[m]);
     }
-    __syncwarp();
-    const double tau = (s_srt[kz - 1] - 1.0) / (double)kz;
-    // ctx = sum_j w_j v_j over the support; resid = ctx + h2_n
-    double c0v = 0.0, c1v = 0.0;
-    for (int j = 0; j < T; ++j) {
-      const double wj = s_sc[j] - tau;
-      if (wj > 0.0) {
-        const double* vr = v + (size_t)(base + j) * H;
-        if (lane < H) c0v = fma(wj, vr[lane], c0v);
-        if (lane + 32 < H) c1v = fma(wj, vr[lane + 32], c1v);
-      }
-    }
-    __syncwarp();  // every lane is done reading q from s_res
-    if (lane < H) s_res[lane] = c0v + h2[(size_t)n * H + lane];
-    if (lane + 32 < H) s_res[lane + 32] = c1v + h2[(size_t)n * H + lane + 32];
-    __syncwarp();
-    for (int l = 0; l < dm.L; ++l) {
-      const double* W = hw + (size_t)l * H * dm.K;
-      double zmax = -INFINITY;
-      for (int e = lane; e < dm.K; e += 32) {
-        double acc = 0.0;
-        for (int i = 0; i < H; ++i) acc = fma(s_res[i], W[(size_t)i * dm.K + e], acc);
-        const double z = acc + hb[(size_t)l * dm.K + e];
-        s_z[e] = z;
-        zmax = fmax(zmax, z);
+    double zmax = -INFINITY;
+#pragma unroll
+    for (int m = 0; m < MZ; ++m)
+      if (lane + 32 * m < K) {
+        z[m] += a.hb[(size_t)l * K + lane + 32 * m];
+        zmax = fmax(zmax, z[m]);
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+    for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+    double ssum = 0.0;
+#pragma unroll
+    for (int m = 0; m < MZ; ++m)
+      if (lane + 32 * m < K) {
+        z[m] = exp(z[m] - zmax);
+        ssum += z[m];
+      }
+    ssum = warp_sum(ssum);
+#pragma unroll
+    for (int m = 0; m < MZ; ++m) z[m] = lane + 32 * m < K ? z[m] / ssum : -2.0;
+    for (int rk = 0; rk < a.topk; ++rk) {
+      double best = -1.0;
+      int bi = 0x7fffffff;
+#pragma unroll
+      for (int m = 0; m < MZ; ++m)
+        if (z[m] > best) { best = z[m]; bi = lane + 32 * m; }
+      seg_argmax(best, bi, 32);
+      if (lane == 0) emit(a, l, n0 + r, rk, bi, best);
+#pragma unroll
+      for (int m = 0; m < MZ; ++m)
+        if (lane + 32 * m == bi) z[m] = -2.0;
+    }
+  }
+}
+
+// CTA = one (sequence, block of kRowsPerBlk query rows). Phase 1, one warp
+// per query row: scores q.k (ref predictor.py:249, unscaled) held in
+// registers, sparsemax threshold by Michelot's fixed point (the support of
+// the sorted closed form of ref numkit.py:42-60, tau = (sum_S z - 1)/|S|),
+// weights max(z - tau, 0), ctx = w V (dense over T; zero weights are exact
+// no-ops), residual + h2 (ref predictor.py:251-252) into smem. Phase 2: the L
+// heads for all rows of the block, softmax over K and top-k.
+__global__ void __launch_bounds__(32 * kAttnWarps, 1)
+attn_heads_kernel(const AttnArgs a) {
+  extern __shared__ double smem_d[];
+  const int H = a.dm.H, K = a.dm.K;
+  const int H3 = 3 * H;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int TS = a.ts;
+  double* s_kT = smem_d;                               // H x TS (transposed keys)
+  double* s_v = s_kT + (size_t)H * TS;                 // TS x H (values)
+  double* s_res = s_v + (size_t)H * TS;                // kRowsPerBlk x kResPitch
+  double* s_w = s_res + (size_t)kRowsPerBlk * kResPitch;  // per warp: kMaxLen weights
+  double* w_w = s_w + (size_t)wib * kMaxLen;
+
+  const int b = blockIdx.x;
+  if (b >= a.blk_off[a.n_seq]) return;
+  int lo = 0, hi = a.n_seq - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (a.blk_off[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  const int sq = lo;
+  const int base = a.seq_off[sq], T = a.seq_off[sq + 1] - base;
+  const int r0 = (b - a.blk_off[sq]) * kRowsPerBlk;
+  const int r1 = min(T, r0 + kRowsPerBlk);
+
+  unsigned long long ph[6] = {0, 0, 0, 0, 0, 0};
+  unsigned long long tk = clock64();
+  auto mark = [&](int i) {
+    if (a.prof) {
+      const unsigned long long t = clock64();
+      ph[i] += t - tk;
+      tk = t;
+    }
+  };
+
+  const bool staged = T <= TS;
+  if (staged) {
+    for (int i = threadIdx.x; i < H * T; i += blockDim.x) {
+      const int j = i / H, c = i % H;
+      s_kT[c * TS + j] = a.qkv[(size_t)(base + j) * H3 + H + c];
+      s_v[i] = a.qkv[(size_t)(base + j) * H3 + 2 * H + c];
+    }
+  }
+  __syncthreads();
+  mark(5);
+  const int nz = (T + 31) / 32;  // score registers in use per lane
+  for (int r = r0 + wib; r < r1; r += kAttnWarps) {
+    const int n = base + r;
+    const double* qrow = a.qkv + (size_t)n * H3;
+    // ---- scores: lane owns columns j = lane + 32 m
+    double z[kMaxZ];
+#pragma unroll
+    for (int m = 0; m < kMaxZ; ++m) z[m] = 0.0;
+    for (int c = 0; c < H; ++c) {
+      const double qc = qrow[c];  // uniform address: broadcast
+#pragma unroll
+      for (int m = 0; m < kMaxZ; ++m) {
+        const int j = lane + 32 * m;
+        if (m < nz && j < T) {
+          const double kv = staged ? s_kT[c * TS + j] : a.qkv[(size_t)(base + j) * H3 + H + c];
+          z[m] = fma(qc, kv, z[m]);
+        }
+      }
+    }
+    mark(0);
+    // ---- sparsemax threshold (Michelot): S_0 = all, tau_i = (sum_{S_i} z - 1)/|S_i|,
+    // S_{i+1} = {z > tau_i}, until the support stops shrinking
+    double tsum = 0.0;
+#pragma unroll
+    for (int m = 0; m < kMaxZ; ++m)
+      if (m < nz && lane + 32 * m < T) tsum += z[m];
+    tsum = warp_sum(tsum);
+    int cnt = T;
+    double tau = (tsum - 1.0) / (double)cnt;
+    for (int it = 0; it < T; ++it) {
       double ssum = 0.0;
-      for (int e = lane; e < dm.K; e += 32) {
-        const double ex = exp(s_z[e] - zmax);
-        s_z[e] = ex;
-        ssum += ex;
-      }
-      ssum = warp_sum(ssum);
-      __syncwarp();
-      for (int e = lane; e < dm.K; e += 32) s_z[e] = s_z[e] / ssum;
-      __syncwarp();
-      // top-k on probabilities, descending, ties to the lower index
-      for (int r = 0; r < topk; ++r) {
-        double best = -1.0;
-        int bi = 0x7fffffff;
-        for (int e = lane; e < dm.K; e += 32) {
-          const double pz = s_z[e];
-          if (pz > best) { best = pz; bi = e; }
-        }
+      int c = 0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      for (int m = 0; m < kMaxZ; ++m)
+        if (m < nz && lane + 32 * m < T && z[m] > tau) {
+          ssum += z[m];
+          ++c;
         }
-        if (lane == 0) {
-          const size_t at = ((size_t)l * n_tokens + n) * topk + r;
-          ids[at] = bi;
-          alpha[at] = best;
-          if (alpha_f32) alpha_f32[at] = (float)best;
-          s_z[bi] = -2.0;  // removed from later ranks
-        }
-        __syncwarp();
-      }
+      ssum = warp_sum(ssum);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (c == cnt) break;
+      cnt = c;
+      tau = (ssum - 1.0) / (double)cnt;
+    }
+    mark(2);
+    // ---- weights -> smem; ctx = w V with lanes over h, four chains over j
+#pragma unroll
+    for (int m = 0; m < kMaxZ; ++m) {
+      const int j = lane + 32 * m;
+      if (m < nz && j < T) w_w[j] = fmax(z[m] - tau, 0.0);
     }
     __syncwarp();
+    double c0[4] = {0.0, 0.0, 0.0, 0.0}, c1[4] = {0.0, 0.0, 0.0, 0.0};
+    const int h0 = lane, h1 = lane + 32;
+    int j = 0;
+    for (; j + 4 <= T; j += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double wj = w_w[j + u];
+        const double* vr = staged ? s_v + (size_t)(j + u) * H
+                                  : a.qkv + (size_t)(base + j + u) * H3 + 2 * H;
+        if (h0 < H) c0[u] = fma(wj, vr[h0], c0[u]);
+        if (h1 < H) c1[u] = fma(wj, vr[h1], c1[u]);
+      }
+    }
+    for (; j < T; ++j) {
+      const double wj = w_w[j];
+      const double* vr = staged ? s_v + (size_t)j * H : a.qkv + (size_t)(base + j) * H3 + 2 * H;
+      if (h0 < H) c0[0] = fma(wj, vr[h0], c0[0]);
+      if (h1 < H) c1[0] = fma(wj, vr[h1], c1[0]);
+    }
+    double* res = s_res + (r - r0) * kResPitch;
+    if (h0 < H) res[h0] = ((c0[0] + c0[1]) + (c0[2] + c0[3])) + a.h2[(size_t)n * H + h0];
+    if (h1 < H) res[h1] = ((c1[0] + c1[1]) + (c1[2] + c1[3])) + a.h2[(size_t)n * H + h1];
+    __syncwarp();
+    mark(3);
+  }
+  __syncthreads();
+  // ---- L heads over the block's rows
+  const int rows = r1 - r0;
+  if (K <= 8) heads_small<8>(a, s_res, rows, base + r0);
+  else if (K <= 16) heads_small<16>(a, s_res, rows, base + r0);
+  else if (K <= 32) heads_small<32>(a, s_res, rows, base + r0);
+  else if (K <= 64) heads_large<2>(a, s_res, rows, base + r0);
+  else if (K <= 128) heads_large<4>(a, s_res, rows, base + r0);
+  else if (K <= 256) heads_large<8>(a, s_res, rows, base + r0);
+  else heads_large<32>(a, s_res, rows, base + r0);
+  mark(4);
+  if (a.prof && lane == 0) {
+    unsigned long long* pr = a.prof + ((size_t)blockIdx.x * kAttnWarps + wib) * 8;
+    for (int i = 0; i < 6; ++i) pr[i] = ph[i];
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// Blocked (GEMM-shaped) attention + heads for sequences of T <= 128: one CTA
+// per (sequence, 64 query rows), 256 threads as a 16 x 16 grid with register
+// tiles, everything staged in smem:
+//   S  = Q K^T          (64 x T, 4 x 8 tile per thread, 48-long k loop)
+//   sparsemax rows      (warp per row, Michelot threshold; weights in place)
+//   R  = W V + h2       (64 x H, 4 x 3 tile per thread)
+//   Z  = R [heads]      (64 x L*K in layer chunks of <= 128 columns)
+//   softmax / top-k     (thread per (row, layer))
+// The arithmetic per element is the same as attn_heads_kernel; only the
+// schedule changes (independent accumulators instead of dependent chains).
+constexpr int kBR = 64;        // rows per block
+constexpr int kBT = 128;       // max keys
+constexpr int kQP = 49;        // pitch (doubles) of Q / K / R rows
+constexpr int kSP = kBT + 1;   // pitch of S / Z rows
+constexpr int kBlockSmem = (kBT * kQP + kBT * 48 + kBR * kQP + kBR * kSP) * 8;
+
+struct BlockArgs {
+  AttnArgs a;
+  const double* hwp;  // heads packed (H, L*K): hwp[i][l*K + e] = head_w[l][i][e]
+};
+
+__global__ void __launch_bounds__(256, 1)
+attn_block_kernel(const BlockArgs ba) {
+  const AttnArgs& a = ba.a;
+  extern __shared__ double smem_d[];
+  const int H = a.dm.H, K = a.dm.K, L = a.dm.L;
+  const int H3 = 3 * H;
+  double* sK = smem_d;                  // kBT x kQP   keys (row-major)
+  double* sV = sK + kBT * kQP;          // kBT x H     values
+  double* sQ = sV + kBT * 48;           // kBR x kQP   queries, later residuals
+  double* sS = sQ + kBR * kQP;          // kBR x kSP   scores -> weights -> logits
+  const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
+  const int tx = tid & 15, ty = tid >> 4;
+
+  const int b = blockIdx.x;
+  if (b >= a.blk_off[a.n_seq]) return;
+  int lo = 0, hi = a.n_seq - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (a.blk_off[mid] <= b) lo = mid; else hi = mid - 1;
+  }
+  const int base = a.seq_off[lo], T = a.seq_off[lo + 1] - base;
+  const int r0 = (b - a.blk_off[lo]) * kBR;
+  const int rows = min(T - r0, kBR);
+
+  for (int i = tid; i < T * H; i += 256) {
+    const int j = i / H, c = i % H;
+    const double* src = a.qkv + (size_t)(base + j) * H3;
+    sK[j * kQP + c] = src[H + c];
+    sV[j * 48 + c] = src[2 * H + c];
+  }
+  for (int i = tid; i < rows * H; i += 256) {
+    const int r = i / H, c = i % H;
+    sQ[r * kQP + c] = a.qkv[(size_t)(base + r0 + r) * H3 + c];
+  }
+  __syncthreads();
+
+  // ---- S = Q K^T: rows ty*4 + {0..3}, columns tx + 16 m (m < 8)
+  {
+    double acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
+    for (int c = 0; c < H; ++c) {
+      double q[4], k[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) q[i] = sQ[(ty * 4 + i) * kQP + c];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) k[m] = sK[(tx + 16 * m) * kQP + c];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[i][m] = fma(q[i], k[m], acc[i][m]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int m = 0; m < 8; ++m) sS[(ty * 4 + i) * kSP + tx + 16 * m] = acc[i][m];
+  }
+  __syncthreads();
+
+  // ---- sparsemax per row (warp per row): Michelot threshold, weights in place
+  for (int r = wib; r < rows; r += 8) {
+    double* srow = sS + r * kSP;
+    double z[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) z[m] = (lane + 32 * m < T) ? srow[lane + 32 * m] : 0.0;
+    double tsum = 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (lane + 32 * m < T) tsum += z[m];
+    tsum = warp_sum(tsum);
+    int cnt = T;
+    double tau = (tsum - 1.0) / (double)cnt;
+    for (int it = 0; it < T; ++it) {
+      double ssum = 0.0;
+      int cc = 0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        if (lane + 32 * m < T && z[m] > tau) {
+          ssum += z[m];
+          ++cc;
+        }
+      ssum = warp_sum(ssum);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cc += __shfl_xor_sync(0xffffffffu, cc, o);
+      if (cc == cnt) break;
+      cnt = cc;
+      tau = (ssum - 1.0) / (double)cnt;
+    }
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const int j = lane + 32 * m;
+      if (j < kBT) srow[j] = (j < T) ? fmax(z[m] - tau, 0.0) : 0.0;
+    }
+  }
+  __syncthreads();
+
+  // ---- R = W V + h2: rows ty*4 + {0..3}, columns tx + 16 m (m < 3)
+  {
+    double acc[4][3];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) acc[i][m] = 0.0;
+    for (int j = 0; j < T; ++j) {
+      double w[4], v[3];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) w[i] = sS[(ty * 4 + i) * kSP + j];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) v[m] = (tx + 16 * m < H) ? sV[j * 48 + tx + 16 * m] : 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) acc[i][m] = fma(w[i], v[m], acc[i][m]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = ty * 4 + i;
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const int c = tx + 16 * m;
+        if (r < rows && c < H) sQ[r * kQP + c] = acc[i][m] + a.h2[(size_t)(base + r0 + r) * H + c];
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- heads in chunks of layers (<= 128 logit columns per chunk)
+  const int lpc = max(1, kBT / K);  // layers per chunk
+  for (int l0 = 0; l0 < L; l0 += lpc) {
+    const int nl = min(lpc, L - l0);
+    const int ncol = nl * K;
+    // Z = R hw[:, l0*K : (l0+nl)*K]: rows ty*4+i, columns tx + 16 m (m < 8)
+    {
+      double acc[4][8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
+      const double* W = ba.hwp + (size_t)l0 * K;
+      const int LK = L * K;
+      for (int c = 0; c < H; ++c) {
+        double rr[4], w[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) rr[i] = sQ[(ty * 4 + i) * kQP + c];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) w[m] = (tx + 16 * m < ncol) ? W[(size_t)c * LK + tx + 16 * m] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int m = 0; m < 8; ++m) acc[i][m] = fma(rr[i], w[m], acc[i][m]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int m = 0; m < 8; ++m) sS[(ty * 4 + i) * kSP + tx + 16 * m] = acc[i][m];
+    }
+    __syncthreads();
+    // softmax over K + top-k per (row, layer)
+    for (int pr = tid; pr < rows * nl; pr += 256) {
+      const int r = pr / nl, l = l0 + pr % nl;
+      double* z = sS + r * kSP + (l - l0) * K;
+      const double* hb = a.hb + (size_t)l * K;
+      double zmax = -INFINITY;
+      for (int e = 0; e < K; ++e) {
+        z[e] += hb[e];
+        zmax = fmax(zmax, z[e]);
+      }
+      double ssum = 0.0;
+      for (int e = 0; e < K; ++e) {
+        z[e] = exp(z[e] - zmax);
+        ssum += z[e];
+      }
+      for (int e = 0; e < K; ++e) z[e] = z[e] / ssum;
+      for (int rk = 0; rk < a.topk; ++rk) {
+        double best = -1.0;
+        int bi = 0;
+        for (int e = 0; e < K; ++e)
+          if (z[e] > best) { best = z[e]; bi = e; }
+        emit(a, l, base + r0 + r, rk, bi, best);
+        z[bi] = -2.0;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -342,6 +771,21 @@ using namespace sida;
 using namespace sida::hash;
 
 static size_t ws_align(size_t b) { return align_up(b, 256); }
+static unsigned long long* g_hash_prof = nullptr;
+static size_t g_hash_prof_n = 0;
+
+// Observability: phase cycles of the last attention/heads launch when run with
+// SIDA_HASH_PROF=1: out[6] = summed (scores, sort, support, ctx, heads, setup).
+extern "C" int sida_debug_hash_prof(unsigned long long* out) {
+  SIDA_REQUIRE(g_hash_prof, SIDA_ERR_UNSUPPORTED, "run with SIDA_HASH_PROF=1");
+  SIDA_CUDA(cudaDeviceSynchronize());
+  std::vector<unsigned long long> h(g_hash_prof_n);
+  SIDA_CUDA(cudaMemcpy(h.data(), g_hash_prof, g_hash_prof_n * 8, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < 6; ++i) out[i] = 0;
+  for (size_t w = 0; w < g_hash_prof_n / 8; ++w)
+    for (int i = 0; i < 6; ++i) out[i] += h[w * 8 + i];
+  return SIDA_OK;
+}
 
 extern "C" size_t sida_hash_param_count(int d, int cd, int H, int L, int K) {
   const size_t G = 4ull * H;
@@ -349,105 +793,230 @@ extern "C" size_t sida_hash_param_count(int d, int cd, int H, int L, int K) {
          3ull * H * H + (size_t)L * H * K + (size_t)L * K;
 }
 
-extern "C" size_t sida_hash_workspace_bytes(int n_tokens, int n_seq, int max_len, int d, int cd,
-                                            int H, int L, int K) {
-  (void)n_seq; (void)max_len; (void)d; (void)cd; (void)L; (void)K;
-  const size_t n = (size_t)n_tokens;
-  return ws_align(n * 4 * H * 8) + 5 * ws_align(n * H * 8);
+extern "C" size_t sida_hash_tables_count(int vocab, int max_len, int H, int L, int K) {
+  return ((size_t)vocab + max_len + 1) * 4 * H + 3ull * H * H + (size_t)H * L * K;
 }
 
-template <int MAXH>
-static int launch_lstm(const double* xw, const double* wh, const double* b, const int32_t* seq_off,
-                       int n_seq, int H, double* h_out, cudaStream_t s) {
+struct TablePtrs {
+  const double *tokx, *posx, *cx, *wqkv, *hwp;
+};
+
+static TablePtrs carve_tables(const double* t, int vocab, int max_len, int H) {
+  const size_t G = 4ull * H;
+  TablePtrs r;
+  r.tokx = t;
+  r.posx = t + (size_t)vocab * G;
+  r.cx = r.posx + (size_t)max_len * G;
+  r.wqkv = r.cx + G;
+  r.hwp = r.wqkv + 3ull * H * H;
+  return r;
+}
+
+// Fold the compress FC and the layer-1 input projection into per-vocabulary
+// and per-position tables (see the header comment), and pack [Wq|Wk|Wv].
+// tok_emb / pos_emb may be NULL (vocab = max_len = 0) for the embed_fn path.
+extern "C" int sida_hash_prepare(const double* params, const uint16_t* tok_emb,
+                                 const uint16_t* pos_emb, int vocab, int max_len, int d, int cd,
+                                 int H, int L, int K, double* tables, void* stream) {
+  SIDA_REQUIRE(H >= 1 && H <= 64 && cd >= 1 && cd <= 64, SIDA_ERR_UNSUPPORTED,
+               "predictor dims cd=%d H=%d outside the kernel contract (<= 64)", cd, H);
+  SIDA_REQUIRE(params && tables && vocab >= 0 && max_len >= 0, SIDA_ERR_CONTRACT,
+               "bad hash_prepare arguments");
+  cudaStream_t s = as_stream(stream);
+  Dims dm{d, cd, H, L, K};
+  ParamPtrs w = carve(params, dm);
+  const int G = 4 * H;
+  TablePtrs t = carve_tables(tables, vocab, max_len, H);
+  if (vocab > 0) {
+    project_rows_kernel<<<ceil_div(vocab, 8), 256, 0, s>>>(tok_emb, nullptr, vocab, dm, w.cw,
+                                                           nullptr, w.wx1,
+                                                           const_cast<double*>(t.tokx));
+    SIDA_LAUNCH_CHECK();
+  }
+  if (max_len > 0) {
+    project_rows_kernel<<<ceil_div(max_len, 8), 256, 0, s>>>(pos_emb, nullptr, max_len, dm, w.cw,
+                                                             nullptr, w.wx1,
+                                                             const_cast<double*>(t.posx));
+    SIDA_LAUNCH_CHECK();
+  }
+  bias_project_kernel<<<ceil_div(G, 128), 128, 0, s>>>(w.cb, w.wx1, cd, G,
+                                                       const_cast<double*>(t.cx));
+  SIDA_LAUNCH_CHECK();
+  for (int l = 0; l < L; ++l)  // heads packed (H, L*K)
+    SIDA_CUDA(cudaMemcpy2DAsync(const_cast<double*>(t.hwp) + (size_t)l * K,
+                                (size_t)L * K * sizeof(double), w.hw + (size_t)l * H * K,
+                                K * sizeof(double), K * sizeof(double), H,
+                                cudaMemcpyDeviceToDevice, s));
+  for (int m = 0; m < 3; ++m) {  // [Wq | Wk | Wv] as one (H x 3H) matrix
+    const double* src = m == 0 ? w.wq : (m == 1 ? w.wk : w.wv);
+    SIDA_CUDA(cudaMemcpy2DAsync(const_cast<double*>(t.wqkv) + m * H, 3 * H * sizeof(double), src,
+                                H * sizeof(double), H * sizeof(double), H,
+                                cudaMemcpyDeviceToDevice, s));
+  }
+  return SIDA_OK;
+}
+
+extern "C" size_t sida_hash_workspace_bytes(int n_tokens, int n_seq, int max_len, int d, int cd,
+                                            int H, int L, int K) {
+  (void)max_len; (void)d; (void)cd; (void)L; (void)K;
+  const size_t n = (size_t)n_tokens;
+  return ws_align(n * 4 * H * 8) + 2 * ws_align(n * H * 8) + ws_align(n * 3 * H * 8) +
+         ws_align(((size_t)n_seq + 1) * 4) + 256;
+}
+
+template <int MAXH, bool FOLD>
+static int launch_lstm(const double* xw, const double* tokx, const double* posx, const double* cx,
+                       const int32_t* tokens, const double* wh, const double* b,
+                       const int32_t* seq_off, int n_seq, int H, double* h_out, cudaStream_t s) {
   int S = 1;
   if (n_seq >= 4 * kNumSMs) S = 4;
   else if (n_seq >= 2 * kNumSMs) S = 2;
   if (S == 4)
-    lstm_kernel<MAXH, 4><<<ceil_div(n_seq, 4), 4 * MAXH, 0, s>>>(xw, wh, b, seq_off, n_seq, H, h_out);
+    lstm_kernel<MAXH, 4, FOLD><<<ceil_div(n_seq, 4), 4 * MAXH, 0, s>>>(
+        xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out);
   else if (S == 2)
-    lstm_kernel<MAXH, 2><<<ceil_div(n_seq, 2), 4 * MAXH, 0, s>>>(xw, wh, b, seq_off, n_seq, H, h_out);
+    lstm_kernel<MAXH, 2, FOLD><<<ceil_div(n_seq, 2), 4 * MAXH, 0, s>>>(
+        xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out);
   else
-    lstm_kernel<MAXH, 1><<<n_seq, 4 * MAXH, 0, s>>>(xw, wh, b, seq_off, n_seq, H, h_out);
+    lstm_kernel<MAXH, 1, FOLD><<<n_seq, 4 * MAXH, 0, s>>>(xw, tokx, posx, cx, tokens, wh, b,
+                                                          seq_off, n_seq, H, h_out);
   SIDA_LAUNCH_CHECK();
   return SIDA_OK;
 }
 
-static int lstm_dispatch(const double* xw, const double* wh, const double* b,
-                         const int32_t* seq_off, int n_seq, int H, double* h_out, cudaStream_t s) {
-  if (H <= 16) return launch_lstm<16>(xw, wh, b, seq_off, n_seq, H, h_out, s);
-  if (H <= 32) return launch_lstm<32>(xw, wh, b, seq_off, n_seq, H, h_out, s);
-  if (H <= 48) return launch_lstm<48>(xw, wh, b, seq_off, n_seq, H, h_out, s);
-  return launch_lstm<64>(xw, wh, b, seq_off, n_seq, H, h_out, s);
+template <bool FOLD>
+static int lstm_dispatch(const double* xw, const double* tokx, const double* posx,
+                         const double* cx, const int32_t* tokens, const double* wh,
+                         const double* b, const int32_t* seq_off, int n_seq, int H, double* h_out,
+                         cudaStream_t s) {
+  if (H <= 16) return launch_lstm<16, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s);
+  if (H <= 32) return launch_lstm<32, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s);
+  if (H <= 48) return launch_lstm<48, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s);
+  return launch_lstm<64, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s);
 }
 
 static int rows_gemm(const double* A, int n, int Kd, const double* B, int M, double* C,
                      cudaStream_t s) {
-  const size_t smem = (size_t)Kd * M * sizeof(double);
+  SIDA_REQUIRE(M >= 1 && M <= 192, SIDA_ERR_UNSUPPORTED, "rows_gemm width %d", M);
+  const size_t smem = ((size_t)Kd * M + (size_t)kRG_Rows * (Kd + 1)) * sizeof(double);
   static size_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
     SIDA_CUDA(cudaFuncSetAttribute(rows_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     configured = smem;
   }
-  rows_gemm_kernel<<<ceil_div(n, 16), 256, smem, s>>>(A, n, Kd, B, M, C);
+  rows_gemm_kernel<<<ceil_div(n, kRG_Rows), 256, smem, s>>>(A, n, Kd, B, M, C);
   SIDA_LAUNCH_CHECK();
   return SIDA_OK;
 }
 
-extern "C" int sida_hash_forward(const double* params, const uint16_t* tok_emb,
-                                 const uint16_t* pos_emb, const double* emb_f64,
-                                 const int32_t* tokens,
-                                 const int32_t* seq_off, int n_seq, int n_tokens, int max_len,
-                                 int d, int cd, int H, int L, int K, int topk, int32_t* ids,
-                                 double* alpha, float* alpha_f32, void* workspace,
-                                 size_t workspace_bytes, void* stream) {
+// blk_off[i] = sum_{s < i} ceil(len_s / 32)   (attention CTA -> sequence map)
+__global__ void block_offsets_kernel(const int32_t* __restrict__ seq_off, int n_seq,
+                                     int32_t* __restrict__ blk_off) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int acc = 0;
+  for (int i = 0; i < n_seq; ++i) {
+    blk_off[i] = acc;
+    acc += (seq_off[i + 1] - seq_off[i] + kRowsPerBlk - 1) / kRowsPerBlk;
+  }
+  blk_off[n_seq] = acc;
+}
+
+extern "C" int sida_hash_forward(const double* params, const double* tables, int vocab,
+                                 int table_max_len, const double* emb_f64,
+                                 const int32_t* tokens, const int32_t* seq_off, int n_seq,
+                                 int n_tokens, int max_len, int d, int cd, int H, int L, int K,
+                                 int topk, int32_t* ids, double* alpha, float* alpha_f32,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
   SIDA_REQUIRE(topk >= 1 && topk <= K, SIDA_ERR_CONTRACT, "eval_top_k=%d out of range for K=%d",
                topk, K);
   SIDA_REQUIRE(n_seq >= 1 && n_tokens >= n_seq, SIDA_ERR_CONTRACT, "empty batch or sequence");
-  SIDA_REQUIRE(H >= 1 && H <= 64 && cd >= 1 && cd <= 64, SIDA_ERR_UNSUPPORTED,
-               "predictor dims cd=%d H=%d outside the kernel contract (<= 64)", cd, H);
+  SIDA_REQUIRE(H >= 1 && H <= 48 && cd >= 1 && cd <= 64, SIDA_ERR_UNSUPPORTED,
+               "predictor dims cd=%d H=%d outside the kernel contract (H <= 48)", cd, H);
   SIDA_REQUIRE(max_len <= kMaxLen, SIDA_ERR_UNSUPPORTED, "sequence length %d > %d", max_len,
                kMaxLen);
   SIDA_REQUIRE(K <= kMaxK, SIDA_ERR_UNSUPPORTED, "K=%d > %d", K, kMaxK);
+  SIDA_REQUIRE(tables && (emb_f64 || (tokens && vocab > 0 && table_max_len >= max_len)),
+               SIDA_ERR_CONTRACT, "hash needs prepared tables and embeddings or tokens");
   SIDA_REQUIRE(workspace_bytes >= sida_hash_workspace_bytes(n_tokens, n_seq, max_len, d, cd, H, L, K),
                SIDA_ERR_CONTRACT, "hash workspace too small");
   cudaStream_t s = as_stream(stream);
   Dims dm{d, cd, H, L, K};
   ParamPtrs w = carve(params, dm);
+  TablePtrs tb = carve_tables(tables, emb_f64 ? 0 : vocab, emb_f64 ? 0 : table_max_len, H);
+  const int G = 4 * H;
   const size_t n = (size_t)n_tokens;
   char* ws = static_cast<char*>(workspace);
-  double* xw = reinterpret_cast<double*>(ws);
-  ws += ws_align(n * 4 * H * 8);
+  double* xw = reinterpret_cast<double*>(ws); ws += ws_align(n * G * 8);
   double* h1 = reinterpret_cast<double*>(ws); ws += ws_align(n * H * 8);
   double* h2 = reinterpret_cast<double*>(ws); ws += ws_align(n * H * 8);
-  double* qb = reinterpret_cast<double*>(ws); ws += ws_align(n * H * 8);
-  double* kb = reinterpret_cast<double*>(ws); ws += ws_align(n * H * 8);
-  double* vb = reinterpret_cast<double*>(ws);
+  double* qkv = reinterpret_cast<double*>(ws); ws += ws_align(n * 3 * H * 8);
+  int32_t* blk_off = reinterpret_cast<int32_t*>(ws);
 
-  SIDA_REQUIRE(emb_f64 || (tok_emb && pos_emb && tokens), SIDA_ERR_CONTRACT,
-               "hash needs either embeddings or (tables, tokens)");
-  embed_xw1_kernel<<<ceil_div(n_tokens, 8), 256, 0, s>>>(tok_emb, pos_emb, emb_f64, tokens, seq_off,
-                                                         n_seq, n_tokens, dm, w, xw);
-  SIDA_LAUNCH_CHECK();
-  int st = lstm_dispatch(xw, w.wh1, w.b1, seq_off, n_seq, H, h1, s);
+  int st;
+  if (emb_f64) {
+    project_rows_kernel<<<ceil_div(n_tokens, 8), 256, 0, s>>>(nullptr, emb_f64, n_tokens, dm, w.cw,
+                                                              w.cb, w.wx1, xw);
+    SIDA_LAUNCH_CHECK();
+    st = lstm_dispatch<false>(xw, nullptr, nullptr, nullptr, nullptr, w.wh1, w.b1, seq_off, n_seq,
+                              H, h1, s);
+  } else {
+    st = lstm_dispatch<true>(nullptr, tb.tokx, tb.posx, tb.cx, tokens, w.wh1, w.b1, seq_off,
+                             n_seq, H, h1, s);
+  }
   if (st) return st;
-  if ((st = rows_gemm(h1, n_tokens, H, w.wx2, 4 * H, xw, s))) return st;
-  if ((st = lstm_dispatch(xw, w.wh2, w.b2, seq_off, n_seq, H, h2, s))) return st;
-  if ((st = rows_gemm(h2, n_tokens, H, w.wq, H, qb, s))) return st;
-  if ((st = rows_gemm(h2, n_tokens, H, w.wk, H, kb, s))) return st;
-  if ((st = rows_gemm(h2, n_tokens, H, w.wv, H, vb, s))) return st;
+  if ((st = rows_gemm(h1, n_tokens, H, w.wx2, G, xw, s))) return st;
+  if ((st = lstm_dispatch<false>(xw, nullptr, nullptr, nullptr, nullptr, w.wh2, w.b2, seq_off,
+                                 n_seq, H, h2, s)))
+    return st;
+  if ((st = rows_gemm(h2, n_tokens, H, tb.wqkv, 3 * H, qkv, s))) return st;
+  block_offsets_kernel<<<1, 32, 0, s>>>(seq_off, n_seq, blk_off);
+  SIDA_LAUNCH_CHECK();
 
-  const size_t smem = (size_t)kAttnWarps * (2 * kMaxLen + 64 + K) * sizeof(double);
+  AttnArgs a;
+  a.qkv = qkv; a.h2 = h2; a.seq_off = seq_off; a.blk_off = blk_off;
+  a.n_seq = n_seq; a.n_tokens = n_tokens; a.dm = dm; a.hw = w.hw; a.hb = w.hb; a.topk = topk;
+  a.ids = ids; a.alpha = alpha; a.alpha_f32 = alpha_f32;
+  a.prof = nullptr;
+  const int n_blocks_ub = ceil_div(n_tokens, kRowsPerBlk) + n_seq;
+  if (getenv("SIDA_HASH_PROF")) {
+    static unsigned long long* buf = nullptr;
+    static size_t cap = 0;
+    const size_t need = (size_t)n_blocks_ub * kAttnWarps * 8;
+    if (need > cap) {
+      if (buf) cudaFree(buf);
+      cudaMalloc(&buf, need * sizeof(unsigned long long));
+      cap = need;
+    }
+    cudaMemsetAsync(buf, 0, need * sizeof(unsigned long long), s);
+    a.prof = buf;
+    g_hash_prof = buf;
+    g_hash_prof_n = need;
+  }
+  a.ts = max_len <= 256 ? max_len : 0;
+  const size_t smem = ((size_t)2 * H * a.ts + (size_t)kRowsPerBlk * kResPitch +
+                       (size_t)kAttnWarps * kMaxLen) * sizeof(double);
   static size_t configured = 0;
   if (smem > configured) {
     SIDA_CUDA(cudaFuncSetAttribute(attn_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     configured = smem;
   }
-  const int blocks = std::min(ceil_div(n_tokens, kAttnWarps), kNumSMs * 8);
-  attn_heads_kernel<<<blocks, 32 * kAttnWarps, smem, s>>>(qb, kb, vb, h2, seq_off, n_seq, n_tokens,
-                                                          dm, w.hw, w.hb, topk, ids, alpha,
-                                                          alpha_f32);
+  if (max_len <= kBT && K <= kBT && H <= 48 && !a.prof) {
+    // blocked path: register-tiled fp64 GEMM shapes, one CTA per 64 rows
+    static bool cfg_block = false;
+    if (!cfg_block) {
+      SIDA_CUDA(cudaFuncSetAttribute(attn_block_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
+      cfg_block = true;
+    }
+    BlockArgs ba{a, tb.hwp};
+    attn_block_kernel<<<n_blocks_ub, 256, kBlockSmem, s>>>(ba);
+    SIDA_LAUNCH_CHECK();
+    return SIDA_OK;
+  }
+  const int blocks = n_blocks_ub;  // >= sum ceil(len/kRowsPerBlk)
+  attn_heads_kernel<<<blocks, 32 * kAttnWarps, smem, s>>>(a);
   SIDA_LAUNCH_CHECK();
   return SIDA_OK;
 }

@@ -102,6 +102,36 @@ class PredictorNet:
             self._packed[key] = torch.from_numpy(flat).to(device)
         return self._packed[key]
 
+    def tables(self, model, device, stream):
+        """Per-model folding tables of sida_hash_prepare (cached): the compress
+        FC and layer-1 input projection folded into vocabulary / position rows
+        of ``model``'s bf16 embedding tables (``model`` None: the caller-
+        embedding path, which only needs the bias row and packed [Wq|Wk|Wv]).
+        Returns (tables, vocab, max_len)."""
+        key = (str(device), id(model))
+        hit = self._tables.get(key) if hasattr(self, "_tables") else None
+        if hit is not None and hit[0] is model:
+            return hit[1], hit[2], hit[3]
+        if not hasattr(self, "_tables"):
+            self._tables = {}
+        h = _lib.lib()
+        c = self.config
+        vocab = model.config.vocab_size if model is not None else 0
+        tmax = model.config.max_seq_len if model is not None else 0
+        if model is not None and model.config.d_model != self.d_model:
+            raise ContractError("predictor d_model does not match the model")
+        n = h.sida_hash_tables_count(vocab, tmax, c.lstm_hidden, self.num_moe_layers,
+                                     self.num_experts)
+        tab = torch.empty(n, dtype=torch.float64, device=device)
+        with torch.cuda.stream(stream):
+            _lib.check(h.sida_hash_prepare(
+                self.packed(device).data_ptr(), _lib.ptr(model.tok_emb) if model else None,
+                _lib.ptr(model.pos_emb) if model else None, vocab, tmax, self.d_model,
+                c.compress_dim, c.lstm_hidden, self.num_moe_layers, self.num_experts,
+                tab.data_ptr(), stream.cuda_stream))
+        self._tables[key] = (model, tab, vocab, tmax)
+        return tab, vocab, tmax
+
 
 class DeviceTable:
     """Device half of an ExpertHashTable: ids/alphas plus the per-layer
@@ -325,9 +355,9 @@ def hash_device(predictor: PredictorNet, model: MoEModel | None, tokens, lengths
                                                c.compress_dim, c.lstm_hidden, L, K)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
         params = predictor.packed(device)
+        tables, vocab, tmax = predictor.tables(model, device, st)
         _lib.check(h.sida_hash_forward(
-            params.data_ptr(), _lib.ptr(model.tok_emb) if use_tables else None,
-            _lib.ptr(model.pos_emb) if use_tables else None, _lib.ptr(emb), _lib.ptr(tokens),
+            params.data_ptr(), tables.data_ptr(), vocab, tmax, _lib.ptr(emb), _lib.ptr(tokens),
             seq_off.data_ptr(), n_seq, n_tok, max_len, predictor.d_model, c.compress_dim,
             c.lstm_hidden, L, K, eval_top_k, ids.data_ptr(), alpha.data_ptr(),
             alpha_f32.data_ptr(), ws.data_ptr(), ws_bytes, st.cuda_stream))
