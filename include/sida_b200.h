@@ -123,7 +123,9 @@ int sida_gather_rows_bf16(const float* x, const int32_t* perm, int n_rows, int k
  * run in waves).
  * row_map (n_rows, optional; identity if NULL): output row of permuted row p.
  * alpha (n_rows, optional; 1 if NULL), resid (optional, indexed like out).
- * out: float32, row stride d. hidden: bf16 workspace (n_rows, h).
+ * out: float32, row stride d; out_bf16 (optional): the same rows rounded to
+ * bf16 (the next layer's GEMM input, saving a conversion pass).
+ * hidden: bf16 workspace (n_rows, h).
  * Requires d % 64 == 0, h % 64 == 0.
  * ------------------------------------------------------------------- */
 size_t sida_slot_bytes(int d, int h);
@@ -131,7 +133,8 @@ int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h, cons
                           int num_experts, const int32_t* expert_slot, const int32_t* expert_list,
                           int n_list, const void* arena, size_t slot_stride, int n_slots,
                           const int32_t* row_map, const float* alpha, const float* resid,
-                          float* out, uint16_t* hidden, int32_t* err_flag, void* stream);
+                          float* out, uint16_t* out_bf16, uint16_t* hidden, int32_t* err_flag,
+                          void* stream);
 
 /* Observability: per-CTA cycle counters of the last sida_grouped_ffn_bf16
  * call when the process runs with SIDA_GEMM_PROF=1 (producer wait, MMA wait
@@ -150,7 +153,7 @@ int sida_grouped_ffn_f32(const float* x_perm, int n_rows, int d, int h, const in
 /* k > 1 combine: out[t] = resid[t] + sum_{r=0..k-1} y[t*k + r] (ranks in
  * order, ref moe.py:252-262). */
 int sida_combine_ranks(const float* y, const float* resid, int n_tokens, int k, int d, float* out,
-                       void* stream);
+                       uint16_t* out_bf16, void* stream);
 
 /* ---------------------------------------------------------------------
  * (2) Expert streaming: one pinned-host expert image -> one HBM slot on the

@@ -37,11 +37,11 @@ SIGNATURES = {
     "sida_gather_rows_bf16": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
     "sida_slot_bytes": (_sz, [_i, _i]),
     "sida_grouped_ffn_bf16": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _i, _vp, _sz, _i, _vp, _vp,
-                                   _vp, _vp, _vp, _vp, _vp]),
+                                   _vp, _vp, _vp, _vp, _vp, _vp]),
     "sida_debug_gemm_prof": (_i, [_vp]),
     "sida_grouped_ffn_f32": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp, _vp]),
-    "sida_combine_ranks": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
+    "sida_combine_ranks": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "sida_expert_copy": (_i, [_vp, _vp, _sz, _vp, _vp, _vp]),
     "sida_pack_expert_host": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp]),
     "sida_plan_placement": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp]),

@@ -78,6 +78,7 @@ struct GemmParams {
   const float* alpha;
   const float* resid;
   float* out;
+  uint16_t* out_bf16;          // GEMM2: optional bf16 copy of out (next layer's GEMM input)
   int32_t* err_flag;
   unsigned long long* prof;    // optional per-CTA cycle counters (sida_debug_gemm_prof)
 };
@@ -553,6 +554,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 o.x = x.x + o.x; o.y = x.y + o.y; o.z = x.z + o.z; o.w = x.w + o.w;
               }
               *reinterpret_cast<float4*>(p.out + at) = o;
+              if (p.out_bf16) {
+                uint2 ob;
+                ob.x = bf16x2_rn(o.x, o.y);
+                ob.y = bf16x2_rn(o.z, o.w);
+                *reinterpret_cast<uint2*>(p.out_bf16 + at) = ob;
+              }
             }
           }
           __syncwarp();
@@ -737,7 +744,8 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
                                      const int32_t* expert_slot, const int32_t* expert_list,
                                      int n_list, const void* arena, size_t slot_stride,
                                      int n_slots, const int32_t* row_map, const float* alpha,
-                                     const float* resid, float* out, uint16_t* hidden,
+                                     const float* resid, float* out, uint16_t* out_bf16,
+                                     uint16_t* hidden,
                                      int32_t* err_flag, void* stream) {
   SIDA_REQUIRE(d % 64 == 0 && h % 64 == 0, SIDA_ERR_UNSUPPORTED,
                "tcgen05 FFN needs d, h multiples of 64 (d=%d h=%d)", d, h);
@@ -768,6 +776,7 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   sm100::GemmParams p2 = p1;
   p2.kdim = h; p2.ndim = d; p2.bias_off = b2_off;
   p2.row_map = row_map; p2.alpha = alpha; p2.resid = resid; p2.out = out;
+  p2.out_bf16 = out_bf16;
   p2.prof = prof_buffer(1);
   return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, listed, cg, s);
 }

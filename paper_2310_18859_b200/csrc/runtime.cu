@@ -82,7 +82,8 @@ extern "C" int sida_pack_expert_host(const double* w1, const double* b1, const d
 // k > 1 rank combine: out[t] = resid[t] + sum_r y[t*k + r], ranks in order
 // (ref moe.py:252-262 accumulates rank outputs in order then adds x).
 __global__ void combine_ranks_kernel(const float4* __restrict__ y, const float4* __restrict__ resid,
-                                     int n_tokens, int k, int d4, float4* __restrict__ out) {
+                                     int n_tokens, int k, int d4, float4* __restrict__ out,
+                                     uint2* __restrict__ out_bf16) {
   long total = (long)n_tokens * d4;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total;
        i += (long)gridDim.x * blockDim.x) {
@@ -98,11 +99,13 @@ __global__ void combine_ranks_kernel(const float4* __restrict__ y, const float4*
       acc.x = x.x + acc.x; acc.y = x.y + acc.y; acc.z = x.z + acc.z; acc.w = x.w + acc.w;
     }
     out[t * d4 + c] = acc;
+    if (out_bf16) out_bf16[t * d4 + c] = make_uint2(sida::pack_bf16x2(acc.x, acc.y),
+                                                   sida::pack_bf16x2(acc.z, acc.w));
   }
 }
 
 extern "C" int sida_combine_ranks(const float* y, const float* resid, int n_tokens, int k, int d,
-                                  float* out, void* stream) {
+                                  float* out, uint16_t* out_bf16, void* stream) {
   SIDA_REQUIRE(d % 4 == 0 && k >= 1 && n_tokens >= 0, SIDA_ERR_UNSUPPORTED,
                "combine needs d %% 4 == 0 (d=%d) and k >= 1", d);
   if (n_tokens == 0) return SIDA_OK;
@@ -110,7 +113,7 @@ extern "C" int sida_combine_ranks(const float* y, const float* resid, int n_toke
   int blocks = (int)std::min<long>((total + 255) / 256, sida::kNumSMs * 8);
   combine_ranks_kernel<<<blocks, 256, 0, sida::as_stream(stream)>>>(
       reinterpret_cast<const float4*>(y), reinterpret_cast<const float4*>(resid), n_tokens, k,
-      d / 4, reinterpret_cast<float4*>(out));
+      d / 4, reinterpret_cast<float4*>(out), reinterpret_cast<uint2*>(out_bf16));
   SIDA_LAUNCH_CHECK();
   return SIDA_OK;
 }

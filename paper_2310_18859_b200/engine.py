@@ -130,21 +130,24 @@ class SidaEngine:
         with torch.cuda.stream(cs):
             lay = BatchLayout(list(lengths), tokens_dev, model.device)
             x = model.embed_layout(lay)
+            xb = None  # bf16 copy of x for the next attention GEMM (FFN epilogue output)
             for layer in range(n_layers):
                 if not issued[layer]:
                     issue(layer)
                 if (self.prefetch == "layer" and layer + 1 < n_layers
                         and plan.groups[layer + 1].prefetchable and not issued[layer + 1]):
                     issue(layer + 1)
-                x = model.attention_mix(layer, x, lay)
+                x = model.attention_mix(layer, x, lay, xb=xb)
                 if self.ffn_events is not None:
                     e_a = torch.cuda.Event(enable_timing=True)
                     e_a.record(cs)
+                xb = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
                 if len(waves[layer]) == 1:
-                    x = run_waves(model, waves[layer], x, dt, store, cs, pre_done=[done[layer]])
+                    x = run_waves(model, waves[layer], x, dt, store, cs, pre_done=[done[layer]],
+                                  out_bf16=xb)
                 else:
                     x = run_waves(model, waves[layer], x, dt, store, cs,
-                                  issue=lambda w: store.enqueue_loads(w.loads))
+                                  issue=lambda w: store.enqueue_loads(w.loads), out_bf16=xb)
                 if self.ffn_events is not None:
                     e_b = torch.cuda.Event(enable_timing=True)
                     e_b.record(cs)

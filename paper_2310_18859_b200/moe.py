@@ -333,24 +333,33 @@ class MoEModel:
         return (self.tok_emb.index_select(0, lay.tokens.long()).float()
                 + self.pos_emb.index_select(0, lay.pos).float())
 
-    def attention_mix(self, layer: int, x: torch.Tensor, lay: BatchLayout) -> torch.Tensor:
-        """x + softmax(q k^T / sqrt(d)) v W_o per sequence (ref moe.py:220-233)."""
+    def attention_mix(self, layer: int, x: torch.Tensor, lay: BatchLayout,
+                      xb: torch.Tensor | None = None) -> torch.Tensor:
+        """x + softmax(q k^T / sqrt(d)) v W_o per sequence (ref moe.py:220-233).
+
+        cuBLAS bf16 GEMMs with fp32 outputs where the result stays fp32:
+        scores (bmm, out_dtype fp32) and the output projection fused with the
+        residual add (addmm, beta = 1). ``xb`` is x already rounded to bf16
+        (the previous layer's FFN epilogue writes it)."""
         d = self.config.d_model
-        qkv = x.to(torch.bfloat16) @ self.wqkv[layer]
+        if xb is None:
+            xb = x.to(torch.bfloat16)
+        qkv = xb @ self.wqkv[layer]
         if lay.uniform:
             qkv = qkv.view(lay.n_seq, lay.max_len, 3 * d)
         else:
             qkv = torch.cat([qkv, qkv.new_zeros(1, 3 * d)]).index_select(0, lay.pad_index)
             qkv = qkv.view(lay.n_seq, lay.max_len, 3 * d)
         q, k, v = qkv.split(d, dim=2)
-        scores = torch.bmm(q, k.transpose(1, 2)).float() * (1.0 / math.sqrt(d))
+        scores = torch.bmm(q, k.transpose(1, 2), out_dtype=torch.float32)
+        scores.div_(math.sqrt(d))
         if not lay.uniform:
-            scores = scores + lay.key_mask
+            scores.add_(lay.key_mask)
         attn = torch.softmax(scores, dim=-1).to(torch.bfloat16)
         ctx = torch.bmm(attn, v).reshape(-1, d)
         if not lay.uniform:
             ctx = ctx.index_select(0, lay.valid_rows)
-        return x + (ctx @ self.wo[layer]).float()
+        return torch.addmm(x, ctx, self.wo[layer], out_dtype=torch.float32)
 
     def pool_classify(self, x: torch.Tensor, lay: BatchLayout) -> torch.Tensor:
         """(n_seq, C): per-sequence mean then the classifier (ref moe.py:264-266)."""
@@ -363,15 +372,17 @@ class MoEModel:
 
     def moe_apply_rows(self, layer_tables, x: torch.Tensor, k: int, arena, slot_row: torch.Tensor,
                        expert_list: torch.Tensor | None = None, out: torch.Tensor | None = None,
-                       y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                       y: torch.Tensor | None = None, stream=None,
+                       out_bf16: torch.Tensor | None = None) -> torch.Tensor:
         """The SiDA expert FFN for one layer over the whole batch.
 
         ``layer_tables`` = (off (K+1,), perm (R,), alpha_perm (R,)) of this
         layer from sida_permute_hist; ``slot_row`` (K,) int32 expert -> slot.
         k == 1: out[t] = x[t] + alpha * f(x[t]) written by the GEMM2
-        epilogue directly (unpermute + residual fused). k > 1: the epilogue
-        writes alpha_r f_r into row t*k+r of ``y`` and sida_combine_ranks adds
-        the ranks in order plus the residual (ref moe.py:252-262).
+        epilogue directly (unpermute + residual fused), plus its bf16 copy in
+        ``out_bf16`` when given. k > 1: the epilogue writes alpha_r f_r into
+        row t*k+r of ``y`` and sida_combine_ranks adds the ranks in order plus
+        the residual (ref moe.py:252-262).
         """
         c = self.config
         h = _lib.lib()
@@ -398,17 +409,19 @@ class MoEModel:
             x_perm.data_ptr(), rows, c.d_model, c.expert_hidden, off.data_ptr(), c.num_experts,
             slot_row.data_ptr(), _lib.ptr(expert_list), n_list, arena.base_ptr,
             arena.slot_stride, arena.n_slots, perm.data_ptr(), alpha_perm.data_ptr(),
-            _lib.ptr(resid), target.data_ptr(), hidden.data_ptr(), err.data_ptr(), sh))
-        return target if k == 1 else target
+            _lib.ptr(resid), target.data_ptr(), _lib.ptr(out_bf16 if k == 1 else None),
+            hidden.data_ptr(), err.data_ptr(), sh))
+        return target
 
     def combine(self, y: torch.Tensor, x: torch.Tensor, k: int, out: torch.Tensor | None = None,
-                stream=None) -> torch.Tensor:
+                stream=None, out_bf16: torch.Tensor | None = None) -> torch.Tensor:
         h = _lib.lib()
         st = torch.cuda.current_stream(self.device) if stream is None else stream
         if out is None:
             out = torch.empty_like(x)
         _lib.check(h.sida_combine_ranks(y.data_ptr(), x.data_ptr(), x.shape[0], k,
-                                        self.config.d_model, out.data_ptr(), st.cuda_stream))
+                                        self.config.d_model, out.data_ptr(), _lib.ptr(out_bf16),
+                                        st.cuda_stream))
         return out
 
 

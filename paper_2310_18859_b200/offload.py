@@ -292,7 +292,8 @@ class ExpertStore:
             self._reader[int(s)] = event
 
     # -- one layer, every required expert resident (model_forward path) ---------------
-    def run_layer(self, model, layer: int, x: torch.Tensor, dev_table, stream=None):
+    def run_layer(self, model, layer: int, x: torch.Tensor, dev_table, stream=None,
+                  out_bf16=None):
         st = stream or torch.cuda.current_stream(model.device)
         table_hist = dev_table.hist
         dev_table.ready.synchronize()
@@ -302,15 +303,17 @@ class ExpertStore:
                  if (layer, e) not in self.slot_of]
         done = self.enqueue_loads(loads)
         wave = Wave(layer, loads, need, self.slot_row(layer, need))
-        return run_waves(model, [wave], x, dev_table, self, st, pre_done=[done])
+        return run_waves(model, [wave], x, dev_table, self, st, pre_done=[done],
+                         out_bf16=out_bf16)
 
 
 def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=None,
-              issue=None):
+              issue=None, out_bf16=None):
     """Execute one layer as a sequence of waves on ``stream``: wait for each
     wave's copies, run the grouped FFN over its experts, record the reader
     event. ``issue(wave)`` (optional) enqueues a wave's copies just in time and
-    returns their done event."""
+    returns their done event. ``out_bf16`` (optional) receives the layer
+    output rounded to bf16 from the same epilogue."""
     c = model.config
     k = dev_table.k
     layer = waves[0].layer
@@ -333,11 +336,11 @@ def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=N
                 elist = torch.from_numpy(np.asarray(wave.experts, dtype=np.int32)).pin_memory().to(
                     x.device, non_blocking=True)
             model.moe_apply_rows(tables, x, k, store, row, expert_list=elist, out=out, y=y,
-                                 stream=stream)
+                                 stream=stream, out_bf16=out_bf16)
         ev = torch.cuda.Event()
         ev.record(stream)
         store.mark_read(wave.slot_row, ev)
     if k > 1:
         with torch.cuda.stream(stream):
-            out = model.combine(y, x, k, out=out, stream=stream)
+            out = model.combine(y, x, k, out=out, stream=stream, out_bf16=out_bf16)
     return out

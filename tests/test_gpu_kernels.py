@@ -155,7 +155,11 @@ def test_grouped_ffn_bf16_vs_oracle(cuda_device, d, hdim, K, N, k):
     dt = table.on_device(model)
     store = ExpertStore.full(model)
     xt = torch.from_numpy(x).float().cuda()
-    out = store.run_layer(model, 0, xt, dt).cpu().numpy()
+    ob = torch.empty((N, d), dtype=torch.bfloat16, device="cuda")
+    out_t = store.run_layer(model, 0, xt, dt, out_bf16=ob)
+    if k == 1:
+        assert torch.equal(ob, out_t.bfloat16())
+    out = out_t.cpu().numpy()
     ref = omoe.moe_apply_grouped(params, 0, x.astype(np.float32).astype(np.float64), ids[0],
                                  alphas[0])
     close_rms(out, ref, 2e-2)
@@ -192,7 +196,10 @@ def test_grouped_ffn_f32_check_path(cuda_device, d, hdim, K, N, k):
                                     pm.data_ptr(), ap.data_ptr(), None, y.data_ptr(),
                                     hid.data_ptr(), s))
     out = torch.empty((N, d), device=dev)
-    _l.check(h.sida_combine_ranks(y.data_ptr(), xt.data_ptr(), N, k, d, out.data_ptr(), s))
+    ob = torch.empty((N, d), dtype=torch.bfloat16, device=dev)
+    _l.check(h.sida_combine_ranks(y.data_ptr(), xt.data_ptr(), N, k, d, out.data_ptr(),
+                                  ob.data_ptr(), s))
+    assert torch.equal(ob, out.bfloat16())
     ref = omoe.moe_apply_grouped(params, 0, x, ids[0], alphas[0])
     close_rms(out.cpu().numpy(), ref, 1e-4)
 
