@@ -148,60 +148,57 @@ def run_reference(args):
 
 # ------------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + clock-event (throttle) reasons sampled every 5 ms through NVML
+    during the timed region (the same fields as the recipe's nvidia-smi line)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.005):
         self.index = index
-        self.proc = None
-        self.lines: list[str] = []
+        self.period = period_s
+        self.samples: list[tuple[int, int, int]] = []
+        self._stop = threading.Event()
+        self._t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
-        except FileNotFoundError:
-            self.proc = None
+        except Exception:  # no NVML: the line then reports zero samples
+            self._t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self._nvml
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.samples.append((sm, self._max, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self._t is not None:
+            self._t.join(timeout=2)
 
     def summary(self):
-        sms, maxes, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sms.append(float(parts[0]))
-                maxes.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sms:
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sms)), "sm_max_mhz": max(maxes),
-                "reasons": sorted(reasons), "samples": len(sms)}
+        reasons = sorted({n for _, _, r in self.samples for n, bit in self.REASONS.items()
+                          if r & bit})
+        return {"sm_mhz": float(np.median([s for s, _, _ in self.samples])),
+                "sm_max_mhz": max(m for _, m, _ in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------------- GPU
@@ -306,6 +303,10 @@ def run_ours(args):
     # ---- roofline of the dominant kernel: grouped FFN (gather + GEMM1 + GEMM2)
     peaks = measured_peaks()
     flops = 4.0 * n_tok * cfg.d_model * cfg.expert_hidden   # per layer launch set
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "r1", "ffn_traffic.json")
+    if os.path.exists(tpath) and n_tok == 32768 and cfg.num_experts == 8:
+        traffic = json.load(open(tpath))["traffic_bytes_per_launch_set"]
     ffn_avg_ms = float(np.mean(ffn_ms))
     achieved = flops / (ffn_avg_ms / 1e3) / 1e12
     peak = peaks.get("bf16_tflops_sustained", 1373.4)
@@ -338,7 +339,7 @@ def run_ours(args):
                           "loads_timed": rep.expert_loads},
         "roofline": {"kernel": "grouped_ffn (row gather + tcgen05 GEMM1 + GEMM2, per layer)",
                      "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "flops_per_launch": flops, "avg_ms": ffn_avg_ms,
                      "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms},

@@ -121,10 +121,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-// arrive on the barrier at shared::cluster address `caddr` (possibly remote)
+// arrive on the barrier at shared::cluster address `caddr` (possibly remote).
+// Default (CTA-scope release) semantics: the epilogue's global stores need no
+// ordering against the MMA, and the TMEM reads are ordered by
+// tcgen05.fence::before_thread_sync; a .release.cluster arrive would add an
+// ERRBAR that stalls every epilogue warp until its stores drain.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr)
-               : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -541,16 +544,27 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           __syncwarp();
           // read back: lane -> (row = i*4 + lane/8, chunk = lane%8); residual
           // and unpermute (row_map) applied per row segment
+          // all eight residual loads in flight before any store (MLP 8)
+          size_t at8[8];
+          float4 x8[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), q = lane & 7;
             const int orow_r = __shfl_sync(0xffffffffu, orow, r);
+            at8[i] = static_cast<size_t>(orow_r) * p.ndim + col0 + q * 4;
+            x8[i] = (p.resid && qrow0 + r < ti.row_end)
+                        ? __ldg(reinterpret_cast<const float4*>(p.resid + at8[i]))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + (lane >> 3), q = lane & 7;
             const uint4 raw = reinterpret_cast<const uint4*>(stile + r * 128)[q ^ (r & 7)];
             if (qrow0 + r < ti.row_end) {
               float4 o = *reinterpret_cast<const float4*>(&raw);
-              const size_t at = static_cast<size_t>(orow_r) * p.ndim + col0 + q * 4;
+              const size_t at = at8[i];
               if (p.resid) {
-                const float4 x = __ldg(reinterpret_cast<const float4*>(p.resid + at));
+                const float4 x = x8[i];
                 o.x = x.x + o.x; o.y = x.y + o.y; o.z = x.z + o.z; o.w = x.w + o.w;
               }
               *reinterpret_cast<float4*>(p.out + at) = o;
