@@ -276,7 +276,9 @@ def run_ours(args):
     sampler.__exit__()
     ms = ev_start.elapsed_time(ev_end)
     ffn_ms = [a.elapsed_time(b) for a, b, _ in engine.ffn_events]
+    mix_ms = [a.elapsed_time(b) for a, b in engine.mix_events]
     engine.ffn_events = None
+    engine.mix_events = []
     if ws > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -342,7 +344,8 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "flops_per_launch": flops, "avg_ms": ffn_avg_ms,
-                     "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms},
+                     "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms,
+                     "attention_mix_avg_ms": float(np.mean(mix_ms)) if mix_ms else None},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": n_tok * 4 + (B + 1) * 4,
                 "d2h_bytes_per_step": B * cfg.num_classes * 4 + cfg.num_layers * cfg.num_experts * 4,

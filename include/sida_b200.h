@@ -150,6 +150,16 @@ int sida_grouped_ffn_f32(const float* x_perm, int n_rows, int d, int h, const in
                          const float* b2, const int32_t* row_map, const float* alpha,
                          const float* resid, float* out, float* hidden, void* stream);
 
+/* Expert parallelism: regroup received bf16 rows
+ * (dst[p] = src[idx[p]]) and combine expert outputs returned in the source
+ * rank's permuted order: out[t] = resid[t] + sum_r alpha_perm[p] y_perm[p],
+ * p = inv[t*k + r], ranks in order; out_bf16 optional. */
+int sida_gather_bf16_rows(const uint16_t* src, const int32_t* idx, int n_rows, int d,
+                          uint16_t* dst, void* stream);
+int sida_unpermute_combine(const uint16_t* y_perm, const int32_t* inv, const float* alpha_perm,
+                           const float* resid, int n_tokens, int k, int d, float* out,
+                           uint16_t* out_bf16, void* stream);
+
 /* k > 1 combine: out[t] = resid[t] + sum_{r=0..k-1} y[t*k + r] (ranks in
  * order, ref moe.py:252-262). */
 int sida_combine_ranks(const float* y, const float* resid, int n_tokens, int k, int d, float* out,

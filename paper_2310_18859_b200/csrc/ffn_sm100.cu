@@ -567,7 +567,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 const float4 x = x8[i];
                 o.x = x.x + o.x; o.y = x.y + o.y; o.z = x.z + o.z; o.w = x.w + o.w;
               }
-              *reinterpret_cast<float4*>(p.out + at) = o;
+              if (p.out) *reinterpret_cast<float4*>(p.out + at) = o;
               if (p.out_bf16) {
                 uint2 ob;
                 ob.x = bf16x2_rn(o.x, o.y);
@@ -770,7 +770,7 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
                sm100::kMaxListed);
   SIDA_REQUIRE(slot_stride % 16 == 0 && slot_stride >= sida_slot_bytes(d, h), SIDA_ERR_CONTRACT,
                "slot stride %zu invalid", slot_stride);
-  SIDA_REQUIRE(err_flag && out && hidden && x_perm && off && expert_slot && arena,
+  SIDA_REQUIRE(err_flag && (out || out_bf16) && hidden && x_perm && off && expert_slot && arena,
                SIDA_ERR_CONTRACT, "null pointer passed to sida_grouped_ffn_bf16");
   if (n_rows == 0 || listed == 0) return SIDA_OK;
   cudaStream_t s = as_stream(stream);

@@ -218,6 +218,77 @@ extern "C" int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, i
   return SIDA_OK;
 }
 
+// dst[p] = src[idx[p]] for bf16 rows (16-byte vectors): the expert-parallel
+// regroup of received rows into local expert-major order.
+__global__ void __launch_bounds__(256)
+gather_bf16_rows_kernel(const uint4* __restrict__ src, const int32_t* __restrict__ idx, int n_rows,
+                        int d8, uint4* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < n_rows; p += warps) {
+    const uint4* s = src + (size_t)idx[p] * d8;
+    uint4* o = dst + (size_t)p * d8;
+    for (int c = lane; c < d8; c += 32) o[c] = __ldg(s + c);
+  }
+}
+
+// out[t] = resid[t] + sum_{r<k} alpha_perm[inv[t*k+r]] * y_perm[inv[t*k+r]] (ranks in
+// order, ref moe.py:252-262): the combine of expert-parallel outputs that
+// come back in the source rank's permuted row order. One warp per token.
+__global__ void __launch_bounds__(256)
+unpermute_combine_kernel(const uint16_t* __restrict__ y_perm, const int32_t* __restrict__ inv,
+                         const float* __restrict__ alpha_perm, const float* __restrict__ resid,
+                         int n_tokens, int k, int d, float* __restrict__ out,
+                         uint16_t* __restrict__ out_bf16) {
+  const int lane = threadIdx.x & 31;
+  const int warps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tokens; t += warps) {
+    for (int c = lane * 4; c < d; c += 128) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int r = 0; r < k; ++r) {
+        const int p = inv[(size_t)t * k + r];
+        const float a = alpha_perm[p];
+        const uint2 raw = *reinterpret_cast<const uint2*>(y_perm + (size_t)p * d + c);
+        acc.x += a * bf16_to_f32(static_cast<uint16_t>(raw.x & 0xFFFF));
+        acc.y += a * bf16_to_f32(static_cast<uint16_t>(raw.x >> 16));
+        acc.z += a * bf16_to_f32(static_cast<uint16_t>(raw.y & 0xFFFF));
+        acc.w += a * bf16_to_f32(static_cast<uint16_t>(raw.y >> 16));
+      }
+      const float4 x = *reinterpret_cast<const float4*>(resid + (size_t)t * d + c);
+      const float4 o = make_float4(x.x + acc.x, x.y + acc.y, x.z + acc.z, x.w + acc.w);
+      *reinterpret_cast<float4*>(out + (size_t)t * d + c) = o;
+      if (out_bf16)
+        *reinterpret_cast<uint2*>(out_bf16 + (size_t)t * d + c) =
+            make_uint2(pack_bf16x2(o.x, o.y), pack_bf16x2(o.z, o.w));
+    }
+  }
+}
+
+extern "C" int sida_gather_bf16_rows(const uint16_t* src, const int32_t* idx, int n_rows, int d,
+                                     uint16_t* dst, void* stream) {
+  SIDA_REQUIRE(d % 8 == 0, SIDA_ERR_UNSUPPORTED, "bf16 gather needs d %% 8 == 0 (d=%d)", d);
+  if (n_rows == 0) return SIDA_OK;
+  const int blocks = std::min(ceil_div(n_rows, 8), kNumSMs * 16);
+  gather_bf16_rows_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const uint4*>(src), idx, n_rows, d / 8, reinterpret_cast<uint4*>(dst));
+  SIDA_LAUNCH_CHECK();
+  return SIDA_OK;
+}
+
+extern "C" int sida_unpermute_combine(const uint16_t* y_perm, const int32_t* inv,
+                                      const float* alpha_perm, const float* resid, int n_tokens,
+                                      int k, int d, float* out, uint16_t* out_bf16, void* stream) {
+  SIDA_REQUIRE(d % 4 == 0 && k >= 1, SIDA_ERR_UNSUPPORTED, "combine needs d %% 4 == 0 (d=%d)", d);
+  SIDA_REQUIRE(y_perm && inv && alpha_perm && resid && out, SIDA_ERR_CONTRACT,
+               "null pointer passed to sida_unpermute_combine");
+  if (n_tokens == 0) return SIDA_OK;
+  const int blocks = std::min(ceil_div(n_tokens, 8), kNumSMs * 16);
+  unpermute_combine_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      y_perm, inv, alpha_perm, resid, n_tokens, k, d, out, out_bf16);
+  SIDA_LAUNCH_CHECK();
+  return SIDA_OK;
+}
+
 extern "C" int sida_gather_rows_bf16(const float* x, const int32_t* perm, int n_rows, int k, int d,
                                      uint16_t* x_perm, void* stream) {
   SIDA_REQUIRE(d % 8 == 0, SIDA_ERR_UNSUPPORTED, "gather needs d %% 8 == 0 (d=%d)", d);

@@ -14,6 +14,7 @@ hash stream one batch ahead.
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -74,13 +75,19 @@ class SidaEngine:
         self.eval_top_k = eval_top_k
         self.prefetch = prefetch
         dev = model.device
-        self.hash_stream, self.compute_stream = streams or (torch.cuda.Stream(device=dev),
-                                                            torch.cuda.Stream(device=dev))
+        # compute at the highest stream priority: the persistent GEMM grids get
+        # SMs first; the hash (one batch ahead) fills what is left
+        lo, hi = torch.cuda.Stream.priority_range()
+        if os.environ.get("SIDA_FLAT_PRIORITY"):  # A/B switch for measurements
+            lo = hi = 0
+        self.hash_stream, self.compute_stream = streams or (
+            torch.cuda.Stream(device=dev, priority=lo), torch.cuda.Stream(device=dev, priority=hi))
         self.store = store or ExpertStore.for_budget(model, budget)
         self.state = getattr(self.store, "residency_state", None) or ResidencyState()
         self.store.residency_state = self.state
         self.peak = 0
         self.ffn_events: list | None = None  # set to a list to time every layer's FFN
+        self.mix_events: list = []           # (filled alongside ffn_events) attention_mix
 
     # -- hash stream ------------------------------------------------------------------
     def hash_tokens(self, batch_id: int, tokens_dev: torch.Tensor, lengths) -> ExpertHashTable:
@@ -137,10 +144,14 @@ class SidaEngine:
                 if (self.prefetch == "layer" and layer + 1 < n_layers
                         and plan.groups[layer + 1].prefetchable and not issued[layer + 1]):
                     issue(layer + 1)
+                if self.ffn_events is not None:
+                    e_m = torch.cuda.Event(enable_timing=True)
+                    e_m.record(cs)
                 x = model.attention_mix(layer, x, lay, xb=xb)
                 if self.ffn_events is not None:
                     e_a = torch.cuda.Event(enable_timing=True)
                     e_a.record(cs)
+                    self.mix_events.append((e_m, e_a))
                 xb = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
                 if len(waves[layer]) == 1:
                     x = run_waves(model, waves[layer], x, dt, store, cs, pre_done=[done[layer]],

@@ -1,0 +1,102 @@
+"""Expert-parallel host logic: split sizes and the regroup map
+against brute force, and the transport over a world_size-2 gloo group on CPU.
+The GPU data path with real kernels is tests/test_gpu_expert_parallel.py."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2310_18859_b200.errors import ContractError
+from paper_2310_18859_b200.expert_parallel import GlooTransport, ep_regroup, ep_splits
+
+
+def _brute(counts, layer, rank, world):
+    K = counts.shape[2]
+    kl = K // world
+    # receive buffer: for each source g, its rows for my experts, expert ascending
+    recv = [(g, e) for g in range(world) for e in range(rank * kl, (rank + 1) * kl)
+            for _ in range(counts[g, layer, e])]
+    order = sorted(range(len(recv)), key=lambda i: (recv[i][1], recv[i][0], i))
+    return np.array(order, dtype=np.int32)
+
+
+@pytest.mark.parametrize("world,K", [(2, 8), (4, 8), (8, 128), (1, 4)])
+def test_splits_and_regroup_match_brute_force(world, K):
+    g = np.random.default_rng(world * K)
+    L = 3
+    counts = g.integers(0, 6, size=(world, L, K))
+    counts[0, 1, :] = 0  # a rank that routes nothing in one layer
+    for rank in range(world):
+        for layer in range(L):
+            send, recv = ep_splits(counts, layer, rank, world)
+            kl = K // world
+            assert send.sum() == counts[rank, layer].sum()
+            for r2 in range(world):  # what r2 receives from me == what I send to r2
+                assert ep_splits(counts, layer, r2, world)[1][rank] == send[r2]
+            src, off = ep_regroup(counts, layer, rank, world)
+            np.testing.assert_array_equal(src, _brute(counts, layer, rank, world))
+            assert off[-1] == recv.sum() == src.size
+            np.testing.assert_array_equal(np.diff(off),
+                                          counts[:, layer, rank * kl:(rank + 1) * kl].sum(0))
+
+
+def test_uneven_expert_split_is_rejected():
+    with pytest.raises(ContractError):
+        ep_splits(np.zeros((3, 1, 8), dtype=np.int64), 0, 0, 3)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _transport_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr = GlooTransport()
+        hist = torch.full((2, 4), rank, dtype=torch.int32)
+        allh = tr.all_gather(hist)
+        assert allh.shape == (world, 2, 4) and int(allh[1, 0, 0]) == 1
+        # rank r sends (r+1)*(g+1) rows to rank g; rows carry (src, dst, i) in bf16 bits
+        send_rows = [(rank + 1) * (g + 1) for g in range(world)]
+        recv_rows = [(g + 1) * (rank + 1) for g in range(world)]
+        rows = []
+        for g in range(world):
+            for i in range(send_rows[g]):
+                rows.append([rank, g, i, 0])
+        send = torch.tensor(rows, dtype=torch.float32).to(torch.bfloat16)
+        recv = tr.all_to_all(send, send_rows, recv_rows)
+        assert recv.dtype == torch.bfloat16
+        got = recv.float().numpy()
+        pos = 0
+        for g in range(world):
+            for i in range(recv_rows[g]):
+                assert list(got[pos][:3]) == [g, rank, i]
+                pos += 1
+        q.put((rank, "ok"))
+    except Exception as exc:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_transport_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transport_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}

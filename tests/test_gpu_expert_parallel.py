@@ -1,0 +1,82 @@
+"""Expert parallelism with the real kernels: two ranks share cuda:0 and talk
+through the gloo transport (the box has one GPU; NCCL needs distinct GPUs).
+Each rank serves its own batch; its logits must match the single-GPU engine
+on the same tokens (the only difference is the bf16 transport of expert
+outputs, so the bar is the bf16 layer bar, rtol 2e-2)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from oracle import moe as omoe
+        from oracle import predictor as opred
+        from paper_2310_18859_b200 import MemoryBudget, MoEConfig, MoEModel, PredictorConfig
+        from paper_2310_18859_b200 import PredictorNet
+        from paper_2310_18859_b200.engine import SidaEngine
+        from paper_2310_18859_b200.expert_parallel import ExpertParallelEngine, GlooTransport
+
+        shape = omoe.MoEShape(vocab_size=512, d_model=256, num_layers=2, num_experts=8,
+                              expert_hidden=1024, max_seq_len=128)
+        params = omoe.bf16_params(omoe.init_params(shape, 0))
+        model = MoEModel(MoEConfig(**shape.__dict__), params=params)
+        pp = opred.init_params(opred.PredictorShape(256, 2, 8), 1)
+        net = PredictorNet(PredictorConfig(), 256, 2, 8, params=pp)
+        eb = model.expert_bytes_each()
+        g = torch.Generator(device="cuda").manual_seed(100 + rank)
+        B, T = 3 + rank, 64
+        lengths = [T] * B
+        toks = torch.randint(0, 512, (B * T,), generator=g, device="cuda", dtype=torch.int32)
+
+        ep = ExpertParallelEngine(model, net, MemoryBudget(8 * eb), transport=GlooTransport())
+        table = ep.hash_tokens(0, toks, lengths)
+        got = ep.forward(table, lengths, tokens_dev=toks)
+        torch.cuda.synchronize()
+        single = SidaEngine(model, net, MemoryBudget(16 * eb))
+        t2 = single.hash_tokens(0, toks, lengths)
+        ref, _, _ = single.forward(t2, lengths, tokens_dev=toks)
+        torch.cuda.synchronize()
+        got, ref = got.cpu().numpy(), ref.cpu().numpy()
+        rms = float(np.sqrt(np.mean(ref ** 2)))
+        err = float(np.max(np.abs(got - ref) - 2e-2 * np.abs(ref)) / rms)
+        q.put((rank, "ok" if err <= 2e-2 else f"logits off by {err:.3e} rms"))
+    except Exception as exc:  # pragma: no cover - reported to the parent
+        import traceback
+
+        q.put((rank, traceback.format_exc()[-800:]))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_expert_parallel_two_ranks_one_gpu(cuda_device):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
