@@ -53,6 +53,10 @@ def parse():
                    help="HBM expert budget as a fraction of all expert bytes")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--parallel", default="dp", choices=["dp", "ep"],
+                   help="N>1: data-parallel replicas (default) or expert parallel over NCCL")
+    p.add_argument("--no-streaming", action="store_true",
+                   help="skip the H2D-link / budget-limited streaming measurement")
     return p.parse_args()
 
 
@@ -209,6 +213,58 @@ def measured_peaks():
         return {}
 
 
+def measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms, steps=3):
+    """Expert streaming evidence: the pinned-host -> HBM link
+    measured with the engine's own copy entry point (sida_expert_copy), and a
+    budget-limited serving run (half of the 96 experts fit, so every batch
+    streams experts) whose step time is compared with the all-resident run."""
+    import torch
+
+    from paper_2310_18859_b200 import MemoryBudget, _lib
+    from paper_2310_18859_b200.engine import SidaEngine
+
+    h = _lib.lib()
+    eb = model.expert_bytes_each()
+    dst = torch.empty(8 * eb, dtype=torch.uint8, device=model.device)
+    cs = torch.cuda.Stream(device=model.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 4
+    for it in range(reps + 1):
+        if it == 1:
+            e0.record(cs)
+        for i in range(8):
+            src = model.expert_images[i]
+            _lib.check(h.sida_expert_copy(dst.data_ptr() + i * eb, src.data_ptr(), eb,
+                                          cs.cuda_stream, None, None))
+    e1.record(cs)
+    torch.cuda.synchronize()
+    h2d_gbs = reps * 8 * eb / (e0.elapsed_time(e1) / 1e3) / 1e9
+    n_all = cfg.num_layers * cfg.num_experts
+    eng = SidaEngine(model, pred, MemoryBudget((n_all // 2) * eb), eval_top_k=1)
+    tables = {0: eng.hash_tokens(0, toks[0], lengths)}
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    loads0 = 0
+    for j in range(steps + 1):
+        if j == 1:
+            torch.cuda.synchronize()
+            loads0 = eng.store.bytes_loaded
+            s0.record(eng.compute_stream)
+        tables[j + 1] = eng.hash_tokens(j + 1, toks[(j + 1) % len(toks)], lengths)
+        eng.forward(tables.pop(j), lengths, tokens_dev=toks[j % len(toks)])
+    s1.record(eng.compute_stream)
+    torch.cuda.synchronize()
+    b_ms = s0.elapsed_time(s1) / steps
+    loaded = (eng.store.bytes_loaded - loads0) / steps
+    return {"h2d_link_gbs": h2d_gbs, "h2d_source": "pinned host -> HBM, 8 expert images x 4 "
+            "via sida_expert_copy on one stream", "budget_slots": n_all // 2,
+            "budget_tokens_per_s": n_tok / (b_ms / 1e3), "budget_ms_per_step": b_ms,
+            "expert_bytes_loaded_per_step": loaded,
+            "copy_ms_at_link_rate": loaded / (h2d_gbs * 1e9) * 1e3,
+            "exposed_ms_per_step": b_ms - step_ms,
+            "note": "uniform random routing activates all 8 experts of every layer in every "
+                    "32K-token batch, so half a budget reloads ~half the experts per step"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -234,10 +290,18 @@ def run_ours(args):
     model = MoEModel.synthetic(cfg, seed=0, device=dev)
     pred = PredictorNet(PredictorConfig(), cfg.d_model, cfg.num_layers, cfg.num_experts, Rng(1))
     eb = model.expert_bytes_each()
-    n_all = cfg.num_layers * cfg.num_experts
+    ep_mode = args.parallel == "ep" and ws > 1
+    n_all = cfg.num_layers * cfg.num_experts // (ws if ep_mode else 1)
     slots = max(1, int(round(args.budget_frac * n_all)))
     budget = MemoryBudget(slots * eb)
-    engine = SidaEngine(model, pred, budget, eval_top_k=1)
+    if ep_mode:
+        from paper_2310_18859_b200.expert_parallel import ExpertParallelEngine
+
+        engine = ExpertParallelEngine(model, pred, budget)
+        engine.compute_stream = engine.base.compute_stream
+        engine.ffn_events, engine.mix_events = None, []
+    else:
+        engine = SidaEngine(model, pred, budget, eval_top_k=1)
     B, T = args.batch, args.seq
     n_tok = B * T
     lengths = [T] * B
@@ -263,19 +327,20 @@ def run_ours(args):
     for j in range(n_steps):
         if j == args.warmup:
             barrier()
-            engine.ffn_events = []
+            if not ep_mode:
+                engine.ffn_events = []
             ev_start.record(cs)
             sampler.__enter__()
             t_wall0 = time.perf_counter()
         tables[j + 1] = engine.hash_tokens(j + 1, toks[j + 1], lengths)
-        logits, rec, _ = engine.forward(tables.pop(j), lengths, tokens_dev=toks[j])
-        outs.append(logits)
+        out = engine.forward(tables.pop(j), lengths, tokens_dev=toks[j])
+        outs.append(out if ep_mode else out[0])
     ev_end.record(cs)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_wall0
     sampler.__exit__()
     ms = ev_start.elapsed_time(ev_end)
-    ffn_ms = [a.elapsed_time(b) for a, b, _ in engine.ffn_events]
+    ffn_ms = [a.elapsed_time(b) for a, b, _ in (engine.ffn_events or [])]
     mix_ms = [a.elapsed_time(b) for a, b in engine.mix_events]
     engine.ffn_events = None
     engine.mix_events = []
@@ -286,21 +351,30 @@ def run_ours(args):
     value = ws * args.steps * n_tok / (ms / 1e3)
 
     # ---- e2e through the public API: host SequenceBatches in, host logits out
-    rng = np.random.default_rng(99 + rank)
-    host_batches = [SequenceBatch(i, [rng.integers(0, cfg.vocab_size, size=T) for _ in range(B)])
-                    for i in range(n_steps)]
-    serve_sida(model, pred, host_batches[: args.warmup], budget, engine=engine)
-    barrier()
-    t0 = time.perf_counter()
-    rep = serve_sida(model, pred, [SequenceBatch(i, b.sequences) for i, b in
-                                   enumerate(host_batches[args.warmup:])], budget, engine=engine)
-    barrier()
-    e2e_s = time.perf_counter() - t0
-    if ws > 1:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = ws * args.steps * n_tok / e2e_s
+    e2e, rep = None, None
+    if not ep_mode:
+        rng = np.random.default_rng(99 + rank)
+        host_batches = [SequenceBatch(i, [rng.integers(0, cfg.vocab_size, size=T)
+                                          for _ in range(B)]) for i in range(n_steps)]
+        serve_sida(model, pred, host_batches[: args.warmup], budget, engine=engine)
+        barrier()
+        t0 = time.perf_counter()
+        rep = serve_sida(model, pred, [SequenceBatch(i, b.sequences) for i, b in
+                                       enumerate(host_batches[args.warmup:])], budget,
+                         engine=engine)
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = ws * args.steps * n_tok / e2e_s
+
+    # ---- expert streaming: pinned H2D link bandwidth, then a budget-limited
+    # run (half of the experts fit) to expose how much copy time is hidden
+    streaming = None
+    if not ep_mode and not args.no_streaming:
+        streaming = measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms=ms / args.steps)
 
     # ---- roofline of the dominant kernel: grouped FFN (gather + GEMM1 + GEMM2)
     peaks = measured_peaks()
@@ -309,12 +383,14 @@ def run_ours(args):
     tpath = os.path.join(REPO, "profiles", "r1", "ffn_traffic.json")
     if os.path.exists(tpath) and n_tok == 32768 and cfg.num_experts == 8:
         traffic = json.load(open(tpath))["traffic_bytes_per_launch_set"]
-    ffn_avg_ms = float(np.mean(ffn_ms))
-    achieved = flops / (ffn_avg_ms / 1e3) / 1e12
+    ffn_avg_ms = float(np.mean(ffn_ms)) if ffn_ms else None
+    achieved = flops / (ffn_avg_ms / 1e3) / 1e12 if ffn_avg_ms else None
     peak = peaks.get("bf16_tflops_sustained", 1373.4)
     step_ms = ms / args.steps
     clocks = sampler.summary()
-    launches_per_step = 8 + 3 + cfg.num_layers * 3  # hash 8, permute 3, per layer gather+2 GEMMs
+    # hash: lstm x2, rows_gemm x2, block offsets, attention; permute: 3; per layer:
+    # gather + GEMM1 + GEMM2 (+ EP: regroup + combine)
+    launches_per_step = 6 + 3 + cfg.num_layers * (5 if ep_mode else 3)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, work, detail = cpu_sample(dict(BASE8, num_experts=args.experts), T, args.cpu_steps)
@@ -333,18 +409,20 @@ def run_ours(args):
                    "tokens_per_step_per_gpu": n_tok, "layers": cfg.num_layers,
                    "experts": cfg.num_experts, "d_model": cfg.d_model,
                    "expert_hidden": cfg.expert_hidden, "top_k": 1,
-                   "hbm_budget_slots": slots, "parallelism": f"replicas{ws}",
+                   "hbm_budget_slots": slots,
+                   "parallelism": f"ep{ws}" if ep_mode else f"replicas{ws}",
                    "l2_note": "per-step working set (activations 32768x768 fp32 + bf16 hidden "
                               "32768x3072 = 300 MB) exceeds the 126 MB L2"},
         "expert_memory": {"footprint_bytes": footprint, "slots": engine.store.peak_slots,
                           "slot_bytes": eb, "all_expert_bytes": model.total_expert_bytes(),
-                          "loads_timed": rep.expert_loads},
+                          "loads_timed": rep.expert_loads if rep else None},
+        "expert_streaming": streaming,
         "roofline": {"kernel": "grouped_ffn (row gather + tcgen05 GEMM1 + GEMM2, per layer)",
                      "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": traffic,
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
                      "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
                      "flops_per_launch": flops, "avg_ms": ffn_avg_ms,
-                     "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms,
+                     "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms if ffn_avg_ms else None,
                      "attention_mix_avg_ms": float(np.mean(mix_ms)) if mix_ms else None},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": n_tok * 4 + (B + 1) * 4,
