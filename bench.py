@@ -164,8 +164,7 @@ class ClockSampler:
         self.samples: list[tuple[int, int, int]] = []
         self._stop = threading.Event()
         self._t = None
-
-    def __enter__(self):
+        # NVML init takes tens of ms: do it here, outside the timed region
         try:
             import pynvml
 
@@ -173,10 +172,13 @@ class ClockSampler:
             self._nvml = pynvml
             self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
             self._max = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # no NVML: the line then reports zero samples
+            self._nvml = None
+
+    def __enter__(self):
+        if self._nvml is not None:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
-        except Exception:  # no NVML: the line then reports zero samples
-            self._t = None
         return self
 
     def _run(self):
@@ -326,11 +328,11 @@ def run_ours(args):
     sampler = ClockSampler(local)
     for j in range(n_steps):
         if j == args.warmup:
-            barrier()
             if not ep_mode:
                 engine.ffn_events = []
-            ev_start.record(cs)
             sampler.__enter__()
+            barrier()
+            ev_start.record(cs)
             t_wall0 = time.perf_counter()
         tables[j + 1] = engine.hash_tokens(j + 1, toks[j + 1], lengths)
         out = engine.forward(tables.pop(j), lengths, tokens_dev=toks[j])
