@@ -165,6 +165,19 @@ int sida_unpermute_combine(const uint16_t* y_perm, const int32_t* inv, const flo
 int sida_combine_ranks(const float* y, const float* resid, int n_tokens, int k, int d, float* out,
                        uint16_t* out_bf16, void* stream);
 
+/* Router-mode selection (the teacher path): probs = softmax(x W_r) per
+ * token, ids = the k most probable experts (descending, equal probabilities
+ * to the lower index), alpha = probs at ids (not renormalised). Replaces ref
+ * moe.py:296-301 (router branch of forward_sequence) with numkit.py:28-33,
+ * 87-93; feeds router-mode model_forward (moe.py:408-442), OracleHasher
+ * (predictor.py:413-426) and serve_standard (pipeline.py:370-377).
+ * x float32 (n_tokens, d); w_r float32 (d, num_experts), num_experts <= 256;
+ * probs float32 (n_tokens, num_experts), optional; ids int32 / alpha float64
+ * / alpha_f32 float32 (optional), all (n_tokens, k). */
+int sida_router_topk(const float* x, int n_tokens, int d, const float* w_r, int num_experts,
+                     int k, float* probs, int32_t* ids, double* alpha, float* alpha_f32,
+                     void* stream);
+
 /* ---------------------------------------------------------------------
  * (2) Expert streaming: one pinned-host expert image -> one HBM slot on the
  * copy stream, ordered after wait_event (the slot's last reader) and

@@ -2,8 +2,9 @@
 
 Restates the forward half of ref `pkg/src/sida/moe.py`: parameter init
 (`:158-181`), `embed` (`:206-218`), `attention_mix` (`:220-233`),
-`moe_apply` (`:235-262`), `pool_classify` (`:264-266`) and the external-table
-batch forward `model_forward(mode="external")` (`:408-442`, `:307-318`).
+`moe_apply` (`:235-262`), `pool_classify` (`:264-266`), the external-table
+batch forward `model_forward(mode="external")` (`:408-442`, `:307-318`) and
+the router-mode forward (`:296-306`, `model_forward(mode="router")`).
 All arithmetic is float64, sequences are processed one at a time (B=1),
 exactly like the reference.
 """
@@ -14,7 +15,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .numkit import make_rng, relu, round_bf16, softmax
+from .numkit import make_rng, relu, round_bf16, softmax, topk_rows
 
 
 @dataclass(frozen=True)
@@ -160,3 +161,35 @@ def forward_external(params, shape: MoEShape, sequences, ids: np.ndarray,
         off += t
     out = np.stack(logits)
     return (out, trace) if return_layers else out
+
+
+def router_select(params, layer: int, x: np.ndarray, k: int):
+    """Teacher routing (ref `moe.py:296-301`): probs = softmax(x @ w_r),
+    sel = topk_rows(probs, k), alphas = probs at sel. Returns (sel, alphas, probs)."""
+    probs = softmax(x @ params[f"block{layer}.w_r"])
+    sel = topk_rows(probs, k)
+    return sel, np.take_along_axis(probs, sel, axis=1), probs
+
+
+def forward_router(params, shape: MoEShape, sequences, k: int | None = None):
+    """Router-mode batch forward (ref `moe.py:408-442` with `forward_sequence`
+    `:280-306`): per sequence and layer, attention_mix -> router -> moe_apply.
+    Returns (logits (B, C), selected (L, N, k), alphas (L, N, k), probs (L, N, K))."""
+    k = shape.routing_k if k is None else k
+    logits, sel_rows, al_rows, pr_rows = [], [], [], []
+    for tokens in sequences:
+        x = embed(params, shape, tokens)
+        sels, als, prs = [], [], []
+        for layer in range(shape.num_layers):
+            x = attention_mix(params, shape, layer, x)
+            sel, al, pr = router_select(params, layer, x, k)
+            x = moe_apply(params, layer, x, sel, al)
+            sels.append(sel)
+            als.append(al)
+            prs.append(pr)
+        logits.append(pool_classify(params, x))
+        sel_rows.append(np.stack(sels))
+        al_rows.append(np.stack(als))
+        pr_rows.append(np.stack(prs))
+    return (np.stack(logits), np.concatenate(sel_rows, axis=1),
+            np.concatenate(al_rows, axis=1), np.concatenate(pr_rows, axis=1))

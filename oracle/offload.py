@@ -4,7 +4,8 @@ Restates ref `pkg/src/sida/offload.py`: `plan_placement` (`:118-140`),
 the four victim classes (`_victim_class`, `:143-152`), the per-layer group
 builder (`_plan_groups`, `:155-204`) including the `prefetchable` rule
 (`:179-183`) and the linear transfer-cost model (`:192-195`), and
-`apply_group_inplace` (`:207-222`).
+`apply_group_inplace` (`:207-222`) and the reactive single-layer load of
+standard serving, `ensure_layer_resident` (`:240-278`).
 
 State is (resident: dict[(layer, expert)] -> bytes, fifo: list of keys in
 arrival order, used: int). A plan is a list of groups
@@ -86,3 +87,26 @@ def apply_group(resident: dict, fifo: list, used: int, group, budget_bytes: int,
             fifo.append(key)
             used += expert_bytes
     return used
+
+
+def ensure_layer(resident: dict, fifo: list, used: int, layer: int, expert_ids,
+                 budget_bytes: int, expert_bytes: int):
+    """ref `offload.py:240-278`: evict FIFO among residents the layer does not
+    need (else the FIFO head), then load the missing experts in ascending
+    order. Mutates (resident, fifo); returns (steps, used)."""
+    if expert_bytes > budget_bytes:
+        raise Unservable("expert larger than the budget")
+    req = {int(e) for e in expert_ids}
+    loads = [(layer, e) for e in sorted(req) if (layer, e) not in resident]
+    steps = []
+    for key in loads:
+        while used + expert_bytes > budget_bytes:
+            victim = next((c for c in fifo if not (c[0] == layer and c[1] in req)), fifo[0])
+            used -= resident.pop(victim)
+            fifo.remove(victim)
+            steps.append(("evict", victim))
+        resident[key] = expert_bytes
+        fifo.append(key)
+        used += expert_bytes
+        steps.append(("load", key))
+    return steps, used

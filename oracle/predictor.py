@@ -113,3 +113,22 @@ def top_gap(params, emb: np.ndarray) -> np.ndarray:
     probs = softmax(forward(params, emb))
     srt = np.sort(probs, axis=-1)
     return (srt[..., -1] - srt[..., -2]) / srt[..., -1]
+
+
+def oracle_table(probs: np.ndarray, eval_top_k: int):
+    """`OracleHasher.build_table` (ref `predictor.py:419-426`): top-k of the
+    teacher's router probabilities (L, N, K) -> (ids, alphas) (L, N, k)."""
+    L, N, K = probs.shape
+    sel = topk_rows(probs.reshape(-1, K), eval_top_k).reshape(L, N, eval_top_k)
+    return sel, np.take_along_axis(probs, sel, axis=-1)
+
+
+def hash_hit_rate(pred_ids: list, teacher_sel: list, k: int) -> float:
+    """ref `predictor.py:429-449`: fraction of (layer, token) whose teacher
+    top-1 expert is among the first k predicted ids."""
+    hits = total = 0
+    for ids, sel in zip(pred_ids, teacher_sel):
+        top1 = sel[:, :, 0]
+        hits += int(np.sum(np.any(ids[:, :, :k] == top1[:, :, None], axis=-1)))
+        total += top1.size
+    return hits / total

@@ -13,9 +13,11 @@ from .predictor import (
     DeviceTable,
     ExpertHashTable,
     PredictorConfig,
+    OracleHasher,
     PredictorHasher,
     PredictorNet,
     build_hash_table,
+    hash_hit_rate,
 )
 from .offload import (
     ExpertStore,
@@ -26,9 +28,10 @@ from .offload import (
     apply_group_inplace,
     apply_plan,
     effective_utilization,
+    ensure_layer_resident,
     memory_reduction,
     plan_placement,
 )
-from .pipeline import HashTableQueue, ServingReport, serve_sida
+from .pipeline import HashTableQueue, ServingReport, fidelity, serve_sida, serve_standard
 
 __version__ = "0.1.0"

@@ -21,6 +21,7 @@ bf16, sida_slot_bytes(d, h) bytes) streamed into HBM slots by
 from __future__ import annotations
 
 import math
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -370,6 +371,24 @@ class MoEModel:
             pooled = xp.view(lay.n_seq, lay.max_len, -1).sum(dim=1) / lay.len_t[:, None]
         return pooled @ self.wc
 
+    def route(self, layer: int, x: torch.Tensor, k: int, stream=None, want_probs: bool = True):
+        """Teacher routing on the GPU (ref moe.py:296-301): one fused kernel,
+        probs = softmax(x W_r), the k most probable experts (ties to the lower
+        index) and their probabilities. Returns (ids int32 (1, N, k), alpha
+        float64 (1, N, k), alpha float32 (1, N, k), probs float32 (N, K) or None)."""
+        c = self.config
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        n = x.shape[0]
+        dev = self.device
+        ids = torch.empty((1, n, k), dtype=torch.int32, device=dev)
+        alpha = torch.empty((1, n, k), dtype=torch.float64, device=dev)
+        alpha32 = torch.empty((1, n, k), dtype=torch.float32, device=dev)
+        probs = torch.empty((n, c.num_experts), dtype=torch.float32, device=dev) if want_probs else None
+        _lib.check(_lib.lib().sida_router_topk(
+            x.data_ptr(), n, c.d_model, self.w_r[layer].data_ptr(), c.num_experts, k,
+            _lib.ptr(probs), ids.data_ptr(), alpha.data_ptr(), alpha32.data_ptr(), st.cuda_stream))
+        return ids, alpha, alpha32, probs
+
     def moe_apply_rows(self, layer_tables, x: torch.Tensor, k: int, arena, slot_row: torch.Tensor,
                        expert_list: torch.Tensor | None = None, out: torch.Tensor | None = None,
                        y: torch.Tensor | None = None, stream=None,
@@ -425,22 +444,72 @@ class MoEModel:
         return out
 
 
-def model_forward(model: MoEModel, batch: SequenceBatch, mode: str = "external", table=None,
-                  timings: dict | None = None, store=None):
-    """Forward a whole batch in external (hash-table) mode (ref moe.py:408-442).
+def router_forward(model: MoEModel, lay: BatchLayout, ktop: int, store=None, stream=None):
+    """Router-mode forward of a whole batch on the device (ref moe.py:280-306
+    router branch, per layer: attention_mix -> softmax(x W_r) -> top-k ->
+    moe_apply). ``ktop`` >= routing_k experts are selected per token; the
+    first routing_k route the token (top-k orders are prefixes of each
+    other). Returns device tensors (logits (B, C), ids int32 (L, N, ktop),
+    alpha float64 (L, N, ktop), probs float32 (L, N, K))."""
+    from .offload import ExpertStore  # local import: offload depends on moe
+    from .predictor import DeviceTable
 
-    Returns (logits numpy (B, C), ActivationTrace). Every expert the table
-    names is made resident in ``store`` (default: a store holding all
-    experts) before its layer runs. Router mode is SURVEY §8(f) "next".
+    c = model.config
+    st = stream or torch.cuda.current_stream(model.device)
+    store = store or ExpertStore.full(model)
+    rk = c.routing_k
+    n = lay.n_tokens
+    ids_all = torch.empty((c.num_layers, n, ktop), dtype=torch.int32, device=model.device)
+    al_all = torch.empty((c.num_layers, n, ktop), dtype=torch.float64, device=model.device)
+    pr_all = torch.empty((c.num_layers, n, c.num_experts), dtype=torch.float32,
+                         device=model.device)
+    with torch.cuda.stream(st):
+        x = model.embed_layout(lay)
+        for layer in range(c.num_layers):
+            x = model.attention_mix(layer, x, lay)
+            ids, al, al32, pr = model.route(layer, x, ktop, stream=st)
+            ids_all[layer].copy_(ids[0])
+            al_all[layer].copy_(al[0])
+            pr_all[layer].copy_(pr)
+            if ktop != rk:
+                ids, al, al32 = (t[:, :, :rk].contiguous() for t in (ids, al, al32))
+            dt = DeviceTable(ids, al, al32, n, rk)
+            dt.permute(c.num_experts, st)
+            x = store.run_layer(model, layer, x, dt, stream=st, table_layer=0)
+        logits = model.pool_classify(x, lay)
+    return logits, ids_all, al_all, pr_all
+
+
+def model_forward(model: MoEModel, batch: SequenceBatch, mode: str = "router", table=None,
+                  timings: dict | None = None, store=None):
+    """Forward a whole batch (ref moe.py:408-442); returns (logits numpy
+    (B, C), ActivationTrace).
+
+    ``mode="router"``: the teacher routers select the experts on the GPU
+    (`sida_router_topk` per layer); the trace holds the selections, their
+    probabilities and the full router distributions. ``mode="external"``:
+    the hash table's (ids, alphas) replace the routers. Every expert a layer
+    needs is made resident in ``store`` (default: a store holding all
+    experts) before its layer runs.
     """
     from .offload import ExpertStore  # local import: offload depends on moe
 
-    if mode != "external":
-        raise ContractError(f"mode {mode!r} is not on the SiDA hot path (external only)")
-    if table is None:
-        raise ContractError("external mode requires a hash table")
+    if mode not in ("router", "external"):
+        raise ContractError(f"unknown forward mode {mode!r}")
     if store is None:
         store = ExpertStore.full(model)
+    if mode == "router":
+        lay = BatchLayout.from_batch(model, batch)
+        t0 = time.perf_counter()
+        logits, ids, al, pr = router_forward(model, lay, model.config.routing_k, store)
+        out = logits.cpu().numpy().astype(np.float64)
+        if timings is not None:
+            timings["forward"] = timings.get("forward", 0.0) + time.perf_counter() - t0
+        trace = ActivationTrace(lengths=batch.lengths, selected=ids.cpu().numpy().astype(np.int64),
+                                alphas=al.cpu().numpy(), probs=pr.cpu().numpy().astype(np.float64))
+        return out, trace
+    if table is None:
+        raise ContractError("external mode requires a hash table")
     dev_table = table.on_device(model)
     if dev_table.n_tokens != batch.num_tokens or table.lengths != batch.lengths:
         raise ContractError("hash table does not cover the requested tokens")

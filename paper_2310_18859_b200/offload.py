@@ -2,7 +2,8 @@
 
 Mirrors ref pkg/src/sida/offload.py (`MemoryBudget`, `ResidencyState`,
 `PlanGroup`, `PlacementPlan`, `plan_placement`, `apply_group_inplace`,
-`apply_plan`, `effective_utilization`, `memory_reduction`). Decisions come
+`apply_plan`, `ensure_layer_resident`, `effective_utilization`,
+`memory_reduction`). Decisions come
 from the native planner (`sida_plan_placement`, csrc/planner.cpp) and are
 identical to the reference's FIFO victim classes; `ExpertStore` executes them
 for real: one HBM arena of ``n_slots`` expert slots, pinned host expert
@@ -174,6 +175,35 @@ def apply_plan(state: ResidencyState, plan: PlacementPlan) -> tuple[ResidencySta
     return new, plan.estimated_transfer_s
 
 
+def ensure_layer_resident(state: ResidencyState, layer: int, expert_ids, budget: MemoryBudget,
+                          expert_bytes: int) -> PlanGroup:
+    """Reactive single-layer load of standard serving (ref offload.py:240-278):
+    evict FIFO among residents this layer does not need (the FIFO head when
+    the layer's working set exceeds the budget), then load the missing
+    experts in ascending order. Mutates ``state``; returns the executed group
+    (bookkeeping only -- `ExpertStore` performs the copies)."""
+    if expert_bytes > budget.fast_tier_bytes:
+        raise UnservableError(
+            f"expert of {expert_bytes} bytes exceeds budget {budget.fast_tier_bytes}")
+    req = {int(e) for e in expert_ids}
+    loads = [(layer, e) for e in sorted(req) if (layer, e) not in state.resident]
+    steps = []
+    for key in loads:
+        while state.used_bytes + expert_bytes > budget.fast_tier_bytes:
+            victim = next((c for c in state.fifo_order if not (c[0] == layer and c[1] in req)),
+                          state.fifo_order[0])
+            state.used_bytes -= state.resident.pop(victim)
+            state.fifo_order.remove(victim)
+            steps.append(("evict", victim))
+        state.resident[key] = expert_bytes
+        state.fifo_order.append(key)
+        state.used_bytes += expert_bytes
+        steps.append(("load", key))
+    transfer_s = (len(loads) * expert_bytes / budget.bandwidth_bytes_per_s
+                  + budget.per_transfer_latency_s * len(loads))
+    return PlanGroup(layer=layer, steps=steps, prefetchable=False, transfer_s=transfer_s)
+
+
 def effective_utilization(state: ResidencyState, activated: set) -> float:
     """ref offload.py:281-289."""
     missing = [k for k in activated if k not in state.resident]
@@ -293,22 +323,25 @@ class ExpertStore:
 
     # -- one layer, every required expert resident (model_forward path) ---------------
     def run_layer(self, model, layer: int, x: torch.Tensor, dev_table, stream=None,
-                  out_bf16=None):
+                  out_bf16=None, table_layer: int | None = None):
+        """``table_layer``: the row of ``dev_table`` holding this layer's routing
+        (default ``layer``; 0 for the single-layer tables of router mode)."""
         st = stream or torch.cuda.current_stream(model.device)
+        tl = layer if table_layer is None else table_layer
         table_hist = dev_table.hist
         dev_table.ready.synchronize()
         st.wait_event(dev_table.ready)
-        need = [int(e) for e in np.nonzero(table_hist[layer].cpu().numpy())[0]]
+        need = [int(e) for e in np.nonzero(table_hist[tl].cpu().numpy())[0]]
         loads = [((layer, e), self.take_slot((layer, e))) for e in need
                  if (layer, e) not in self.slot_of]
         done = self.enqueue_loads(loads)
         wave = Wave(layer, loads, need, self.slot_row(layer, need))
         return run_waves(model, [wave], x, dev_table, self, st, pre_done=[done],
-                         out_bf16=out_bf16)
+                         out_bf16=out_bf16, table_layer=tl)
 
 
 def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=None,
-              issue=None, out_bf16=None):
+              issue=None, out_bf16=None, table_layer: int | None = None):
     """Execute one layer as a sequence of waves on ``stream``: wait for each
     wave's copies, run the grouped FFN over its experts, record the reader
     event. ``issue(wave)`` (optional) enqueues a wave's copies just in time and
@@ -317,7 +350,7 @@ def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=N
     c = model.config
     k = dev_table.k
     layer = waves[0].layer
-    tables = dev_table.layer(layer)
+    tables = dev_table.layer(layer if table_layer is None else table_layer)
     out = torch.empty_like(x)
     y = None
     if k > 1:

@@ -18,8 +18,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ContractError
-from .moe import MoEModel, Rng, SequenceBatch
+from .errors import ContractError, CoverageError
+from .moe import BatchLayout, MoEModel, Rng, SequenceBatch, router_forward
 
 
 @dataclass
@@ -377,3 +377,53 @@ class PredictorHasher:
 
     def build_table(self, batch: SequenceBatch, eval_top_k: int) -> ExpertHashTable:
         return build_hash_table(self.predictor, batch, eval_top_k, self.embed_fn, self.stream)
+
+
+class OracleHasher:
+    """The teacher routers as the hash function (ref predictor.py:413-426):
+    a router-mode forward on the GPU whose per-layer top-``eval_top_k``
+    selections (descending probability, ties to the lower index) and
+    probabilities become the table. Upper-bounds hit rate and fidelity."""
+
+    def __init__(self, model: MoEModel, stream=None, store=None):
+        self.model = model
+        self.stream = stream
+        self.store = store
+
+    def build_table(self, batch: SequenceBatch, eval_top_k: int) -> ExpertHashTable:
+        c = self.model.config
+        if not 1 <= eval_top_k <= c.num_experts:
+            raise ContractError(f"k={eval_top_k} out of range for width-{c.num_experts} rows")
+        st = self.stream or torch.cuda.current_stream(self.model.device)
+        with torch.cuda.stream(st):
+            lay = BatchLayout.from_batch(self.model, batch)
+            ktop = max(eval_top_k, c.routing_k)
+            _, ids, al, _ = router_forward(self.model, lay, ktop, store=self.store, stream=st)
+            ids = ids[:, :, :eval_top_k].contiguous()
+            al = al[:, :, :eval_top_k].contiguous()
+            dt = DeviceTable(ids, al, al.float(), lay.n_tokens, eval_top_k, tokens=lay.tokens)
+            dt.permute(c.num_experts, st)
+        return ExpertHashTable(batch.batch_id, batch.lengths, device_table=dt)
+
+
+def hash_hit_rate(tables: list, traces: list, k: int) -> float:
+    """Fraction of (layer, token) whose teacher top-1 expert is among the
+    first k predicted ids (ref predictor.py:429-449)."""
+    if len(tables) != len(traces):
+        raise CoverageError("table/trace counts differ")
+    if k < 1:
+        raise ContractError("k must be >= 1")
+    hits = total = 0
+    for table, trace in zip(tables, traces):
+        if table.lengths != list(trace.lengths):
+            raise CoverageError("table and trace cover different sequences")
+        if table.num_layers != trace.num_layers:
+            raise CoverageError("table and trace cover different layer counts")
+        if k > table.eval_top_k:
+            raise CoverageError(f"k={k} exceeds table width {table.eval_top_k}")
+        top1 = trace.selected[:, :, 0]
+        hits += int(np.sum(np.any(table.ids[:, :, :k] == top1[:, :, None], axis=-1)))
+        total += top1.size
+    if total == 0:
+        raise CoverageError("empty coverage")
+    return hits / total

@@ -34,8 +34,21 @@ sys.path.insert(0, REPO)
 from sida import numkit as ref_numkit  # noqa: E402
 from sida.moe import MoEConfig, MoEModel, SequenceBatch, model_forward  # noqa: E402
 from sida.numkit import Rng  # noqa: E402
-from sida.offload import MemoryBudget, ResidencyState, apply_plan, plan_placement  # noqa: E402
-from sida.predictor import PredictorConfig, PredictorNet, build_hash_table  # noqa: E402
+from sida.offload import (  # noqa: E402
+    MemoryBudget,
+    ResidencyState,
+    apply_plan,
+    ensure_layer_resident,
+    plan_placement,
+)
+from sida.pipeline import serve_sida, serve_standard  # noqa: E402
+from sida.predictor import (  # noqa: E402
+    OracleHasher,
+    PredictorConfig,
+    PredictorNet,
+    build_hash_table,
+    hash_hit_rate,
+)
 
 from oracle.numkit import round_bf16  # noqa: E402
 
@@ -148,7 +161,75 @@ def planner_case():
         json.dump(cases, fh)
 
 
+def router_case(name, cfg, lengths, eval_ks, seq_seed=2):
+    """Router mode (the teacher path): model_forward(mode="router"), the
+    OracleHasher table, hash_hit_rate of the predictor's tables against the
+    teacher traces, serve_standard with a tight budget and serve_sida with
+    the oracle hasher (predictor=None)."""
+    model = MoEModel(cfg, Rng(0))
+    for k in model.params:
+        model.params[k] = round_bf16(model.params[k])
+    net = PredictorNet(PredictorConfig(), cfg.d_model, cfg.num_layers, cfg.num_experts, Rng(1))
+    rng = Rng(seq_seed)
+    seqs = [rng.integers(0, cfg.vocab_size, size=n) for n in lengths]
+    batch = SequenceBatch(0, seqs)
+    out = {"lengths": np.array(lengths), "tokens": np.concatenate(seqs)}
+    logits, trace = model_forward(model, batch, mode="router")
+    out["logits"] = logits
+    out["selected"] = trace.selected
+    out["alphas"] = trace.alphas
+    out["probs"] = trace.probs
+    # layer-0 router input (attention output of every sequence) for the kernel check
+    out["router_in_l0"] = np.concatenate(
+        [model.attention_mix(0, model.embed(s)) for s in seqs])
+    for k in eval_ks:
+        t = OracleHasher(model).build_table(batch, k)
+        out[f"oracle_ids_k{k}"] = t.ids
+        out[f"oracle_alphas_k{k}"] = t.alphas
+        pt = build_hash_table(net, batch, k, model.embed)
+        out[f"pred_ids_k{k}"] = pt.ids
+        out[f"hit_rate_k{k}"] = np.array(hash_hit_rate([pt], [trace], k))
+    eb = model.expert_bytes_each()
+    budget = MemoryBudget(max(1, cfg.num_experts // 2) * eb)
+    rep = serve_standard(model, [batch, SequenceBatch(1, seqs[::-1])], budget)
+    out["standard_logits_b0"] = rep.logits[0]
+    out["standard_logits_b1"] = rep.logits[1]
+    out["standard_peak"] = np.array(rep.peak_fast_tier_bytes // eb)
+    rep = serve_sida(model, None, [batch], MemoryBudget(cfg.num_layers * cfg.num_experts * eb),
+                     eval_top_k=1)
+    out["oracle_serve_hit_rate"] = np.array(rep.hit_rate)
+    out["oracle_serve_logits"] = rep.logits[0]
+    np.savez_compressed(os.path.join(HERE, f"router_{name}.npz"), **out)
+
+
+def ensure_case():
+    """ensure_layer_resident (ref offload.py:240-278) on random request streams."""
+    g = np.random.default_rng(11)
+    cases = []
+    eb = 1000
+    for _ in range(40):
+        n_layers, n_exp = int(g.integers(1, 5)), int(g.integers(2, 9))
+        slots = int(g.integers(1, n_layers * n_exp + 2))
+        budget = MemoryBudget(slots * eb)
+        state = ResidencyState()
+        calls = []
+        for _ in range(int(g.integers(1, 12))):
+            layer = int(g.integers(0, n_layers))
+            req = sorted(set(g.integers(0, n_exp, size=int(g.integers(1, n_exp + 1))).tolist()))
+            grp = ensure_layer_resident(state, layer, req, budget, eb)
+            calls.append({"layer": layer, "required": req,
+                          "steps": [[op, list(k)] for op, k in grp.steps],
+                          "transfer_s": grp.transfer_s,
+                          "fifo_after": [list(k) for k in state.fifo_order]})
+        cases.append({"slots": slots, "expert_bytes": eb, "calls": calls})
+    with open(os.path.join(HERE, "ensure.json"), "w") as fh:
+        json.dump(cases, fh)
+
+
 def main():
+    if "--router" in sys.argv:  # router-mode fixtures only (added after the first set)
+        router_main()
+        return
     numkit_case()
     model_case("tiny", MoEConfig(vocab_size=64, d_model=32, num_layers=2, num_experts=8,
                                  expert_hidden=64, max_seq_len=16, routing_k=1, num_classes=3),
@@ -158,6 +239,21 @@ def main():
                                expert_hidden=1024, max_seq_len=128, routing_k=1, num_classes=4),
                lengths=[128] * 8, ks=(1,))
     planner_case()
+    router_main()
+
+
+def router_main():
+    router_case("tiny", MoEConfig(vocab_size=64, d_model=32, num_layers=2, num_experts=8,
+                                  expert_hidden=64, max_seq_len=16, routing_k=1, num_classes=3),
+                lengths=[5, 16, 9, 1, 12], eval_ks=(1, 2))
+    router_case("tiny_r2", MoEConfig(vocab_size=64, d_model=32, num_layers=3, num_experts=6,
+                                     expert_hidden=64, max_seq_len=16, routing_k=2,
+                                     num_classes=3),
+                lengths=[7, 16, 3], eval_ks=(1, 3))
+    router_case("c0", MoEConfig(vocab_size=512, d_model=256, num_layers=2, num_experts=8,
+                                expert_hidden=1024, max_seq_len=128, routing_k=1, num_classes=4),
+                lengths=[128] * 8, eval_ks=(1,))
+    ensure_case()
 
 
 if __name__ == "__main__":

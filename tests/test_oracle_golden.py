@@ -131,3 +131,54 @@ def test_planner_replays_reference_plans():
             for gr in groups:
                 used = ooff.apply_group(resident, fifo, used, gr, budget, eb)
             assert [list(k) for k in fifo] == b["fifo_after"]
+
+
+ROUTER_CFGS = {
+    "tiny": dict(vocab_size=64, d_model=32, num_layers=2, num_experts=8, expert_hidden=64,
+                 max_seq_len=16, routing_k=1, num_classes=3),
+    "tiny_r2": dict(vocab_size=64, d_model=32, num_layers=3, num_experts=6, expert_hidden=64,
+                    max_seq_len=16, routing_k=2, num_classes=3),
+    "c0": dict(vocab_size=512, d_model=256, num_layers=2, num_experts=8, expert_hidden=1024,
+               max_seq_len=128, routing_k=1, num_classes=4),
+}
+
+
+@pytest.mark.parametrize("name", sorted(ROUTER_CFGS))
+def test_router_mode_matches_reference(name):
+    """Router-mode forward, OracleHasher table and hash_hit_rate
+    (ref moe.py:296-306, predictor.py:413-449) against the reference's outputs."""
+    shape = omoe.MoEShape(**ROUTER_CFGS[name])
+    g = load_golden("router_" + name)
+    params = omoe.bf16_params(omoe.init_params(shape, 0))
+    pparams = opred.init_params(opred.PredictorShape(shape.d_model, shape.num_layers,
+                                                     shape.num_experts), 1)
+    seqs = np.split(g["tokens"], np.cumsum(g["lengths"])[:-1])
+    logits, sel, al, probs = omoe.forward_router(params, shape, seqs)
+    np.testing.assert_array_equal(sel, g["selected"])
+    np.testing.assert_allclose(al, g["alphas"], rtol=1e-12)
+    np.testing.assert_allclose(probs, g["probs"], rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(logits, g["logits"], rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(logits, g["standard_logits_b0"], rtol=1e-10, atol=1e-12)
+    emb = lambda t: omoe.embed(params, shape, t)  # noqa: E731
+    for key in g.files:
+        if key.startswith("oracle_ids_k"):
+            k = int(key[len("oracle_ids_k"):])
+            ids, alphas = opred.oracle_table(probs, k)
+            np.testing.assert_array_equal(ids, g[key])
+            np.testing.assert_allclose(alphas, g[f"oracle_alphas_k{k}"], rtol=1e-12)
+            pids, _ = opred.build_hash_table(pparams, seqs, k, emb)
+            np.testing.assert_array_equal(pids, g[f"pred_ids_k{k}"])
+            assert opred.hash_hit_rate([pids], [sel], k) == float(g[f"hit_rate_k{k}"])
+    assert float(g["oracle_serve_hit_rate"]) == 1.0
+
+
+def test_ensure_layer_resident_replays_reference():
+    cases = json.load(open(os.path.join(GOLDEN, "ensure.json")))
+    for case in cases:
+        eb = case["expert_bytes"]
+        resident, fifo, used = {}, [], 0
+        for call in case["calls"]:
+            steps, used = ooff.ensure_layer(resident, fifo, used, call["layer"], call["required"],
+                                            case["slots"] * eb, eb)
+            assert [[op, list(k)] for op, k in steps] == call["steps"]
+            assert [list(k) for k in fifo] == call["fifo_after"]
