@@ -268,6 +268,23 @@ __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// explicit shared-space 128-bit accesses: the staging tile's address comes
+// from an aligned integer, so generic pointers would compile to LD.E/ST.E
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
 __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);  // one cvt.rn.bf16x2.f32
   return *reinterpret_cast<uint32_t*>(&v);
@@ -311,8 +328,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   constexpr int kTile = stage_tile_bytes<STAGE>();
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-B alignment for SWIZZLE_128B, as an offset from the shared array so
+  // every derived pointer keeps the shared address space (LDS/STS, not LD.E/ST.E)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + kStages * kABytes;
   uint8_t* sOut = sB + kStages * kBBytes;  // kEpiWarps staging tiles
@@ -459,7 +477,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     const int half = (warp - 2) >> 2;
     constexpr int kHalfCols = BN / 2;
     constexpr int kChunks = kHalfCols / 32;
-    uint8_t* stile = sOut + (warp - 2) * kTile;
+    const uint32_t stile = smem_u32(sOut + (warp - 2) * kTile);
     int acc = 0;
     uint32_t acc_phase = 0;
     unsigned long long w_full = 0;
@@ -510,7 +528,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         }
         if (STAGE == 1) {
           // row-per-lane write: row r = lane, 4 x 16 B chunks, chunk' = q ^ ((r>>1)&3)
-          uint4* srow = reinterpret_cast<uint4*>(stile + lane * 64);
+          const uint32_t srow = stile + lane * 64;
           const int sw = (lane >> 1) & 3;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -519,14 +537,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             o.y = bf16x2_rn(fmaxf(f[q * 8 + 2], 0.f), fmaxf(f[q * 8 + 3], 0.f));
             o.z = bf16x2_rn(fmaxf(f[q * 8 + 4], 0.f), fmaxf(f[q * 8 + 5], 0.f));
             o.w = bf16x2_rn(fmaxf(f[q * 8 + 6], 0.f), fmaxf(f[q * 8 + 7], 0.f));
-            srow[q ^ sw] = o;
+            sts128(srow + ((q ^ sw) << 4), o);
           }
           __syncwarp();
           // read back: lane -> (row = i*8 + lane/4, chunk = lane%4)
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int r = i * 8 + (lane >> 2), q = lane & 3;
-            const uint4 val = reinterpret_cast<const uint4*>(stile + r * 64)[q ^ ((r >> 1) & 3)];
+            const uint4 val = lds128(stile + r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
             if (qrow0 + r < ti.row_end)
               *reinterpret_cast<uint4*>(p.hidden + static_cast<size_t>(qrow0 + r) * p.ndim +
                                         col0 + q * 8) = val;
@@ -534,12 +552,12 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           __syncwarp();
         } else {
           // row-per-lane write of alpha*(acc+b2): 8 x 16 B chunks, chunk' = q ^ (r & 7)
-          uint4* srow = reinterpret_cast<uint4*>(stile + lane * 128);
+          const uint32_t srow = stile + lane * 128;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             float4 o = make_float4(f[q * 4 + 0] * a_scale, f[q * 4 + 1] * a_scale,
                                    f[q * 4 + 2] * a_scale, f[q * 4 + 3] * a_scale);
-            srow[q ^ (lane & 7)] = *reinterpret_cast<uint4*>(&o);
+            sts128(srow + ((q ^ (lane & 7)) << 4), *reinterpret_cast<uint4*>(&o));
           }
           __syncwarp();
           // read back: lane -> (row = i*4 + lane/8, chunk = lane%8); residual
@@ -559,7 +577,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), q = lane & 7;
-            const uint4 raw = reinterpret_cast<const uint4*>(stile + r * 128)[q ^ (r & 7)];
+            const uint4 raw = lds128(stile + r * 128 + ((q ^ (r & 7)) << 4));
             if (qrow0 + r < ti.row_end) {
               float4 o = *reinterpret_cast<const float4*>(&raw);
               const size_t at = at8[i];

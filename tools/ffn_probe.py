@@ -20,6 +20,7 @@ p.add_argument("--experts", type=int, default=8)
 p.add_argument("--d", type=int, default=768)
 p.add_argument("--h", type=int, default=3072)
 p.add_argument("--iters", type=int, default=20)
+p.add_argument("--no-cublas", action="store_true")
 a = p.parse_args()
 cfg = MoEConfig(vocab_size=64, d_model=a.d, num_layers=1, num_experts=a.experts,
                 expert_hidden=a.h, max_seq_len=16)
@@ -62,6 +63,8 @@ if os.environ.get("SIDA_GEMM_PROF"):
         tot = b[:, 3].mean()
         print(f"GEMM{gi + 1}: " + ", ".join(f"{n}={b[:, i].mean():.0f}" for i, n in enumerate(names))
               + f"  | mma waits epi {b[:, 1].mean() / tot:.1%} tma {b[:, 2].mean() / tot:.1%}")
+if a.no_cublas:
+    sys.exit(0)
 # cuBLAS reference on the same shapes (dense bmm, no gather/epilogue fusion)
 E = K
 xs = torch.randn(E, N // E, a.d, device="cuda", dtype=torch.bfloat16)
