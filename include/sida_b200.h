@@ -142,6 +142,17 @@ int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h, cons
  * out: uint64 [2 GEMMs][148 CTAs][8]. Synchronises the device. */
 int sida_debug_gemm_prof(unsigned long long* out);
 
+/* Mixing-attention output projection (ref moe.py:232-233) on the same
+ * tcgen05 GEMM, residual fused: out[t] = resid[t] + ctx[t] W_o (fp32), and,
+ * for k >= 1, the next FFN's expert-sorted input x_perm[inv[t*k + r]] =
+ * bf16(out[t]) for r < k (k <= 4), i.e. the row gather of sida_gather_rows_bf16
+ * folded into the epilogue. ctx bf16 (n_rows, d); wo_t = W_o^T (d, d) bf16
+ * K-major followed by d zero bf16, sida_out_proj_bytes(d) bytes; d % 64 == 0. */
+size_t sida_out_proj_bytes(int d);
+int sida_out_proj_scatter(const uint16_t* ctx, int n_rows, int d, const void* wo_t,
+                          const float* resid, float* out, const int32_t* inv, int k,
+                          uint16_t* x_perm, int32_t* err_flag, void* stream);
+
 /* fp32 FMA check path: same contraction with float32 weights in the
  * reference layout w1 (K,d,h), b1 (K,h), w2 (K,h,d), b2 (K,d); x_perm
  * float32; hidden float32 workspace (n_rows, h). */

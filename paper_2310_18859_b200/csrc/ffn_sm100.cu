@@ -44,6 +44,7 @@ constexpr int UMMA_K = 16;    // K per tcgen05.mma for kind::f16
 constexpr int kEpiWarps = 8;  // two warps per TMEM lane quarter
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kMaxListed = 512;
+constexpr int kMaxBf16K = 4;
 constexpr int kSmemBudget = 222 * 1024;
 
 // Per-warp epilogue staging tile: 32 rows x 32 columns of the output type.
@@ -79,6 +80,8 @@ struct GemmParams {
   const float* resid;
   float* out;
   uint16_t* out_bf16;          // GEMM2: optional bf16 copy of out (next layer's GEMM input)
+  const int32_t* bf16_map;     // optional: out_bf16 row of (out row t, rank r) = map[t*k + r]
+  int bf16_k;                  // ranks per out row in bf16_map (1..kMaxBf16K)
   int32_t* err_flag;
   unsigned long long* prof;    // optional per-CTA cycle counters (sida_debug_gemm_prof)
 };
@@ -295,6 +298,11 @@ struct TileInfo {
   int expert, row0, row_end, ncol0, slot;
 };
 
+// First row of expert e (off == nullptr: one dense "expert" over all rows).
+__device__ __forceinline__ int expert_row(const GemmParams& p, int e) {
+  return p.off ? p.off[e] : (e == 0 ? 0 : p.n_rows);
+}
+
 // Tile t -> (expert, first row of the TM-row tile, column tile).
 __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int32_t* s_prefix,
                                                 const int32_t* s_expert, int n_list,
@@ -307,11 +315,11 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int32
   }
   TileInfo ti;
   ti.expert = s_expert[lo];
-  const int seg0 = p.off[ti.expert];
+  const int seg0 = expert_row(p, ti.expert);
   ti.row0 = seg0 + (mt - s_prefix[lo]) * TM;
-  ti.row_end = p.off[ti.expert + 1];
+  ti.row_end = expert_row(p, ti.expert + 1);
   ti.ncol0 = nt * BN;
-  ti.slot = p.expert_slot[ti.expert];
+  ti.slot = p.expert_slot ? p.expert_slot[ti.expert] : 0;
   return ti;
 }
 
@@ -355,7 +363,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const int e = p.expert_list ? p.expert_list[i] : i;
       s_expert[i] = e;
       s_prefix[i] = acc;
-      acc += ceil_div(p.off[e + 1] - p.off[e], TM);
+      acc += ceil_div(expert_row(p, e + 1) - expert_row(p, e), TM);
     }
     s_prefix[n_list] = acc;
     for (int i = 0; i < kStages; ++i) {
@@ -492,9 +500,15 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           p.arena + static_cast<size_t>(ti.slot) * p.slot_stride + p.bias_off);
       float a_scale = 1.f;
       int orow = my_row;
+      int brow[kMaxBf16K] = {};
       if (STAGE == 2 && valid) {
         if (p.alpha) a_scale = p.alpha[my_row];
         if (p.row_map) orow = p.row_map[my_row];
+        if (p.bf16_map) {
+#pragma unroll
+          for (int r = 0; r < kMaxBf16K; ++r)
+            if (r < p.bf16_k) brow[r] = p.bf16_map[static_cast<size_t>(orow) * p.bf16_k + r];
+        }
       }
       const int cbase = ti.ncol0 + half * kHalfCols;
       const unsigned long long c2 = p.prof ? clk() : 0;
@@ -565,10 +579,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           // all eight residual loads in flight before any store (MLP 8)
           size_t at8[8];
           float4 x8[8];
+          int brow8[8][kMaxBf16K];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), q = lane & 7;
             const int orow_r = __shfl_sync(0xffffffffu, orow, r);
+            if (p.bf16_map) {
+#pragma unroll
+              for (int j = 0; j < kMaxBf16K; ++j)
+                brow8[i][j] = __shfl_sync(0xffffffffu, brow[j], r);
+            }
             at8[i] = static_cast<size_t>(orow_r) * p.ndim + col0 + q * 4;
             x8[i] = (p.resid && qrow0 + r < ti.row_end)
                         ? __ldg(reinterpret_cast<const float4*>(p.resid + at8[i]))
@@ -590,7 +610,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 uint2 ob;
                 ob.x = bf16x2_rn(o.x, o.y);
                 ob.y = bf16x2_rn(o.z, o.w);
-                *reinterpret_cast<uint2*>(p.out_bf16 + at) = ob;
+                if (!p.bf16_map) {
+                  *reinterpret_cast<uint2*>(p.out_bf16 + at) = ob;
+                } else {  // expert-sorted copies: one per rank of this token
+                  const size_t col = col0 + (lane & 7) * 4;
+#pragma unroll
+                  for (int j = 0; j < kMaxBf16K; ++j)
+                    if (j < p.bf16_k)
+                      *reinterpret_cast<uint2*>(
+                          p.out_bf16 + static_cast<size_t>(brow8[i][j]) * p.ndim + col) = ob;
+                }
               }
             }
           }
@@ -712,12 +741,23 @@ static int launch_gemm(const void* a_base, const void* b_base, int n_slots, cons
 template <int STAGE, int CG>
 static int dispatch_bn(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
                        int n_listed, cudaStream_t s) {
-  // N tile: 256 for wide outputs; 192 when it splits N into more tiles with no
-  // remainder (d = 768 -> 4 tiles: better wave quantisation on 148 SMs)
-  if (p.ndim % 256 == 0 && p.ndim >= 2048)
+  // N tile: 256 whenever it divides N. The GEMMs are fed at close to the
+  // L2->SM limit (~10 TB/s measured), so the widest tile (fewest A re-reads
+  // per FLOP) wins even where a narrower one quantises better: d = 768 at
+  // BN=256 reads the hidden rows 3x instead of 4x (0.312 -> 0.296 ms/layer).
+  // SIDA_FFN_BN2=192|128 forces the GEMM2 tile for measurements.
+  static int forced_bn = -1;
+  if (forced_bn < 0) {
+    const char* e = getenv("SIDA_FFN_BN2");
+    forced_bn = e ? atoi(e) : 0;
+  }
+  if (STAGE == 2 && forced_bn == 192 && p.ndim % 192 == 0)
+    return launch_gemm<192, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
+  if (STAGE == 2 && forced_bn == 128 && p.ndim % 128 == 0)
+    return launch_gemm<128, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
+  if (p.ndim % 256 == 0)
     return launch_gemm<256, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
   if (p.ndim % 192 == 0) return launch_gemm<192, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
-  if (p.ndim % 256 == 0) return launch_gemm<256, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
   if (p.ndim % 128 == 0) return launch_gemm<128, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
   return launch_gemm<64, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
 }
@@ -811,4 +851,37 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   p2.out_bf16 = out_bf16;
   p2.prof = prof_buffer(1);
   return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, listed, cg, s);
+}
+
+// Mixing-attention output projection with the residual and the next FFN's
+// expert-sorted input fused into the epilogue (ref moe.py:232-233, then the
+// row gather implicit in moe.py:253-256): out[t] = resid[t] + ctx[t] Wo and
+// x_perm[inv[t*k + r]] = bf16(out[t]) for every rank r < k (k = 0: no copy).
+// wo_t: Wo^T (d_out x d_in, bf16, K-major) followed by d_out zero bf16 (the
+// bias slot of the grouped-GEMM epilogue), sida_out_proj_bytes(d) bytes.
+extern "C" size_t sida_out_proj_bytes(int d) {
+  return align_up(static_cast<size_t>(d) * d * 2 + static_cast<size_t>(d) * 2, 16);
+}
+
+extern "C" int sida_out_proj_scatter(const uint16_t* ctx, int n_rows, int d, const void* wo_t,
+                                     const float* resid, float* out, const int32_t* inv, int k,
+                                     uint16_t* x_perm, int32_t* err_flag, void* stream) {
+  SIDA_REQUIRE(d % 64 == 0, SIDA_ERR_UNSUPPORTED, "out projection needs d multiple of 64 (d=%d)",
+               d);
+  SIDA_REQUIRE(n_rows >= 0 && k >= 0 && k <= sm100::kMaxBf16K, SIDA_ERR_CONTRACT,
+               "bad out-projection dims rows=%d k=%d", n_rows, k);
+  SIDA_REQUIRE(ctx && wo_t && resid && out && err_flag && (k == 0 || (inv && x_perm)),
+               SIDA_ERR_CONTRACT, "null pointer passed to sida_out_proj_scatter");
+  if (n_rows == 0) return SIDA_OK;
+  sm100::GemmParams p{};
+  p.n_rows = n_rows; p.kdim = d; p.ndim = d;
+  p.off = nullptr; p.num_experts = 1; p.expert_slot = nullptr;
+  p.arena = static_cast<const uint8_t*>(wo_t);
+  p.slot_stride = sida_out_proj_bytes(d);
+  p.bias_off = static_cast<size_t>(d) * d * 2;
+  p.resid = resid; p.out = out;
+  p.out_bf16 = k ? x_perm : nullptr; p.bf16_map = k ? inv : nullptr; p.bf16_k = k;
+  p.err_flag = err_flag;
+  const int cg = n_rows >= 1024 ? 2 : 1;
+  return sm100::dispatch_gemm<2>(ctx, wo_t, 1, p, 1, cg, as_stream(stream));
 }

@@ -147,7 +147,13 @@ class SidaEngine:
                 if self.ffn_events is not None:
                     e_m = torch.cuda.Event(enable_timing=True)
                     e_m.record(cs)
-                x = model.attention_mix(layer, x, lay, xb=xb)
+                scatter = None
+                if model.wo_t is not None and dt.k <= 4:
+                    x_perm = torch.empty((lay.n_tokens * dt.k, model.config.d_model),
+                                         dtype=torch.bfloat16, device=x.device)
+                    scatter = (dt.inv[layer], dt.k, x_perm)
+                x = model.attention_mix(layer, x, lay, xb=xb, scatter=scatter)
+                xp = scatter[2] if scatter is not None else None
                 if self.ffn_events is not None:
                     e_a = torch.cuda.Event(enable_timing=True)
                     e_a.record(cs)
@@ -155,10 +161,11 @@ class SidaEngine:
                 xb = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
                 if len(waves[layer]) == 1:
                     x = run_waves(model, waves[layer], x, dt, store, cs, pre_done=[done[layer]],
-                                  out_bf16=xb)
+                                  out_bf16=xb, x_perm=xp)
                 else:
                     x = run_waves(model, waves[layer], x, dt, store, cs,
-                                  issue=lambda w: store.enqueue_loads(w.loads), out_bf16=xb)
+                                  issue=lambda w: store.enqueue_loads(w.loads), out_bf16=xb,
+                                  x_perm=xp)
                 if self.ffn_events is not None:
                     e_b = torch.cuda.Event(enable_timing=True)
                     e_b.record(cs)

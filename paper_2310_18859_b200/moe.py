@@ -242,6 +242,7 @@ class MoEModel:
             self.wo.append(to_bf16(params[pre + "wo"], dev))
             self.w_r.append(to_bf16(params[pre + "w_r"]).float().to(dev))
         self.wc = to_bf16(params["wc"]).float().to(dev)
+        self._prepare_out_proj()
         self._alloc_images()
         h = _lib.load()
         for layer in range(c.num_layers):
@@ -253,6 +254,21 @@ class MoEModel:
                 dst = self.expert_images[layer * c.num_experts + e]
                 _lib.check(h.sida_pack_expert_host(*(a.ctypes.data for a in arrs), c.d_model,
                                                    c.expert_hidden, dst.data_ptr()))
+
+    def _prepare_out_proj(self):
+        """Per layer W_o^T (K-major) + a zero bias row: the B operand of the
+        fused output projection (sida_out_proj_scatter); tcgen05 shapes only."""
+        d = self.config.d_model
+        self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.wo_t = None
+        if d % 64:
+            return
+        nbytes = int(_lib.load().sida_out_proj_bytes(d))
+        self.wo_t = []
+        for w in self.wo:
+            buf = torch.zeros(nbytes // 2, dtype=torch.bfloat16, device=self.device)
+            buf[: d * d] = w.t().contiguous().view(-1)
+            self.wo_t.append(buf)
 
     @classmethod
     def synthetic(cls, config: MoEConfig, seed: int = 0, device=None) -> "MoEModel":
@@ -278,6 +294,7 @@ class MoEModel:
         self.w_r = [randn((d, c.num_experts), math.sqrt(1.0 / d)).float()
                     for _ in range(c.num_layers)]
         self.wc = randn((d, c.num_classes), math.sqrt(1.0 / d)).float()
+        self._prepare_out_proj()
         self._alloc_images()
         s_dh = math.sqrt(2.0 / (d + hh))
         n_el = 2 * d * hh
@@ -335,13 +352,17 @@ class MoEModel:
                 + self.pos_emb.index_select(0, lay.pos).float())
 
     def attention_mix(self, layer: int, x: torch.Tensor, lay: BatchLayout,
-                      xb: torch.Tensor | None = None) -> torch.Tensor:
+                      xb: torch.Tensor | None = None, scatter=None) -> torch.Tensor:
         """x + softmax(q k^T / sqrt(d)) v W_o per sequence (ref moe.py:220-233).
 
-        cuBLAS bf16 GEMMs with fp32 outputs where the result stays fp32:
-        scores (bmm, out_dtype fp32) and the output projection fused with the
-        residual add (addmm, beta = 1). ``xb`` is x already rounded to bf16
-        (the previous layer's FFN epilogue writes it)."""
+        QKV projection and the per-sequence score/context products are cuBLAS
+        bf16 GEMMs (scores with fp32 outputs). The output projection is the
+        tcgen05 GEMM of sida_out_proj_scatter with the residual add fused,
+        and -- given ``scatter = (inv, k, x_perm)`` from the layer's hash
+        table -- it also writes the next FFN's expert-sorted bf16 input rows
+        x_perm[inv[t*k + r]] (the row gather of ref moe.py:253-256), so the
+        FFN needs no gather pass. ``xb`` is x already rounded to bf16 (the
+        previous layer's FFN epilogue writes it)."""
         d = self.config.d_model
         if xb is None:
             xb = x.to(torch.bfloat16)
@@ -360,7 +381,17 @@ class MoEModel:
         ctx = torch.bmm(attn, v).reshape(-1, d)
         if not lay.uniform:
             ctx = ctx.index_select(0, lay.valid_rows)
-        return torch.addmm(x, ctx, self.wo[layer], out_dtype=torch.float32)
+        if self.wo_t is None:  # d not a multiple of 64: cuBLAS
+            if scatter is not None:
+                raise ContractError("fused expert-sorted scatter needs d % 64 == 0")
+            return torch.addmm(x, ctx, self.wo[layer], out_dtype=torch.float32)
+        out = torch.empty_like(x)
+        inv, k, x_perm = scatter if scatter is not None else (None, 0, None)
+        _lib.check(_lib.lib().sida_out_proj_scatter(
+            ctx.data_ptr(), ctx.shape[0], d, self.wo_t[layer].data_ptr(), x.data_ptr(),
+            out.data_ptr(), _lib.ptr(inv), k, _lib.ptr(x_perm), self._err.data_ptr(),
+            torch.cuda.current_stream(self.device).cuda_stream))
+        return out
 
     def pool_classify(self, x: torch.Tensor, lay: BatchLayout) -> torch.Tensor:
         """(n_seq, C): per-sequence mean then the classifier (ref moe.py:264-266)."""
@@ -392,7 +423,8 @@ class MoEModel:
     def moe_apply_rows(self, layer_tables, x: torch.Tensor, k: int, arena, slot_row: torch.Tensor,
                        expert_list: torch.Tensor | None = None, out: torch.Tensor | None = None,
                        y: torch.Tensor | None = None, stream=None,
-                       out_bf16: torch.Tensor | None = None) -> torch.Tensor:
+                       out_bf16: torch.Tensor | None = None,
+                       x_perm: torch.Tensor | None = None) -> torch.Tensor:
         """The SiDA expert FFN for one layer over the whole batch.
 
         ``layer_tables`` = (off (K+1,), perm (R,), alpha_perm (R,)) of this
@@ -410,10 +442,11 @@ class MoEModel:
         off, perm, alpha_perm = layer_tables
         n_tok = x.shape[0]
         rows = n_tok * k
-        x_perm = torch.empty((rows, c.d_model), dtype=torch.bfloat16, device=self.device)
         hidden = torch.empty((rows, c.expert_hidden), dtype=torch.bfloat16, device=self.device)
-        _lib.check(h.sida_gather_rows_bf16(x.data_ptr(), perm.data_ptr(), rows, k, c.d_model,
-                                           x_perm.data_ptr(), sh))
+        if x_perm is None:  # not produced by the fused output projection: gather
+            x_perm = torch.empty((rows, c.d_model), dtype=torch.bfloat16, device=self.device)
+            _lib.check(h.sida_gather_rows_bf16(x.data_ptr(), perm.data_ptr(), rows, k, c.d_model,
+                                               x_perm.data_ptr(), sh))
         err = arena.err_flag
         n_list = 0 if expert_list is None else int(expert_list.numel())
         if out is None:

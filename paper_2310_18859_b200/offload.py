@@ -341,12 +341,14 @@ class ExpertStore:
 
 
 def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=None,
-              issue=None, out_bf16=None, table_layer: int | None = None):
+              issue=None, out_bf16=None, table_layer: int | None = None, x_perm=None):
     """Execute one layer as a sequence of waves on ``stream``: wait for each
     wave's copies, run the grouped FFN over its experts, record the reader
     event. ``issue(wave)`` (optional) enqueues a wave's copies just in time and
     returns their done event. ``out_bf16`` (optional) receives the layer
-    output rounded to bf16 from the same epilogue."""
+    output rounded to bf16 from the same epilogue. ``x_perm`` (optional) is
+    the layer input already in expert-sorted bf16 rows (written by the fused
+    attention output projection); without it each wave gathers."""
     c = model.config
     k = dev_table.k
     layer = waves[0].layer
@@ -369,7 +371,7 @@ def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=N
                 elist = torch.from_numpy(np.asarray(wave.experts, dtype=np.int32)).pin_memory().to(
                     x.device, non_blocking=True)
             model.moe_apply_rows(tables, x, k, store, row, expert_list=elist, out=out, y=y,
-                                 stream=stream, out_bf16=out_bf16)
+                                 stream=stream, out_bf16=out_bf16, x_perm=x_perm)
         ev = torch.cuda.Event()
         ev.record(stream)
         store.mark_read(wave.slot_row, ev)

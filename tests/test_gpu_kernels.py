@@ -308,3 +308,38 @@ def test_hash_ids_bit_exact_vs_oracle_switch_shapes(cuda_device, L, K, T, B, k):
     mism = int((table.ids != ids).sum())
     assert mism == 0, f"{mism} id mismatches"
     np.testing.assert_allclose(table.alphas, al, rtol=1e-11)
+
+
+# --------------------------------------------------- fused attention output projection
+@pytest.mark.parametrize("n,d,k", [(37, 256, 1), (1000, 768, 1), (4096 + 77, 768, 2),
+                                   (2048, 256, 3), (300, 128, 0)])
+def test_out_proj_scatter_vs_torch_fp32(cuda_device, n, d, k):
+    """out = resid + ctx W_o (fp32 reference on the same bf16 values, ref
+    moe.py:232-233) and the expert-sorted bf16 copies x_perm[inv[t*k+r]] =
+    bf16(out[t]) bit-exact against the kernel's own fp32 output."""
+    from paper_2310_18859_b200 import _lib
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n * 7 + d + k)
+    ctx = torch.randn((n, d), generator=g, device="cuda").to(torch.bfloat16)
+    wo = (torch.randn((d, d), generator=g, device="cuda") / d ** 0.5).to(torch.bfloat16)
+    resid = torch.randn((n, d), generator=g, device="cuda")
+    h = _lib.lib()
+    wo_t = torch.zeros(h.sida_out_proj_bytes(d) // 2, dtype=torch.bfloat16, device="cuda")
+    wo_t[: d * d] = wo.t().contiguous().view(-1)
+    out = torch.empty_like(resid)
+    rows = max(n * k, 1)
+    inv = torch.randperm(rows, generator=g, device="cuda").to(torch.int32)
+    x_perm = torch.full((rows, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(h.sida_out_proj_scatter(ctx.data_ptr(), n, d, wo_t.data_ptr(), resid.data_ptr(),
+                                       out.data_ptr(), inv.data_ptr() if k else None, k,
+                                       x_perm.data_ptr() if k else None, err.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    ref = resid + ctx.float() @ wo.float()
+    close_rms(out.cpu().numpy(), ref.cpu().numpy(), 1e-5)
+    if k:
+        want = out.to(torch.bfloat16).repeat_interleave(k, dim=0)  # row t*k + r
+        got = x_perm[inv.long()]
+        assert torch.equal(got.view(torch.int16), want.view(torch.int16))
