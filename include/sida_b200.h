@@ -142,6 +142,14 @@ int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h, cons
  * out: uint64 [2 GEMMs][148 CTAs][8]. Synchronises the device. */
 int sida_debug_gemm_prof(unsigned long long* out);
 
+/* Fused mixing-attention core (ref moe.py:220-233 without the projections):
+ * ctx = softmax(q k^T / sqrt(d)) v per sequence, single head, non-causal, on
+ * tcgen05 (scores and P.V in TMEM, softmax in registers). qkv bf16
+ * (n_tokens, 3d) = [q | k | v]; seq_off int32 (n_seq + 1) device offsets;
+ * every sequence <= 128 tokens (max_len), d % 128 == 0; ctx bf16 (n_tokens, d). */
+int sida_attention_core(const uint16_t* qkv, const int32_t* seq_off, int n_seq, int n_tokens,
+                        int max_len, int d, uint16_t* ctx, void* stream);
+
 /* Mixing-attention output projection (ref moe.py:232-233) on the same
  * tcgen05 GEMM, residual fused: out[t] = resid[t] + ctx[t] W_o (fp32), and,
  * for k >= 1, the next FFN's expert-sorted input x_perm[inv[t*k + r]] =

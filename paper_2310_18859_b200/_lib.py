@@ -44,6 +44,7 @@ SIGNATURES = {
     "sida_combine_ranks": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "sida_gather_bf16_rows": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "sida_unpermute_combine": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
+    "sida_attention_core": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sida_out_proj_bytes": (_sz, [_i]),
     "sida_out_proj_scatter": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "sida_router_topk": (_i, [_vp, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp]),

@@ -1,0 +1,335 @@
+// Fused mixing-attention core on the 5th-gen tensor cores (sm_100a):
+//   ctx = softmax(q k^T / sqrt(d)) v        per sequence, single head, non-causal
+// for sequences of at most 128 tokens (ref moe.py:220-233; the projections
+// q,k,v = x W and the output projection run as GEMMs around this kernel).
+//
+// One CTA per sequence, two CTAs per SM (~105 KB smem, 256 TMEM columns
+// each), so a 256-sequence batch is resident in a single wave. Inside a CTA:
+//
+//   phase 1  S = Q K^T (M=128 queries, N=128 keys, K=d) with tcgen05.mma,
+//            Q and K k-blocks streamed by TMA through a 2-slot ring,
+//            accumulator in TMEM columns [0, 128)
+//   phase 2  softmax rows (4 warps, thread = query row): row max of the
+//            scaled scores over the sequence's keys, e = exp(s/sqrt(d) - m)
+//            written as bf16 straight into the K-major SWIZZLE_128B layout
+//            of the next MMA's A operand; 1/sum kept in a register
+//   phase 3  C = P V in d-chunks of 128 columns (V read MN-major: the token
+//            rows of qkv are the K dimension), TMEM double buffer
+//            {[128,256), [0,128)} so the epilogue of chunk j overlaps the
+//            MMAs of chunk j+1; epilogue scales by 1/sum, rounds to bf16 and
+//            stores through a swizzled smem transpose (coalesced 64 B rows).
+//
+// Keys past the sequence end are masked (their TMA rows belong to the next
+// sequence or are zero-filled past the batch), query rows past it are
+// computed and dropped. softmax(s) V = (e V) / sum: normalising after the
+// product instead of before is exact in real arithmetic; both forms round P
+// to bf16 once.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "sm100_ptx.cuh"
+
+namespace sida {
+namespace attn {
+
+using namespace sm100;
+
+constexpr int BM = 128;        // queries per CTA (one TMEM lane each)
+constexpr int NKEY = 128;      // keys per CTA (max sequence length here)
+constexpr int BK = 64;         // d per phase-1 k-block (one SW128 row)
+constexpr int NC = 128;        // d columns per phase-3 chunk
+constexpr int kSlot = 32 * 1024;        // Q+K k-block (16+16 KB) or V chunk (2 x 16 KB)
+constexpr int kSlots = 2;
+constexpr int kPBytes = BM * NKEY * 2;  // P: 2 K-atoms x 128 rows x 128 B
+constexpr int kStageTile = 32 * 32 * 2; // per-warp bf16 epilogue staging tile
+constexpr int kEpiWarps = 4;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
+constexpr uint32_t kTmemCols = 256;
+constexpr size_t kSmem = 1024 + kSlots * kSlot + kPBytes + kEpiWarps * kStageTile + 256;
+
+// SWIZZLE_128B MN-major operand: 64-element MN groups `lbo` bytes apart, 8-row
+// K groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFF) >> 4);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+__device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 2)
+attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ seq_off,
+                 int d, float scale_log2e, uint16_t* __restrict__ ctx) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ring = smem;
+  uint8_t* sP = ring + kSlots * kSlot;
+  uint8_t* sOut = sP + kPBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + kEpiWarps * kStageTile);
+  uint64_t* full = bars;              // [kSlots]
+  uint64_t* empty = bars + kSlots;    // [kSlots]
+  uint64_t* s_full = bars + 2 * kSlots;
+  uint64_t* p_full = s_full + 1;
+  uint64_t* c_full = p_full + 1;      // [2]
+  uint64_t* c_empty = c_full + 2;     // [2]
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(c_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int seq = blockIdx.x;
+  const int row0 = seq_off[seq];
+  const int T = seq_off[seq + 1] - row0;
+  const int n_kb = d / BK, n_chunks = d / NC;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, kEpiWarps);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&c_full[i], 1);
+      mbar_init(&c_empty[i], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tm_qkv)) : "memory");
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+
+  if (warp == 0) {
+    // ===== TMA producer: 12 (Q, K) k-blocks, then d/NC V chunks, one ring
+    if (lane == 0) {
+      int slot = 0;
+      uint32_t phase = 0;
+      const int n_loads = n_kb + n_chunks;
+      for (int i = 0; i < n_loads; ++i) {
+        mbar_wait(&empty[slot], phase ^ 1);
+        mbar_expect_tx(&full[slot], kSlot);
+        uint8_t* dst = ring + slot * kSlot;
+        const uint32_t fb = smem_u32(&full[slot]);
+        if (i < n_kb) {
+          tma_load_2d<1>(dst, &tm_qkv, i * BK, row0, fb);                  // Q rows
+          tma_load_2d<1>(dst + kSlot / 2, &tm_qkv, d + i * BK, row0, fb);  // K rows
+        } else {
+          const int c0 = 2 * d + (i - n_kb) * NC;
+          tma_load_2d<1>(dst, &tm_qkv, c0, row0, fb);                      // V[:, c0:c0+64]
+          tma_load_2d<1>(dst + kSlot / 2, &tm_qkv, c0 + 64, row0, fb);     // V[:, +64:+128]
+        }
+        if (++slot == kSlots) { slot = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (one thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16<BM, NKEY>();
+      constexpr uint32_t idesc_c = idesc_bf16<BM, NC>() | (1u << 16);  // B (V) MN-major
+      int slot = 0;
+      uint32_t phase = 0;
+      for (int i = 0; i < n_kb; ++i) {
+        mbar_wait(&full[slot], phase);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(ring + slot * kSlot);
+        const uint32_t b0 = a0 + kSlot / 2;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_bf16<1>(tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc_s,
+                       (i | k) != 0);
+        tc_commit<1>(&empty[slot]);
+        if (++slot == kSlots) { slot = 0; phase ^= 1; }
+      }
+      tc_commit<1>(s_full);
+      mbar_wait(p_full, 0);  // P in smem (and S fully read: TMEM cols [0,128) free)
+      tc_fence_after();
+      const uint32_t p0 = smem_u32(sP);
+      for (int j = 0; j < n_chunks; ++j) {
+        const int b = j & 1;
+        if (j >= 2) mbar_wait(&c_empty[b], ((j >> 1) - 1) & 1);
+        mbar_wait(&full[slot], phase);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem + (b == 0 ? 128u : 0u);
+        const uint32_t v0 = smem_u32(ring + slot * kSlot);
+#pragma unroll
+        for (int k = 0; k < NKEY / 16; ++k)  // 16 keys per MMA: P atom k/4, V rows 16k..
+          umma_bf16<1>(d_tmem, sw128_desc(p0 + (k >> 2) * (BM * 128) + (k & 3) * 32),
+                       sw128_mn_desc(v0 + k * 16 * 128, kSlot / 2), idesc_c, k != 0);
+        tc_commit<1>(&empty[slot]);
+        tc_commit<1>(&c_full[b]);
+        if (++slot == kSlots) { slot = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ===== softmax + epilogue: warp w owns TMEM lanes / query rows 32*(w%4)..
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;  // query row within the CTA
+    const uint32_t t_lane = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    mbar_wait(s_full, 0);
+    tc_fence_after();
+    uint32_t v[32];
+    float m = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < NKEY / 32; ++c) {
+      tmem_ld32_nowait(t_lane + c * 32, v);
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (c * 32 + j < T) m = fmaxf(m, __uint_as_float(v[j]));
+    }
+    const float mb = m * scale_log2e;
+    float sum = 0.f;
+    const uint32_t prow = smem_u32(sP) + r * 128;
+#pragma unroll
+    for (int c = 0; c < NKEY / 32; ++c) {
+      tmem_ld32_nowait(t_lane + c * 32, v);
+      tmem_wait_ld();
+      float e[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        e[j] = c * 32 + j < T ? exp2f(fmaf(__uint_as_float(v[j]), scale_log2e, -mb)) : 0.f;
+        sum += e[j];
+      }
+      // keys c*32 .. +31 = atom c/2, 16-B chunks 4*(c%2) .. +3 of row r
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 o;
+        o.x = bf16x2_rn(e[q * 8 + 0], e[q * 8 + 1]);
+        o.y = bf16x2_rn(e[q * 8 + 2], e[q * 8 + 3]);
+        o.z = bf16x2_rn(e[q * 8 + 4], e[q * 8 + 5]);
+        o.w = bf16x2_rn(e[q * 8 + 6], e[q * 8 + 7]);
+        const int chunk = (c & 1) * 4 + q;
+        sts128(prow + (c >> 1) * (BM * 128) + ((chunk ^ (r & 7)) << 4), o);
+      }
+    }
+    const float inv_sum = 1.f / sum;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P -> tensor core
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_local(p_full);
+
+    // epilogue: chunk j of C -> bf16 ctx rows, through a swizzled 32x32 tile
+    const uint32_t stile = smem_u32(sOut + (warp - 2) * kStageTile);
+    const int q_row0 = row0 + quarter * 32;  // first global row of this warp
+    for (int j = 0; j < n_chunks; ++j) {
+      const int b = j & 1;
+      mbar_wait(&c_full[b], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t t_c = t_lane + (b == 0 ? 128u : 0u);
+#pragma unroll
+      for (int c = 0; c < NC / 32; ++c) {
+        tmem_ld32_nowait(t_c + c * 32, v);
+        tmem_wait_ld();
+        const uint32_t srow = stile + lane * 64;
+        const int sw = (lane >> 1) & 3;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 o;
+          o.x = bf16x2_rn(__uint_as_float(v[q * 8 + 0]) * inv_sum,
+                          __uint_as_float(v[q * 8 + 1]) * inv_sum);
+          o.y = bf16x2_rn(__uint_as_float(v[q * 8 + 2]) * inv_sum,
+                          __uint_as_float(v[q * 8 + 3]) * inv_sum);
+          o.z = bf16x2_rn(__uint_as_float(v[q * 8 + 4]) * inv_sum,
+                          __uint_as_float(v[q * 8 + 5]) * inv_sum);
+          o.w = bf16x2_rn(__uint_as_float(v[q * 8 + 6]) * inv_sum,
+                          __uint_as_float(v[q * 8 + 7]) * inv_sum);
+          sts128(srow + ((q ^ sw) << 4), o);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = i * 8 + (lane >> 2), q = lane & 3;
+          const uint4 val = lds128(stile + rr * 64 + ((q ^ ((rr >> 1) & 3)) << 4));
+          if (quarter * 32 + rr < T)
+            *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(q_row0 + rr) * d + j * NC +
+                                      c * 32 + q * 8) = val;
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&c_empty[b]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+}  // namespace attn
+}  // namespace sida
+
+using namespace sida;
+
+// qkv: bf16 (n_tokens, 3d) = [q | k | v] per token (x @ [Wq|Wk|Wv]);
+// seq_off: int32 (n_seq + 1) exclusive offsets on the concatenated token axis;
+// every sequence at most 128 tokens; ctx: bf16 (n_tokens, d).
+extern "C" int sida_attention_core(const uint16_t* qkv, const int32_t* seq_off, int n_seq,
+                                   int n_tokens, int max_len, int d, uint16_t* ctx,
+                                   void* stream) {
+  SIDA_REQUIRE(d % attn::NC == 0 && d >= attn::NC, SIDA_ERR_UNSUPPORTED,
+               "fused attention needs d multiple of %d (d=%d)", attn::NC, d);
+  SIDA_REQUIRE(max_len >= 1 && max_len <= attn::NKEY, SIDA_ERR_UNSUPPORTED,
+               "fused attention handles sequences of at most %d tokens (got %d)", attn::NKEY,
+               max_len);
+  SIDA_REQUIRE(n_seq >= 0 && n_tokens >= 0, SIDA_ERR_CONTRACT, "bad attention dims");
+  SIDA_REQUIRE(qkv && seq_off && ctx, SIDA_ERR_CONTRACT,
+               "null pointer passed to sida_attention_core");
+  if (n_seq == 0 || n_tokens == 0) return SIDA_OK;
+  auto fn = attn::encode_fn();
+  SIDA_REQUIRE(fn, SIDA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(3 * d), static_cast<cuuint64_t>(n_tokens)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(3 * d) * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(qkv), dims,
+                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  SIDA_REQUIRE(r == CUDA_SUCCESS, SIDA_ERR_CUDA, "tensor map encode failed: %d", (int)r);
+  static bool configured = false;
+  if (!configured) {
+    SIDA_CUDA(cudaFuncSetAttribute(attn::attn_core_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)attn::kSmem));
+    configured = true;
+  }
+  const float scale_log2e = 1.4426950408889634f / sqrtf(static_cast<float>(d));
+  attn::attn_core_kernel<<<n_seq, attn::kThreads, attn::kSmem, as_stream(stream)>>>(
+      tm, seq_off, d, scale_log2e, ctx);
+  SIDA_LAUNCH_CHECK();
+  return SIDA_OK;
+}

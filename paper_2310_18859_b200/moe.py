@@ -21,6 +21,7 @@ bf16, sida_slot_bytes(d, h) bytes) streamed into HBM slots by
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass
 
@@ -29,6 +30,11 @@ import torch
 
 from . import _lib
 from .errors import ContractError
+
+
+# A/B switch for measurements: SIDA_ATTN_CUBLAS=1 runs the attention core as
+# cuBLAS batched products + torch softmax instead of sida_attention_core.
+_ATTN_CUBLAS = bool(os.environ.get("SIDA_ATTN_CUBLAS"))
 
 
 @dataclass
@@ -154,6 +160,8 @@ class BatchLayout:
         self.tokens = tokens  # int32 (n_tokens,) on device
         if self.uniform:  # positions derived on the device: no per-token H2D traffic
             self.pos = torch.arange(self.n_tokens, device=device) % self.max_len
+            self.seq_off = torch.arange(0, self.n_tokens + 1, self.max_len, device=device,
+                                        dtype=torch.int32)
             return
 
         def h2d(a):
@@ -162,6 +170,7 @@ class BatchLayout:
 
         seq_id = np.repeat(np.arange(self.n_seq), self.lengths)
         self.pos = h2d(np.arange(self.n_tokens) - off[seq_id])
+        self.seq_off = h2d(off.astype(np.int32))
         self.len_t = h2d(np.asarray(self.lengths, dtype=np.float32))
         if not self.uniform:
             pad = np.full((self.n_seq, self.max_len), self.n_tokens, dtype=np.int64)
@@ -355,8 +364,10 @@ class MoEModel:
                       xb: torch.Tensor | None = None, scatter=None) -> torch.Tensor:
         """x + softmax(q k^T / sqrt(d)) v W_o per sequence (ref moe.py:220-233).
 
-        QKV projection and the per-sequence score/context products are cuBLAS
-        bf16 GEMMs (scores with fp32 outputs). The output projection is the
+        The QKV projection is a cuBLAS bf16 GEMM. For sequences of at most 128
+        tokens (d % 128 == 0) the score / softmax / context core is the fused
+        tcgen05 kernel sida_attention_core; longer sequences use cuBLAS batched
+        products (scores with fp32 outputs) and torch softmax. The output projection is the
         tcgen05 GEMM of sida_out_proj_scatter with the residual add fused,
         and -- given ``scatter = (inv, k, x_perm)`` from the layer's hash
         table -- it also writes the next FFN's expert-sorted bf16 input rows
@@ -367,6 +378,13 @@ class MoEModel:
         if xb is None:
             xb = x.to(torch.bfloat16)
         qkv = xb @ self.wqkv[layer]
+        if d % 128 == 0 and lay.max_len <= 128 and not _ATTN_CUBLAS:
+            # fused tcgen05 core: scores, softmax and P.V without HBM round trips
+            ctx = torch.empty((lay.n_tokens, d), dtype=torch.bfloat16, device=x.device)
+            _lib.check(_lib.lib().sida_attention_core(
+                qkv.data_ptr(), lay.seq_off.data_ptr(), lay.n_seq, lay.n_tokens, lay.max_len, d,
+                ctx.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+            return self._out_proj(layer, x, ctx, scatter)
         if lay.uniform:
             qkv = qkv.view(lay.n_seq, lay.max_len, 3 * d)
         else:
@@ -381,6 +399,10 @@ class MoEModel:
         ctx = torch.bmm(attn, v).reshape(-1, d)
         if not lay.uniform:
             ctx = ctx.index_select(0, lay.valid_rows)
+        return self._out_proj(layer, x, ctx, scatter)
+
+    def _out_proj(self, layer: int, x: torch.Tensor, ctx: torch.Tensor, scatter):
+        d = self.config.d_model
         if self.wo_t is None:  # d not a multiple of 64: cuBLAS
             if scatter is not None:
                 raise ContractError("fused expert-sorted scatter needs d % 64 == 0")

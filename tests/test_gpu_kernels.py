@@ -343,3 +343,47 @@ def test_out_proj_scatter_vs_torch_fp32(cuda_device, n, d, k):
         want = out.to(torch.bfloat16).repeat_interleave(k, dim=0)  # row t*k + r
         got = x_perm[inv.long()]
         assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+
+
+# ------------------------------------------------------------- fused attention core
+@pytest.mark.parametrize("lengths,d", [([128] * 3, 768), ([1, 5, 77, 128, 64, 128], 256),
+                                       ([100] * 7 + [3], 128), ([128] * 300, 768)])
+def test_attention_core_vs_torch_fp32(cuda_device, lengths, d):
+    """ctx = softmax(q k^T / sqrt(d)) v per sequence (ref moe.py:220-233 core)
+    against an fp32 torch reference on the same bf16 q, k, v, at the bf16 bar
+    (rtol 2e-2): P and ctx are rounded to bf16 once each, exactly like the
+    cuBLAS/torch path it replaces (both measure ~1.2e-2 * rms worst case,
+    tools/attn_check.py)."""
+    from paper_2310_18859_b200 import _lib
+
+    n = sum(lengths)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + d)
+    qkv = (torch.randn((n, 3 * d), generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+    off = np.zeros(len(lengths) + 1, dtype=np.int32)
+    np.cumsum(lengths, out=off[1:])
+    seq_off = torch.from_numpy(off).cuda()
+    ctx = torch.full((n, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _lib.check(_lib.lib().sida_attention_core(qkv.data_ptr(), seq_off.data_ptr(), len(lengths),
+                                              n, max(lengths), d, ctx.data_ptr(),
+                                              torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    q, k, v = qkv.float().split(d, dim=1)
+    ref = torch.empty((n, d), device="cuda")
+    for s in range(len(lengths)):
+        a, b = int(off[s]), int(off[s + 1])
+        att = torch.softmax(q[a:b] @ k[a:b].T / d ** 0.5, dim=-1)
+        ref[a:b] = att @ v[a:b]
+    close_rms(ctx.float().cpu().numpy(), ref.cpu().numpy(), 2e-2)
+
+
+def test_attention_core_contracts(cuda_device):
+    from paper_2310_18859_b200 import _lib
+    from paper_2310_18859_b200.errors import NativeLibraryError
+
+    qkv = torch.zeros((300, 3 * 128), dtype=torch.bfloat16, device="cuda")
+    off = torch.tensor([0, 129, 300], dtype=torch.int32, device="cuda")
+    ctx = torch.empty((300, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(NativeLibraryError):  # sequence longer than 128 tokens
+        _lib.check(_lib.lib().sida_attention_core(qkv.data_ptr(), off.data_ptr(), 2, 300, 171,
+                                                  128, ctx.data_ptr(), None))
