@@ -82,6 +82,8 @@ class SidaEngine:
             lo = hi = 0
         self.hash_stream, self.compute_stream = streams or (
             torch.cuda.Stream(device=dev, priority=lo), torch.cuda.Stream(device=dev, priority=hi))
+        if os.environ.get("SIDA_HASH_SERIAL") and streams is None:  # A/B: one stream
+            self.hash_stream = self.compute_stream
         self.store = store or ExpertStore.for_budget(model, budget)
         self.state = getattr(self.store, "residency_state", None) or ResidencyState()
         self.store.residency_state = self.state
