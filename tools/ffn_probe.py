@@ -21,6 +21,9 @@ p.add_argument("--d", type=int, default=768)
 p.add_argument("--h", type=int, default=3072)
 p.add_argument("--iters", type=int, default=20)
 p.add_argument("--no-cublas", action="store_true")
+p.add_argument("--alias-slots", type=int, default=0,
+               help="map every expert onto this many slots (weights L2-resident: isolates "
+                    "the HBM weight stream)")
 a = p.parse_args()
 cfg = MoEConfig(vocab_size=64, d_model=a.d, num_layers=1, num_experts=a.experts,
                 expert_hidden=a.h, max_seq_len=16)
@@ -41,6 +44,8 @@ e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=Tr
 from paper_2310_18859_b200.offload import Wave, run_waves  # noqa: E402
 need = list(range(K))
 wave = Wave(0, [], need, store.slot_row(0, need))
+if a.alias_slots:
+    wave.slot_row = (wave.slot_row % a.alias_slots).astype(np.int32)
 for _ in range(3):
     run_waves(model, [wave], x, dt, store, torch.cuda.current_stream())
 torch.cuda.synchronize()
