@@ -35,6 +35,8 @@ from .errors import ContractError
 # A/B switch for measurements: SIDA_ATTN_CUBLAS=1 runs the attention core as
 # cuBLAS batched products + torch softmax instead of sida_attention_core.
 _ATTN_CUBLAS = bool(os.environ.get("SIDA_ATTN_CUBLAS"))
+# SIDA_OUTPROJ_CUBLAS=1: output projection as cuBLAS addmm (+ the FFN's row gather)
+_OUTPROJ_CUBLAS = bool(os.environ.get("SIDA_OUTPROJ_CUBLAS"))
 
 
 @dataclass
@@ -270,7 +272,7 @@ class MoEModel:
         d = self.config.d_model
         self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.wo_t = None
-        if d % 64:
+        if d % 64 or _OUTPROJ_CUBLAS:
             return
         nbytes = int(_lib.load().sida_out_proj_bytes(d))
         self.wo_t = []
