@@ -52,7 +52,8 @@ def parse():
     p.add_argument("--budget-frac", type=float, default=1.0,
                    help="HBM expert budget as a fraction of all expert bytes")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-steps", type=int, default=2)
+    p.add_argument("--cpu-steps", type=int, default=8,
+                   help="CPU oracle sample size (sequences); ~1.3 s of CPU work each")
     p.add_argument("--parallel", default="dp", choices=["dp", "ep"],
                    help="N>1: data-parallel replicas (default) or expert parallel over NCCL")
     p.add_argument("--no-streaming", action="store_true",
@@ -342,7 +343,8 @@ def run_ours(args):
     wall = time.perf_counter() - t_wall0
     sampler.__exit__()
     ms = ev_start.elapsed_time(ev_end)
-    ffn_ms = [a.elapsed_time(b) for a, b, _ in (engine.ffn_events or [])]
+    ffn_ms = [a.elapsed_time(b) for a, b, _, _ in (engine.ffn_events or [])]
+    ffn_active = [n for _, _, _, n in (engine.ffn_events or [])]
     mix_ms = [a.elapsed_time(b) for a, b in engine.mix_events]
     engine.ffn_events = None
     engine.mix_events = []
@@ -381,20 +383,35 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel: grouped FFN (GEMM1 + GEMM2; the row
     # gather is folded into the attention output projection's epilogue)
+    # roofline time = max(FLOPs / tensor peak, min bytes / HBM peak)
+    # with FLOPs = 4 d h N k and min bytes = active experts x (2dh+h+d) x 2 (the
+    # weights, once) + 3 N k d x 2 (x_perm read, residual read, output write)
     peaks = measured_peaks()
-    flops = 4.0 * n_tok * cfg.d_model * cfg.expert_hidden   # per layer launch set
+    d_, h_ = cfg.d_model, cfg.expert_hidden
+    flops = 4.0 * n_tok * d_ * h_   # per layer launch set
+    n_active = float(np.mean(ffn_active)) if ffn_active else float(cfg.num_experts)
+    min_bytes = n_active * (2 * d_ * h_ + h_ + d_) * 2 + 3.0 * n_tok * d_ * 2
     traffic = None
     tpath = os.path.join(REPO, "profiles", "r1", "ffn_traffic.json")
     if os.path.exists(tpath) and n_tok == 32768 and cfg.num_experts == 8:
         traffic = json.load(open(tpath))["traffic_bytes_per_launch_set"]
     ffn_avg_ms = float(np.mean(ffn_ms)) if ffn_ms else None
-    achieved = flops / (ffn_avg_ms / 1e3) / 1e12 if ffn_avg_ms else None
-    peak = peaks.get("bf16_tflops_sustained", 1373.4)
+    peak_t = peaks.get("bf16_tflops_sustained", 1373.4)
+    peak_b = peaks.get("hbm_gbs", 6549.4)
+    t_tensor = flops / (peak_t * 1e12) * 1e3    # ms
+    t_hbm = min_bytes / (peak_b * 1e9) * 1e3    # ms
+    if t_tensor >= t_hbm:
+        bound, unit, peak = "tensor", "TFLOP/s", peak_t
+        achieved = flops / (ffn_avg_ms / 1e3) / 1e12 if ffn_avg_ms else None
+    else:
+        bound, unit, peak = "hbm", "GB/s", peak_b
+        achieved = min_bytes / (ffn_avg_ms / 1e3) / 1e9 if ffn_avg_ms else None
     step_ms = ms / args.steps
     clocks = sampler.summary()
     # hash: lstm x2, rows_gemm x2, block offsets, attention; permute: 3; per layer:
-    # out-projection (+ scatter) + GEMM1 + GEMM2 (EP: + gather, regroup, combine)
-    launches_per_step = 6 + 3 + cfg.num_layers * (6 if ep_mode else 3)
+    # attention core + out-projection (+ scatter) + GEMM1 + GEMM2 (EP: + gather,
+    # regroup, combine; the QKV projection is cuBLAS and not counted)
+    launches_per_step = 6 + 3 + cfg.num_layers * (7 if ep_mode else 4)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rate, work, detail = cpu_sample(dict(BASE8, num_experts=args.experts), T, args.cpu_steps)
@@ -422,10 +439,15 @@ def run_ours(args):
                           "loads_timed": rep.expert_loads if rep else None},
         "expert_streaming": streaming,
         "roofline": {"kernel": "grouped_ffn (tcgen05 GEMM1 + GEMM2, per layer)",
-                     "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained",
-                     "flops_per_launch": flops, "avg_ms": ffn_avg_ms,
+                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained / hbm_gbs",
+                     "flops_per_launch": flops, "min_bytes_per_launch": min_bytes,
+                     "active_experts_per_layer": n_active,
+                     "roofline_ms": max(t_tensor, t_hbm), "tensor_ms": t_tensor,
+                     "hbm_ms": t_hbm,
+                     "tflops_achieved": flops / (ffn_avg_ms / 1e3) / 1e12 if ffn_avg_ms else None,
+                     "avg_ms": ffn_avg_ms,
                      "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms if ffn_avg_ms else None,
                      "attention_mix_avg_ms": float(np.mean(mix_ms)) if mix_ms else None},
         "cpu_baseline": cpu,

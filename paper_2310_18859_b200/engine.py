@@ -171,7 +171,7 @@ class SidaEngine:
                 if self.ffn_events is not None:
                     e_b = torch.cuda.Event(enable_timing=True)
                     e_b.record(cs)
-                    self.ffn_events.append((e_a, e_b, x.shape[0]))
+                    self.ffn_events.append((e_a, e_b, x.shape[0], len(required[layer])))
             logits = model.pool_classify(x, lay)
         ev1.record(cs)
         resident_req = [k for k in table.required_experts() if k in state.resident]
