@@ -32,6 +32,7 @@ from .offload import (
     memory_reduction,
     plan_placement,
 )
+from .checkpoint import load_moe, load_predictor, save_moe, save_predictor
 from .pipeline import HashTableQueue, ServingReport, fidelity, serve_sida, serve_standard
 
 __version__ = "0.1.0"

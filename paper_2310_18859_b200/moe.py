@@ -136,7 +136,10 @@ class Rng:
 def to_bf16(a: np.ndarray, device=None) -> torch.Tensor:
     """float64 -> float32 (RNE) -> bfloat16 (RNE): the one rounding recipe the
     GPU model and the parity oracle share (tests/test_oracle_golden.py)."""
-    t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(torch.float32)
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if not a.flags.writeable:  # memory-mapped checkpoint tensors
+        a = a.copy()
+    t = torch.from_numpy(a).to(torch.float32)
     t = t.to(torch.bfloat16)
     return t if device is None else t.to(device)
 

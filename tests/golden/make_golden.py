@@ -226,7 +226,24 @@ def ensure_case():
         json.dump(cases, fh)
 
 
+def checkpoint_case():
+    """Reference-written containers (ref checkpoint.py, moe.py:581-596,
+    predictor.py:550-571): a small tcgen05-shaped model and its predictor."""
+    from sida.moe import save_moe
+    from sida.predictor import save_predictor
+
+    cfg = MoEConfig(vocab_size=64, d_model=64, num_layers=2, num_experts=4, expert_hidden=128,
+                    max_seq_len=16, routing_k=1, num_classes=3)
+    save_moe(MoEModel(cfg, Rng(0)), os.path.join(HERE, "mini64.sidamoe"))
+    net = PredictorNet(PredictorConfig(compress_dim=8, lstm_hidden=16), cfg.d_model,
+                       cfg.num_layers, cfg.num_experts, Rng(1))
+    save_predictor(net, os.path.join(HERE, "mini64.sidahsh"))
+
+
 def main():
+    if "--checkpoint" in sys.argv:  # container fixtures only
+        checkpoint_case()
+        return
     if "--router" in sys.argv:  # router-mode fixtures only (added after the first set)
         router_main()
         return
@@ -240,6 +257,7 @@ def main():
                lengths=[128] * 8, ks=(1,))
     planner_case()
     router_main()
+    checkpoint_case()
 
 
 def router_main():
