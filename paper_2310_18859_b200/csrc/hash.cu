@@ -562,14 +562,19 @@ attn_heads_kernel(const AttnArgs a) {
 //   sparsemax rows      (warp per row, Michelot threshold; weights in place)
 //   R  = W V + h2       (64 x H, 4 x 3 tile per thread)
 //   Z  = R [heads]      (64 x L*K in layer chunks of <= 128 columns)
-//   softmax / top-k     (thread per (row, layer))
+//   softmax / top-k     (K <= 32: thread per (row, layer); else warp per (row,
+//                        layer); K > 128: online max/sum/top-k
+//                        state per row across 128-expert slices)
 // The arithmetic per element is the same as attn_heads_kernel; only the
 // schedule changes (independent accumulators instead of dependent chains).
 constexpr int kBR = 64;        // rows per block
 constexpr int kBT = 128;       // max keys
 constexpr int kQP = 49;        // pitch (doubles) of Q / K / R rows
 constexpr int kSP = kBT + 1;   // pitch of S / Z rows
-constexpr int kBlockSmem = (kBT * kQP + kBT * 48 + kBR * kQP + kBR * kSP) * 8;
+constexpr int kMaxBlockTop = 8;                    // eval_top_k of the blocked path
+constexpr int kStatePitch = 2 + 2 * kMaxBlockTop;   // online heads state per row
+constexpr int kBlockSmem =
+    (kBT * kQP + kBT * 48 + kBR * kQP + kBR * kSP + kBR * kStatePitch) * 8;
 
 struct BlockArgs {
   AttnArgs a;
@@ -704,63 +709,170 @@ attn_block_kernel(const BlockArgs ba) {
   }
   __syncthreads();
 
-  // ---- heads in chunks of layers (<= 128 logit columns per chunk)
-  const int lpc = max(1, kBT / K);  // layers per chunk
+  // ---- heads. Logit columns in chunks of <= kBT: whole layers when K <= kBT
+  // (lpc layers per chunk), else kBT-expert slices of one layer with an
+  // online (max, sum, top-k) state per row carried across the slices.
+  const int LK = L * K;
+  const int lpc = K <= kBT ? kBT / K : 1;             // layers per chunk
+  const int cpl = K <= kBT ? 1 : (K + kBT - 1) / kBT;  // chunks per layer
+  double* st = sS + kBR * kSP;                         // kBR x kStatePitch online state
   for (int l0 = 0; l0 < L; l0 += lpc) {
     const int nl = min(lpc, L - l0);
-    const int ncol = nl * K;
-    // Z = R hw[:, l0*K : (l0+nl)*K]: rows ty*4+i, columns tx + 16 m (m < 8)
-    {
-      double acc[4][8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
-      const double* W = ba.hwp + (size_t)l0 * K;
-      const int LK = L * K;
-      for (int c = 0; c < H; ++c) {
-        double rr[4], w[8];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) rr[i] = sQ[(ty * 4 + i) * kQP + c];
-#pragma unroll
-        for (int m = 0; m < 8; ++m) w[m] = (tx + 16 * m < ncol) ? W[(size_t)c * LK + tx + 16 * m] : 0.0;
+    for (int ch = 0; ch < cpl; ++ch) {
+      const int c0 = ch * kBT;
+      const int ncol = K <= kBT ? nl * K : min(kBT, K - c0);
+      // Z = R hw[:, col0 : col0 + ncol]: rows ty*4+i, columns tx + 16 m (m < 8);
+      // the (H x ncol) weight slice is staged in the (dead) key buffer
+      {
+        const double* W = ba.hwp + (size_t)l0 * K + c0;
+        double* sW = sK;  // H x kBT
+        for (int i = tid; i < H * kBT; i += 256) {
+          const int c = i / kBT, j = i % kBT;
+          sW[i] = j < ncol ? __ldg(W + (size_t)c * LK + j) : 0.0;
+        }
+        __syncthreads();
+        double acc[4][8];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int m = 0; m < 8; ++m) acc[i][m] = fma(rr[i], w[m], acc[i][m]);
-      }
+          for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
+        for (int c = 0; c < H; ++c) {
+          double rr[4], w[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i) rr[i] = sQ[(ty * 4 + i) * kQP + c];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) sS[(ty * 4 + i) * kSP + tx + 16 * m] = acc[i][m];
+          for (int m = 0; m < 8; ++m) w[m] = sW[c * kBT + tx + 16 * m];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int m = 0; m < 8; ++m) acc[i][m] = fma(rr[i], w[m], acc[i][m]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int m = 0; m < 8; ++m) sS[(ty * 4 + i) * kSP + tx + 16 * m] = acc[i][m];
+      }
+      __syncthreads();
+      if (K <= 32) {
+        // small K: thread per (row, layer), the row's K logits in place in smem
+        for (int pr = tid; pr < rows * nl; pr += 256) {
+          const int r = pr / nl, l = l0 + pr % nl;
+          double* z = sS + r * kSP + (l - l0) * K;
+          const double* hb = a.hb + (size_t)l * K;
+          double zmax = -INFINITY;
+          for (int e = 0; e < K; ++e) {
+            z[e] += hb[e];
+            zmax = fmax(zmax, z[e]);
+          }
+          double ssum = 0.0;
+          for (int e = 0; e < K; ++e) {
+            z[e] = exp(z[e] - zmax);
+            ssum += z[e];
+          }
+          for (int e = 0; e < K; ++e) z[e] = z[e] / ssum;
+          for (int rk = 0; rk < a.topk; ++rk) {
+            double best = -1.0;
+            int bi = 0;
+            for (int e = 0; e < K; ++e)
+              if (z[e] > best) { best = z[e]; bi = e; }
+            emit(a, l, base + r0 + r, rk, bi, best);
+            z[bi] = -2.0;
+          }
+        }
+        __syncthreads();
+        continue;
+      }
+      // warp per (row, layer of the chunk): lanes over the chunk's experts
+      for (int pr = wib; pr < rows * nl; pr += 8) {
+        const int r = pr / nl, l = l0 + pr % nl;
+        const int cw = K <= kBT ? K : ncol;                  // experts in this slice
+        const double* zr = sS + r * kSP + (l - l0) * (K <= kBT ? K : 0);
+        const double* hb = a.hb + (size_t)l * K + c0;
+        double z[4];
+        double zmax = -INFINITY;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int e = lane + 32 * m;
+          z[m] = e < cw ? zr[e] + hb[e] : -INFINITY;
+          zmax = fmax(zmax, z[m]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+        if (K <= kBT) {
+          // whole row here: softmax then top-k on the probabilities, exactly
+          // ref numkit.py:28-33 / :87-93 (descending, ties to the lower index)
+          double p[4], ssum = 0.0;
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            p[m] = lane + 32 * m < cw ? exp(z[m] - zmax) : 0.0;
+            ssum += p[m];
+          }
+          ssum = warp_sum(ssum);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) p[m] = lane + 32 * m < cw ? p[m] / ssum : -2.0;
+          for (int rk = 0; rk < a.topk; ++rk) {
+            double best = -1.0;
+            int bi = 0x7fffffff;
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (p[m] > best) { best = p[m]; bi = lane + 32 * m; }
+            seg_argmax(best, bi, 32);
+            if (lane == 0) emit(a, l, base + r0 + r, rk, bi, best);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (lane + 32 * m == bi) p[m] = -2.0;
+          }
+        } else {
+          // online state: st[r] = {max, sum, (logit, id) x topk}, ids ranked
+          // by logit (= probability order), ties to the lower index
+          double* srow = st + r * kStatePitch;
+          double esum = 0.0;
+          double M = zmax;
+          if (ch > 0) M = fmax(srow[0], zmax);
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+            if (lane + 32 * m < cw) esum += exp(z[m] - M);
+          esum = warp_sum(esum);
+          const double S = ch > 0 ? srow[1] * exp(srow[0] - M) + esum : esum;
+          for (int rk = 0; rk < a.topk; ++rk) {
+            double best = -INFINITY;
+            int bi = 0x7fffffff;
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (lane + 32 * m < cw && z[m] > best) { best = z[m]; bi = lane + 32 * m; }
+            seg_argmax(best, bi, 32);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+              if (lane + 32 * m == bi) z[m] = -INFINITY;
+            if (lane == 0 && bi != 0x7fffffff) {
+              // insert (best, c0 + bi) into the ranked list (earlier slices
+              // hold lower ids, so equal logits keep the earlier entry first)
+              double* lst = srow + 2;
+              const int n_have = ch > 0 ? a.topk : rk;
+              int pos = n_have;
+              while (pos > 0 && lst[2 * (pos - 1)] < best) --pos;
+              if (pos < a.topk) {
+                for (int q = min(n_have, a.topk - 1); q > pos; --q) {
+                  lst[2 * q] = lst[2 * (q - 1)];
+                  lst[2 * q + 1] = lst[2 * (q - 1) + 1];
+                }
+                lst[2 * pos] = best;
+                lst[2 * pos + 1] = (double)(c0 + bi);
+              }
+            }
+          }
+          if (lane == 0) {
+            srow[0] = M;
+            srow[1] = S;
+            if (ch == cpl - 1)
+              for (int rk = 0; rk < a.topk; ++rk)
+                emit(a, l, base + r0 + r, rk, (int)srow[2 + 2 * rk + 1],
+                     exp(srow[2 + 2 * rk] - M) / S);
+          }
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    // softmax over K + top-k per (row, layer)
-    for (int pr = tid; pr < rows * nl; pr += 256) {
-      const int r = pr / nl, l = l0 + pr % nl;
-      double* z = sS + r * kSP + (l - l0) * K;
-      const double* hb = a.hb + (size_t)l * K;
-      double zmax = -INFINITY;
-      for (int e = 0; e < K; ++e) {
-        z[e] += hb[e];
-        zmax = fmax(zmax, z[e]);
-      }
-      double ssum = 0.0;
-      for (int e = 0; e < K; ++e) {
-        z[e] = exp(z[e] - zmax);
-        ssum += z[e];
-      }
-      for (int e = 0; e < K; ++e) z[e] = z[e] / ssum;
-      for (int rk = 0; rk < a.topk; ++rk) {
-        double best = -1.0;
-        int bi = 0;
-        for (int e = 0; e < K; ++e)
-          if (z[e] > best) { best = z[e]; bi = e; }
-        emit(a, l, base + r0 + r, rk, bi, best);
-        z[bi] = -2.0;
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -1002,7 +1114,7 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
                                    (int)smem));
     configured = smem;
   }
-  if (max_len <= kBT && K <= kBT && H <= 48 && !a.prof) {
+  if (max_len <= kBT && topk <= kMaxBlockTop && H <= 48 && !a.prof) {
     // blocked path: register-tiled fp64 GEMM shapes, one CTA per 64 rows
     static bool cfg_block = false;
     if (!cfg_block) {

@@ -273,9 +273,13 @@ def test_hash_with_callable_embed_fn(cuda_device):
     np.testing.assert_allclose(table.alphas.sum(axis=2), 1.0, atol=1e-9)  # full width
 
 
-@pytest.mark.parametrize("L,K,T,B,k", [(12, 128, 128, 6, 1), (12, 8, 96, 4, 2), (2, 256, 512, 2, 3)])
+@pytest.mark.parametrize("L,K,T,B,k", [(12, 128, 128, 6, 1), (12, 8, 96, 4, 2), (2, 256, 512, 2, 3),
+                                       (12, 256, 128, 4, 2), (3, 1000, 100, 3, 4),
+                                       (2, 200, 128, 3, 8), (2, 129, 64, 2, 1)])
 def test_hash_ids_bit_exact_vs_oracle_switch_shapes(cuda_device, L, K, T, B, k):
-    """Switch-base predictor heads (K = 8 / 128 / 256, 12 layers), up to T=512."""
+    """Switch-base predictor heads (K = 8 / 128 / 256, 12 layers), up to T=512;
+    K > 128 in the blocked kernel runs the online (max, sum, top-k) state over
+    128-expert slices (K = 129, 200, 256, 1000; top-k up to 8)."""
     from paper_2310_18859_b200.moe import MoEConfig, MoEModel, SequenceBatch
     from paper_2310_18859_b200.predictor import PredictorConfig, PredictorNet, build_hash_table
 
