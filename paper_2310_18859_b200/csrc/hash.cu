@@ -555,42 +555,46 @@ attn_heads_kernel(const AttnArgs a) {
 
 
 // ---------------------------------------------------------------------------
-// Blocked (GEMM-shaped) attention + heads for sequences of T <= 128: one CTA
-// per (sequence, 64 query rows), 256 threads as a 16 x 16 grid with register
-// tiles, everything staged in smem:
-//   S  = Q K^T          (64 x T, 4 x 8 tile per thread, 48-long k loop)
+// Blocked (GEMM-shaped) attention + heads: one CTA per (sequence, BR query
+// rows) -- BR = 64 for T <= 128, BR = 32 for T <= 512 -- 256 threads as a
+// 16 x 16 grid with register tiles (RT = BR/16 rows per thread), keys and
+// values streamed through smem in chunks of 128:
+//   S  = Q K^T          (BR x T, RT x 8 tile per thread, 48-long k loop)
 //   sparsemax rows      (warp per row, Michelot threshold; weights in place)
-//   R  = W V + h2       (64 x H, 4 x 3 tile per thread)
-//   Z  = R [heads]      (64 x L*K in layer chunks of <= 128 columns)
+//   R  = W V + h2       (BR x H, RT x 3 tile per thread, over V chunks)
+//   Z  = R [heads]      (BR x L*K in layer chunks of <= 128 columns)
 //   softmax / top-k     (K <= 32: thread per (row, layer); else warp per (row,
 //                        layer); K > 128: online max/sum/top-k
 //                        state per row across 128-expert slices)
 // The arithmetic per element is the same as attn_heads_kernel; only the
 // schedule changes (independent accumulators instead of dependent chains).
-constexpr int kBR = 64;        // rows per block
-constexpr int kBT = 128;       // max keys
+constexpr int kBT = 128;       // key / logit chunk
 constexpr int kQP = 49;        // pitch (doubles) of Q / K / R rows
-constexpr int kSP = kBT + 1;   // pitch of S / Z rows
 constexpr int kMaxBlockTop = 8;                    // eval_top_k of the blocked path
 constexpr int kStatePitch = 2 + 2 * kMaxBlockTop;   // online heads state per row
-constexpr int kBlockSmem =
-    (kBT * kQP + kBT * 48 + kBR * kQP + kBR * kSP + kBR * kStatePitch) * 8;
+template <int BR, int TMAX>
+__host__ __device__ constexpr int block_smem() {
+  return (kBT * kQP + BR * kQP + BR * (TMAX + 1) + BR * kStatePitch) * 8;
+}
 
 struct BlockArgs {
   AttnArgs a;
   const double* hwp;  // heads packed (H, L*K): hwp[i][l*K + e] = head_w[l][i][e]
 };
 
+template <int BR, int TMAX>
 __global__ void __launch_bounds__(256, 1)
 attn_block_kernel(const BlockArgs ba) {
+  constexpr int RT = BR / 16;          // rows per thread in the register tiles
+  constexpr int kSP = TMAX + 1;        // pitch of S / Z rows
+  constexpr int NZ = TMAX / 32;        // scores per lane in the sparsemax
   const AttnArgs& a = ba.a;
   extern __shared__ double smem_d[];
   const int H = a.dm.H, K = a.dm.K, L = a.dm.L;
   const int H3 = 3 * H;
-  double* sK = smem_d;                  // kBT x kQP   keys (row-major)
-  double* sV = sK + kBT * kQP;          // kBT x H     values
-  double* sQ = sV + kBT * 48;           // kBR x kQP   queries, later residuals
-  double* sS = sQ + kBR * kQP;          // kBR x kSP   scores -> weights -> logits
+  double* sK = smem_d;                  // kBT x kQP   key / value chunk, head weights
+  double* sQ = sK + kBT * kQP;          // BR x kQP    queries, later residuals
+  double* sS = sQ + BR * kQP;           // BR x kSP    scores -> weights -> logits
   const int tid = threadIdx.x, lane = tid & 31, wib = tid >> 5;
   const int tx = tid & 15, ty = tid >> 4;
 
@@ -602,55 +606,53 @@ attn_block_kernel(const BlockArgs ba) {
     if (a.blk_off[mid] <= b) lo = mid; else hi = mid - 1;
   }
   const int base = a.seq_off[lo], T = a.seq_off[lo + 1] - base;
-  const int r0 = (b - a.blk_off[lo]) * kBR;
-  const int rows = min(T - r0, kBR);
+  const int r0 = (b - a.blk_off[lo]) * BR;
+  const int rows = min(T - r0, BR);
 
-  for (int i = tid; i < T * H; i += 256) {
-    const int j = i / H, c = i % H;
-    const double* src = a.qkv + (size_t)(base + j) * H3;
-    sK[j * kQP + c] = src[H + c];
-    sV[j * 48 + c] = src[2 * H + c];
-  }
   for (int i = tid; i < rows * H; i += 256) {
     const int r = i / H, c = i % H;
     sQ[r * kQP + c] = a.qkv[(size_t)(base + r0 + r) * H3 + c];
   }
-  __syncthreads();
-
-  // ---- S = Q K^T: rows ty*4 + {0..3}, columns tx + 16 m (m < 8)
-  {
-    double acc[4][8];
+  // ---- S = Q K^T over key chunks: rows ty*RT + i, columns kc + tx + 16 m (m < 8)
+  for (int kc = 0; kc < T; kc += kBT) {
+    const int nk = min(kBT, T - kc);
+    for (int i = tid; i < nk * H; i += 256) {
+      const int j = i / H, c = i % H;
+      sK[j * kQP + c] = a.qkv[(size_t)(base + kc + j) * H3 + H + c];
+    }
+    __syncthreads();
+    double acc[RT][8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RT; ++i)
 #pragma unroll
       for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
     for (int c = 0; c < H; ++c) {
-      double q[4], k[8];
+      double q[RT], k[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) q[i] = sQ[(ty * 4 + i) * kQP + c];
+      for (int i = 0; i < RT; ++i) q[i] = sQ[(ty * RT + i) * kQP + c];
 #pragma unroll
       for (int m = 0; m < 8; ++m) k[m] = sK[(tx + 16 * m) * kQP + c];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < RT; ++i)
 #pragma unroll
         for (int m = 0; m < 8; ++m) acc[i][m] = fma(q[i], k[m], acc[i][m]);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RT; ++i)
 #pragma unroll
-      for (int m = 0; m < 8; ++m) sS[(ty * 4 + i) * kSP + tx + 16 * m] = acc[i][m];
+      for (int m = 0; m < 8; ++m) sS[(ty * RT + i) * kSP + kc + tx + 16 * m] = acc[i][m];
+    __syncthreads();
   }
-  __syncthreads();
 
   // ---- sparsemax per row (warp per row): Michelot threshold, weights in place
   for (int r = wib; r < rows; r += 8) {
     double* srow = sS + r * kSP;
-    double z[4];
+    double z[NZ];
 #pragma unroll
-    for (int m = 0; m < 4; ++m) z[m] = (lane + 32 * m < T) ? srow[lane + 32 * m] : 0.0;
+    for (int m = 0; m < NZ; ++m) z[m] = (lane + 32 * m < T) ? srow[lane + 32 * m] : 0.0;
     double tsum = 0.0;
 #pragma unroll
-    for (int m = 0; m < 4; ++m)
+    for (int m = 0; m < NZ; ++m)
       if (lane + 32 * m < T) tsum += z[m];
     tsum = warp_sum(tsum);
     int cnt = T;
@@ -659,7 +661,7 @@ attn_block_kernel(const BlockArgs ba) {
       double ssum = 0.0;
       int cc = 0;
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < NZ; ++m)
         if (lane + 32 * m < T && z[m] > tau) {
           ssum += z[m];
           ++cc;
@@ -672,34 +674,44 @@ attn_block_kernel(const BlockArgs ba) {
       tau = (ssum - 1.0) / (double)cnt;
     }
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < NZ; ++m) {
       const int j = lane + 32 * m;
-      if (j < kBT) srow[j] = (j < T) ? fmax(z[m] - tau, 0.0) : 0.0;
+      if (j < TMAX) srow[j] = (j < T) ? fmax(z[m] - tau, 0.0) : 0.0;
     }
   }
   __syncthreads();
 
-  // ---- R = W V + h2: rows ty*4 + {0..3}, columns tx + 16 m (m < 3)
+  // ---- R = W V + h2 over value chunks: rows ty*RT + i, columns tx + 16 m (m < 3)
   {
-    double acc[4][3];
+    double acc[RT][3];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RT; ++i)
 #pragma unroll
       for (int m = 0; m < 3; ++m) acc[i][m] = 0.0;
-    for (int j = 0; j < T; ++j) {
-      double w[4], v[3];
+    double* sV = sK;  // kBT x 48
+    for (int kc = 0; kc < T; kc += kBT) {
+      const int nk = min(kBT, T - kc);
+      for (int i = tid; i < nk * H; i += 256) {
+        const int j = i / H, c = i % H;
+        sV[j * 48 + c] = a.qkv[(size_t)(base + kc + j) * H3 + 2 * H + c];
+      }
+      __syncthreads();
+      for (int j = 0; j < nk; ++j) {
+        double w[RT], v[3];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) w[i] = sS[(ty * 4 + i) * kSP + j];
+        for (int i = 0; i < RT; ++i) w[i] = sS[(ty * RT + i) * kSP + kc + j];
 #pragma unroll
-      for (int m = 0; m < 3; ++m) v[m] = (tx + 16 * m < H) ? sV[j * 48 + tx + 16 * m] : 0.0;
+        for (int m = 0; m < 3; ++m) v[m] = (tx + 16 * m < H) ? sV[j * 48 + tx + 16 * m] : 0.0;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < RT; ++i)
 #pragma unroll
-        for (int m = 0; m < 3; ++m) acc[i][m] = fma(w[i], v[m], acc[i][m]);
+          for (int m = 0; m < 3; ++m) acc[i][m] = fma(w[i], v[m], acc[i][m]);
+      }
+      __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = ty * 4 + i;
+    for (int i = 0; i < RT; ++i) {
+      const int r = ty * RT + i;
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
         const int c = tx + 16 * m;
@@ -715,7 +727,7 @@ attn_block_kernel(const BlockArgs ba) {
   const int LK = L * K;
   const int lpc = K <= kBT ? kBT / K : 1;             // layers per chunk
   const int cpl = K <= kBT ? 1 : (K + kBT - 1) / kBT;  // chunks per layer
-  double* st = sS + kBR * kSP;                         // kBR x kStatePitch online state
+  double* st = sS + BR * kSP;                          // BR x kStatePitch online state
   for (int l0 = 0; l0 < L; l0 += lpc) {
     const int nl = min(lpc, L - l0);
     for (int ch = 0; ch < cpl; ++ch) {
@@ -731,26 +743,26 @@ attn_block_kernel(const BlockArgs ba) {
           sW[i] = j < ncol ? __ldg(W + (size_t)c * LK + j) : 0.0;
         }
         __syncthreads();
-        double acc[4][8];
+        double acc[RT][8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < RT; ++i)
 #pragma unroll
           for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
         for (int c = 0; c < H; ++c) {
-          double rr[4], w[8];
+          double rr[RT], w[8];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) rr[i] = sQ[(ty * 4 + i) * kQP + c];
+          for (int i = 0; i < RT; ++i) rr[i] = sQ[(ty * RT + i) * kQP + c];
 #pragma unroll
           for (int m = 0; m < 8; ++m) w[m] = sW[c * kBT + tx + 16 * m];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < RT; ++i)
 #pragma unroll
             for (int m = 0; m < 8; ++m) acc[i][m] = fma(rr[i], w[m], acc[i][m]);
         }
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < RT; ++i)
 #pragma unroll
-          for (int m = 0; m < 8; ++m) sS[(ty * 4 + i) * kSP + tx + 16 * m] = acc[i][m];
+          for (int m = 0; m < 8; ++m) sS[(ty * RT + i) * kSP + tx + 16 * m] = acc[i][m];
       }
       __syncthreads();
       if (K <= 32) {
@@ -1023,13 +1035,13 @@ static int rows_gemm(const double* A, int n, int Kd, const double* B, int M, dou
 }
 
 // blk_off[i] = sum_{s < i} ceil(len_s / 32)   (attention CTA -> sequence map)
-__global__ void block_offsets_kernel(const int32_t* __restrict__ seq_off, int n_seq,
+__global__ void block_offsets_kernel(const int32_t* __restrict__ seq_off, int n_seq, int rpb,
                                      int32_t* __restrict__ blk_off) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int acc = 0;
   for (int i = 0; i < n_seq; ++i) {
     blk_off[i] = acc;
-    acc += (seq_off[i + 1] - seq_off[i] + kRowsPerBlk - 1) / kRowsPerBlk;
+    acc += (seq_off[i + 1] - seq_off[i] + rpb - 1) / rpb;
   }
   blk_off[n_seq] = acc;
 }
@@ -1082,7 +1094,11 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
                                  n_seq, H, h2, s)))
     return st;
   if ((st = rows_gemm(h2, n_tokens, H, tb.wqkv, 3 * H, qkv, s))) return st;
-  block_offsets_kernel<<<1, 32, 0, s>>>(seq_off, n_seq, blk_off);
+  // blocked path (register-tiled fp64 GEMM shapes, K/V streamed in chunks):
+  // 64 query rows per CTA up to T = 128, 32 up to T = 512
+  const bool blocked = topk <= kMaxBlockTop && H <= 48 && !getenv("SIDA_HASH_PROF");
+  const int rpb = blocked && max_len <= kBT ? 64 : blocked ? 32 : kRowsPerBlk;
+  block_offsets_kernel<<<1, 32, 0, s>>>(seq_off, n_seq, rpb, blk_off);
   SIDA_LAUNCH_CHECK();
 
   AttnArgs a;
@@ -1090,7 +1106,31 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
   a.n_seq = n_seq; a.n_tokens = n_tokens; a.dm = dm; a.hw = w.hw; a.hb = w.hb; a.topk = topk;
   a.ids = ids; a.alpha = alpha; a.alpha_f32 = alpha_f32;
   a.prof = nullptr;
-  const int n_blocks_ub = ceil_div(n_tokens, kRowsPerBlk) + n_seq;
+  const int n_blocks_ub = ceil_div(n_tokens, rpb) + n_seq;
+  if (blocked) {
+    BlockArgs ba{a, tb.hwp};
+    if (max_len <= kBT) {
+      constexpr int sm = block_smem<64, 128>();
+      static bool cfg64 = false;
+      if (!cfg64) {
+        SIDA_CUDA(cudaFuncSetAttribute(attn_block_kernel<64, 128>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        cfg64 = true;
+      }
+      attn_block_kernel<64, 128><<<n_blocks_ub, 256, sm, s>>>(ba);
+    } else {
+      constexpr int sm = block_smem<32, kMaxLen>();
+      static bool cfg32 = false;
+      if (!cfg32) {
+        SIDA_CUDA(cudaFuncSetAttribute(attn_block_kernel<32, kMaxLen>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        cfg32 = true;
+      }
+      attn_block_kernel<32, kMaxLen><<<n_blocks_ub, 256, sm, s>>>(ba);
+    }
+    SIDA_LAUNCH_CHECK();
+    return SIDA_OK;
+  }
   if (getenv("SIDA_HASH_PROF")) {
     static unsigned long long* buf = nullptr;
     static size_t cap = 0;
@@ -1105,27 +1145,20 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
     g_hash_prof = buf;
     g_hash_prof_n = need;
   }
-  a.ts = max_len <= 256 ? max_len : 0;
-  const size_t smem = ((size_t)2 * H * a.ts + (size_t)kRowsPerBlk * kResPitch +
-                       (size_t)kAttnWarps * kMaxLen) * sizeof(double);
+  // warp-per-row kernel (SIDA_HASH_PROF phase counters, eval_top_k > 8):
+  // stage K/V of the sequence in smem when they fit next to the residual and
+  // score buffers (227 KB per CTA), else read them from L2
+  auto heads_smem = [&](int ts) {
+    return ((size_t)2 * H * ts + (size_t)kRowsPerBlk * kResPitch +
+            (size_t)kAttnWarps * kMaxLen) * sizeof(double);
+  };
+  a.ts = heads_smem(max_len) <= 227 * 1024 ? max_len : 0;
+  const size_t smem = heads_smem(a.ts);
   static size_t configured = 0;
   if (smem > configured) {
     SIDA_CUDA(cudaFuncSetAttribute(attn_heads_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     configured = smem;
-  }
-  if (max_len <= kBT && topk <= kMaxBlockTop && H <= 48 && !a.prof) {
-    // blocked path: register-tiled fp64 GEMM shapes, one CTA per 64 rows
-    static bool cfg_block = false;
-    if (!cfg_block) {
-      SIDA_CUDA(cudaFuncSetAttribute(attn_block_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
-      cfg_block = true;
-    }
-    BlockArgs ba{a, tb.hwp};
-    attn_block_kernel<<<n_blocks_ub, 256, kBlockSmem, s>>>(ba);
-    SIDA_LAUNCH_CHECK();
-    return SIDA_OK;
   }
   const int blocks = n_blocks_ub;  // >= sum ceil(len/kRowsPerBlk)
   attn_heads_kernel<<<blocks, 32 * kAttnWarps, smem, s>>>(a);

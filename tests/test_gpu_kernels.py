@@ -275,7 +275,8 @@ def test_hash_with_callable_embed_fn(cuda_device):
 
 @pytest.mark.parametrize("L,K,T,B,k", [(12, 128, 128, 6, 1), (12, 8, 96, 4, 2), (2, 256, 512, 2, 3),
                                        (12, 256, 128, 4, 2), (3, 1000, 100, 3, 4),
-                                       (2, 200, 128, 3, 8), (2, 129, 64, 2, 1)])
+                                       (2, 200, 128, 3, 8), (2, 129, 64, 2, 1),
+                                       (3, 64, 256, 3, 2), (2, 8, 200, 2, 1)])
 def test_hash_ids_bit_exact_vs_oracle_switch_shapes(cuda_device, L, K, T, B, k):
     """Switch-base predictor heads (K = 8 / 128 / 256, 12 layers), up to T=512;
     K > 128 in the blocked kernel runs the online (max, sum, top-k) state over
