@@ -168,23 +168,38 @@ lstm_kernel(const double* __restrict__ xw, const double* __restrict__ tokx,
   double c_state = 0.0;
   for (int i = threadIdx.x; i < S * MAXH; i += blockDim.x) (&s_h[0][0])[i] = 0.0;
   __syncthreads();
-  // x_t Wx does not depend on h: its load for step t+1 is issued during step
-  // t so the (random-row) table / L2 latency leaves the recurrence's path
-  auto load_x = [&](int s, int t) -> double {
-    if (g >= G || t >= len[s]) return 0.0;
-    const int n = base[s] + t;
-    if (FOLD) return (tokx[(size_t)tokens[n] * G + g] + posx[(size_t)t * G + g]) + cg;
-    return xw[(size_t)n * G + g];
+  // x_t Wx does not depend on h, so it is fetched ahead of the recurrence:
+  // the token id two steps ahead, its table row (and the position row) one
+  // step ahead, and the parts are only added when the step consumes them --
+  // the dependent id -> row load chain stays off the critical path.
+  auto tok_at = [&](int s, int t) -> int {
+    return (FOLD && g < G && t < len[s]) ? __ldg(tokens + base[s] + t) : 0;
   };
-  double xnext[S];
+  auto load_parts = [&](int s, int t, int tok, double& pa, double& pb) {
+    pa = pb = 0.0;
+    if (g >= G || t >= len[s]) return;
+    if (FOLD) {
+      pa = __ldg(tokx + (size_t)tok * G + g);
+      pb = __ldg(posx + (size_t)t * G + g);
+    } else {
+      pa = __ldg(xw + (size_t)(base[s] + t) * G + g);
+    }
+  };
+  double xa[S], xb[S];
+  int tok1[S];
 #pragma unroll
-  for (int s = 0; s < S; ++s) xnext[s] = load_x(s, 0);
+  for (int s = 0; s < S; ++s) {
+    load_parts(s, 0, tok_at(s, 0), xa[s], xb[s]);
+    tok1[s] = tok_at(s, 1);
+  }
   for (int t = 0; t < tmax; ++t) {
     double xcur[S];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-      xcur[s] = xnext[s];
-      xnext[s] = load_x(s, t + 1);
+      xcur[s] = FOLD ? (xa[s] + xb[s]) + cg : xa[s];
+      const int tok2 = tok_at(s, t + 2);
+      load_parts(s, t + 1, tok1[s], xa[s], xb[s]);
+      tok1[s] = tok2;
     }
     if (g < G) {
 #pragma unroll
