@@ -113,6 +113,9 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  // let the output projection (launched with programmatic serialization)
+  // start its prologue while this grid drains
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     // ===== TMA producer: 12 (Q, K) k-blocks, then d/NC V chunks, one ring

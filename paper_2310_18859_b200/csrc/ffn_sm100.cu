@@ -199,6 +199,11 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   if constexpr (CG == 1) __syncthreads(); else cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
+  // programmatic dependent launch: everything above (barriers, TMEM, tile
+  // table) overlapped the previous kernel's tail; its outputs (A rows,
+  // residual) are read only after it has completed and flushed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   const int n_ntiles = p.ndim / BN;
   const int total = s_prefix[n_list] * n_ntiles;
@@ -506,6 +511,17 @@ static int make_map_3d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
   return SIDA_OK;
 }
 
+// Programmatic dependent launch of every grouped-GEMM launch (its prologue
+// overlaps the previous kernel's tail); SIDA_PDL=0 turns it off (A/B).
+static int pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SIDA_PDL");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 template <int BN, int STAGE, int CG>
 static int launch_gemm(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
                        int n_listed, cudaStream_t s) {
@@ -528,13 +544,15 @@ static int launch_gemm(const void* a_base, const void* b_base, int n_slots, cons
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem_bytes<BN, STAGE, CG>();
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return SIDA_OK;
 }
