@@ -104,11 +104,10 @@ __device__ __forceinline__ int expert_row(const GemmParams& p, int e) {
   return p.off ? p.off[e] : (e == 0 ? 0 : p.n_rows);
 }
 
-// Tile t -> (expert, first row of the TM-row tile, column tile).
-__device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int32_t* s_prefix,
-                                                const int32_t* s_expert, int n_list,
-                                                const GemmParams& p, int BN, int TM) {
-  const int mt = t / n_ntiles, nt = t - mt * n_ntiles;
+// m-tile mt, column tile nt -> (expert, first row of the TM-row tile, ...).
+__device__ __forceinline__ TileInfo decode_mt(int mt, int nt, const int32_t* s_prefix,
+                                              const int32_t* s_expert, int n_list,
+                                              const GemmParams& p, int BN, int TM) {
   int lo = 0, hi = n_list - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
@@ -124,10 +123,46 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int32
   return ti;
 }
 
+// Tile t -> (expert, first row of the TM-row tile, column tile).
+__device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int32_t* s_prefix,
+                                                const int32_t* s_expert, int n_list,
+                                                const GemmParams& p, int BN, int TM) {
+  const int mt = t / n_ntiles;
+  return decode_mt(mt, t - mt * n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
+}
+
+// Fused FFN tile order over MT m-tiles: step s issues the n1 GEMM1 tiles of
+// m-tile s, then the n2 GEMM2 tiles of m-tile s - lag, so every GEMM2 tile
+// comes after the GEMM1 tiles it reads (deadlock-free with in-order
+// persistent units) and the hidden rows in between (lag m-tiles) stay in L2.
+__device__ __forceinline__ void fused_order(int t, int MT, int n1, int n2, int lag, bool& g2,
+                                            int& mt, int& nt) {
+  const int a = min(lag, MT);
+  if (t < a * n1) {
+    g2 = false; mt = t / n1; nt = t - mt * n1;
+    return;
+  }
+  t -= a * n1;
+  const int nb = (MT - a) * (n1 + n2);
+  if (t < nb) {
+    const int s = t / (n1 + n2), r = t - s * (n1 + n2);
+    if (r < n1) { g2 = false; mt = a + s; nt = r; }
+    else { g2 = true; mt = a + s - lag; nt = r - n1; }
+    return;
+  }
+  t -= nb;
+  g2 = true; mt = MT - a + t / n2; nt = t - (t / n2) * n2;
+}
+
 template <int BN, int STAGE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmParams p) {
+                    const GemmParams p, const __grid_constant__ CUtensorMap tmA2,
+                    const __grid_constant__ CUtensorMap tmB2, const GemmParams p2,
+                    int32_t* __restrict__ mflags, int lag) {
+  // STAGE 1: GEMM1 (bias+ReLU -> hidden), 2: GEMM2 (alpha, unpermute,
+  // residual), 3: both in one persistent launch (p: GEMM1, p2: GEMM2; GEMM2
+  // tiles of an m-tile wait on mflags[mt] = CG * (h / BN) GEMM1 tile releases)
   constexpr int TM = BM * CG;                    // rows per tile (per CTA pair)
   constexpr int BNL = BN / CG;                   // B rows this CTA loads
   constexpr uint32_t kABytes = BM * BK * 2;
@@ -181,6 +216,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    if (STAGE == 3) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA2)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
+    }
   }
   if (warp == 1) {
     if constexpr (CG == 1) {
@@ -205,9 +244,38 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  const int n_ntiles = p.ndim / BN;
-  const int total = s_prefix[n_list] * n_ntiles;
-  const int n_kblocks = p.kdim / BK;
+  const int n_ntiles = p.ndim / BN;            // (STAGE 3: GEMM1 column tiles)
+  const int n2tiles = STAGE == 3 ? p2.ndim / BN : 0;
+  const int MT = s_prefix[n_list];
+  // STAGE 3 work items: per m-tile, n2tiles GEMM1 items of `sub` column tiles
+  // each (sub = n1 / n2: every item costs h/BK... = the same MMA work as one
+  // GEMM2 tile, so the static round-robin over items stays balanced) and
+  // n2tiles GEMM2 items of one tile
+  const int sub = STAGE == 3 ? n_ntiles / n2tiles : 1;
+  const int total = STAGE == 3 ? MT * 2 * n2tiles : MT * n_ntiles;
+  auto item_subs = [&](int it) -> int {
+    if constexpr (STAGE == 3) {
+      bool g2;
+      int mt, nt;
+      fused_order(it, MT, n2tiles, n2tiles, lag, g2, mt, nt);
+      return g2 ? 1 : sub;
+    }
+    return 1;
+  };
+  // (item, sub-tile) -> (GEMM2?, m-tile, tile info)
+  auto get_tile = [&](int it, int j, bool& g2, int& mt) -> TileInfo {
+    int nt;
+    if constexpr (STAGE == 3) {
+      fused_order(it, MT, n2tiles, n2tiles, lag, g2, mt, nt);
+      if (!g2) nt = nt * sub + j;
+    } else {
+      g2 = STAGE == 2;
+      mt = it / n_ntiles;
+      nt = it - mt * n_ntiles;
+    }
+    return decode_mt(mt, nt, s_prefix, s_expert, n_list, p, BN, TM);
+  };
+  const int flag_target = CG * n_ntiles;
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs): own 128 rows of A, own BN/CG rows of B
@@ -215,19 +283,37 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       int stage = 0;
       uint32_t phase = 0;
       unsigned long long w_empty = 0;
-      for (int t = unit; t < total; t += n_units) {
-        const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
+      for (int it = unit; it < total; it += n_units) {
+      const int nsub = item_subs(it);
+      for (int j = 0; j < nsub; ++j) {
+        bool g2;
+        int mt;
+        const TileInfo ti = get_tile(it, j, g2, mt);
         if (ti.slot < 0) continue;
-        for (int kb = 0; kb < n_kblocks; ++kb) {
+        if (STAGE == 3 && g2) {
+          // the hidden rows of this m-tile: every GEMM1 column tile released
+          int v;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(mflags + mt) : "memory");
+            if (v >= flag_target) break;
+            __nanosleep(64);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        const CUtensorMap* ta = (STAGE == 3 && g2) ? &tmA2 : &tmA;
+        const CUtensorMap* tb = (STAGE == 3 && g2) ? &tmB2 : &tmB;
+        const int nkb = ((STAGE == 3 && g2) ? p2.kdim : p.kdim) / BK;
+        for (int kb = 0; kb < nkb; ++kb) {
           const unsigned long long c0 = p.prof ? clk() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
           if (p.prof) w_empty += clk() - c0;
           const uint32_t fb = CG == 1 ? smem_u32(&full[stage]) : map_rank(smem_u32(&full[stage]), 0);
           if (leader) mbar_expect_tx(&full[stage], CG * (kABytes + kBBytes));
-          tma_load_2d<CG>(sA + stage * kABytes, &tmA, kb * BK, ti.row0 + rank * BM, fb);
-          tma_load_3d<CG>(sB + stage * kBBytes, &tmB, kb * BK, ti.ncol0 + rank * BNL, ti.slot, fb);
+          tma_load_2d<CG>(sA + stage * kABytes, ta, kb * BK, ti.row0 + rank * BM, fb);
+          tma_load_3d<CG>(sB + stage * kBBytes, tb, kb * BK, ti.ncol0 + rank * BNL, ti.slot, fb);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
+      }
       }
       if (p.prof) p.prof[blockIdx.x * kProfSlots + 0] = w_empty;
     }
@@ -241,12 +327,17 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       uint32_t acc_phase = 0;
       unsigned long long w_epi = 0, w_tma = 0, n_tiles = 0;
       const unsigned long long m0 = p.prof ? clk() : 0;
-      for (int t = unit; t < total; t += n_units) {
-        const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
+      for (int it = unit; it < total; it += n_units) {
+      const int nsub = item_subs(it);
+      for (int j = 0; j < nsub; ++j) {
+        bool g2;
+        int mt;
+        const TileInfo ti = get_tile(it, j, g2, mt);
         if (ti.slot < 0) {
           atomicExch(p.err_flag, 1);
           continue;
         }
+        const int n_kblocks = ((STAGE == 3 && g2) ? p2.kdim : p.kdim) / BK;
         ++n_tiles;
         const unsigned long long c0 = p.prof ? clk() : 0;
         if constexpr (CG == 1) mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -272,6 +363,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         tc_commit<CG>(&tmem_full[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      }
       if (p.prof) {
         unsigned long long* pr = p.prof + blockIdx.x * kProfSlots;
         pr[1] = w_epi;
@@ -296,24 +388,30 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
     uint32_t acc_phase = 0;
     unsigned long long w_full = 0;
     const unsigned long long e0 = p.prof ? clk() : 0;
-    for (int t = unit; t < total; t += n_units) {
-      const TileInfo ti = decode_tile(t, n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
+    for (int it = unit; it < total; it += n_units) {
+      const int nsub = item_subs(it);
+      for (int j = 0; j < nsub; ++j) {
+      bool g2;
+      int mt;
+      const TileInfo ti = get_tile(it, j, g2, mt);
       if (ti.slot < 0) continue;
+      const bool st2 = STAGE == 2 || (STAGE == 3 && g2);
+      const GemmParams& gp = (STAGE == 3 && g2) ? p2 : p;
       const int qrow0 = ti.row0 + rank * BM + quarter * 32;  // first row of this warp's quarter
       const int my_row = qrow0 + lane;
       const bool valid = my_row < ti.row_end;
       const uint16_t* bias = reinterpret_cast<const uint16_t*>(
-          p.arena + static_cast<size_t>(ti.slot) * p.slot_stride + p.bias_off);
+          gp.arena + static_cast<size_t>(ti.slot) * gp.slot_stride + gp.bias_off);
       float a_scale = 1.f;
       int orow = my_row;
       int brow[kMaxBf16K] = {};
-      if (STAGE == 2 && valid) {
-        if (p.alpha) a_scale = p.alpha[my_row];
-        if (p.row_map) orow = p.row_map[my_row];
-        if (p.bf16_map) {
+      if (st2 && valid) {
+        if (gp.alpha) a_scale = gp.alpha[my_row];
+        if (gp.row_map) orow = gp.row_map[my_row];
+        if (gp.bf16_map) {
 #pragma unroll
           for (int r = 0; r < kMaxBf16K; ++r)
-            if (r < p.bf16_k) brow[r] = p.bf16_map[static_cast<size_t>(orow) * p.bf16_k + r];
+            if (r < gp.bf16_k) brow[r] = gp.bf16_map[static_cast<size_t>(orow) * gp.bf16_k + r];
         }
       }
       const int cbase = ti.ncol0 + half * kHalfCols;
@@ -346,7 +444,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 __uint_as_float(vv[q * 8 + 2 * j + 1]) + __uint_as_float(w[j] & 0xFFFF0000u);
           }
         }
-        if (STAGE == 1) {
+        if (!st2) {
           // row-per-lane write: row r = lane, 4 x 16 B chunks, chunk' = q ^ ((r>>1)&3)
           const uint32_t srow = stile + lane * 64;
           const int sw = (lane >> 1) & 3;
@@ -366,7 +464,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             const int r = i * 8 + (lane >> 2), q = lane & 3;
             const uint4 val = lds128(stile + r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
             if (qrow0 + r < ti.row_end)
-              *reinterpret_cast<uint4*>(p.hidden + static_cast<size_t>(qrow0 + r) * p.ndim +
+              *reinterpret_cast<uint4*>(gp.hidden + static_cast<size_t>(qrow0 + r) * gp.ndim +
                                         col0 + q * 8) = val;
           }
           __syncwarp();
@@ -390,14 +488,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), q = lane & 7;
             const int orow_r = __shfl_sync(0xffffffffu, orow, r);
-            if (p.bf16_map) {
+            if (gp.bf16_map) {
 #pragma unroll
               for (int j = 0; j < kMaxBf16K; ++j)
                 brow8[i][j] = __shfl_sync(0xffffffffu, brow[j], r);
             }
-            at8[i] = static_cast<size_t>(orow_r) * p.ndim + col0 + q * 4;
-            x8[i] = (p.resid && qrow0 + r < ti.row_end)
-                        ? __ldg(reinterpret_cast<const float4*>(p.resid + at8[i]))
+            at8[i] = static_cast<size_t>(orow_r) * gp.ndim + col0 + q * 4;
+            x8[i] = (gp.resid && qrow0 + r < ti.row_end)
+                        ? __ldg(reinterpret_cast<const float4*>(gp.resid + at8[i]))
                         : make_float4(0.f, 0.f, 0.f, 0.f);
           }
 #pragma unroll
@@ -407,24 +505,24 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             if (qrow0 + r < ti.row_end) {
               float4 o = *reinterpret_cast<const float4*>(&raw);
               const size_t at = at8[i];
-              if (p.resid) {
+              if (gp.resid) {
                 const float4 x = x8[i];
                 o.x = x.x + o.x; o.y = x.y + o.y; o.z = x.z + o.z; o.w = x.w + o.w;
               }
-              if (p.out) *reinterpret_cast<float4*>(p.out + at) = o;
-              if (p.out_bf16) {
+              if (gp.out) *reinterpret_cast<float4*>(gp.out + at) = o;
+              if (gp.out_bf16) {
                 uint2 ob;
                 ob.x = bf16x2_rn(o.x, o.y);
                 ob.y = bf16x2_rn(o.z, o.w);
-                if (!p.bf16_map) {
-                  *reinterpret_cast<uint2*>(p.out_bf16 + at) = ob;
+                if (!gp.bf16_map) {
+                  *reinterpret_cast<uint2*>(gp.out_bf16 + at) = ob;
                 } else {  // expert-sorted copies: one per rank of this token
                   const size_t col = col0 + (lane & 7) * 4;
 #pragma unroll
                   for (int j = 0; j < kMaxBf16K; ++j)
-                    if (j < p.bf16_k)
+                    if (j < gp.bf16_k)
                       *reinterpret_cast<uint2*>(
-                          p.out_bf16 + static_cast<size_t>(brow8[i][j]) * p.ndim + col) = ob;
+                          gp.out_bf16 + static_cast<size_t>(brow8[i][j]) * gp.ndim + col) = ob;
                 }
               }
             }
@@ -440,7 +538,17 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         mbar_arrive_cluster(CG == 1 ? eb : map_rank(eb, 0));
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (STAGE == 3 && !st2) {
+        // this CTA's rows of hidden tile (mt, nt) are stored: release them to
+        // the GEMM2 producers (stores -> CTA barrier -> gpu fence -> count)
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        if (warp == 2 && lane == 0) {
+          __threadfence();
+          atomicAdd(mflags + mt, 1);
+        }
+      }
     }
+      }
     if (p.prof && warp == 2 && lane == 0) {
       p.prof[blockIdx.x * kProfSlots + 4] = w_full;
       p.prof[blockIdx.x * kProfSlots + 5] = clk() - e0;
@@ -524,7 +632,9 @@ static int pdl_enabled() {
 
 template <int BN, int STAGE, int CG>
 static int launch_gemm(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
-                       int n_listed, cudaStream_t s) {
+                       int n_listed, cudaStream_t s, const void* a2_base = nullptr,
+                       const void* b2_base = nullptr, const GemmParams* p2 = nullptr,
+                       int32_t* mflags = nullptr, int lag = 0) {
   auto kern = grouped_gemm_kernel<BN, STAGE, CG>;
   static bool configured = false;
   if (!configured) {
@@ -532,12 +642,22 @@ static int launch_gemm(const void* a_base, const void* b_base, int n_slots, cons
                                    (int)smem_bytes<BN, STAGE, CG>()));
     configured = true;
   }
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, ta2, tb2;
   int st = make_map_2d(&ta, a_base, p.kdim, p.n_rows, BM);
   if (st) return st;
   st = make_map_3d(&tb, b_base, p.kdim, p.ndim, n_slots, p.slot_stride, BN / CG);
   if (st) return st;
-  const int max_tiles = (ceil_div(p.n_rows, BM * CG) + n_listed) * (p.ndim / BN);
+  const GemmParams& q2 = p2 ? *p2 : p;
+  if (STAGE == 3) {
+    if ((st = make_map_2d(&ta2, a2_base, q2.kdim, q2.n_rows, BM))) return st;
+    if ((st = make_map_3d(&tb2, b2_base, q2.kdim, q2.ndim, n_slots, q2.slot_stride, BN / CG)))
+      return st;
+  } else {
+    ta2 = ta;
+    tb2 = tb;
+  }
+  const int col_tiles = p.ndim / BN + (STAGE == 3 ? q2.ndim / BN : 0);
+  const int max_tiles = (ceil_div(p.n_rows, BM * CG) + n_listed) * col_tiles;
   const int units = std::max(1, std::min(max_tiles, kNumSMs / CG));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(units * CG);
@@ -553,7 +673,7 @@ static int launch_gemm(const void* a_base, const void* b_base, int n_slots, cons
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p, ta2, tb2, q2, mflags, lag));
   return SIDA_OK;
 }
 
@@ -703,4 +823,56 @@ extern "C" int sida_out_proj_scatter(const uint16_t* ctx, int n_rows, int d, con
   p.err_flag = err_flag;
   const int cg = n_rows >= 1024 ? 2 : 1;
   return sm100::dispatch_gemm<2>(ctx, wo_t, 1, p, 1, cg, as_stream(stream));
+}
+
+// Both expert GEMMs of one layer in ONE persistent launch (STAGE 3): GEMM1
+// and GEMM2 tiles interleaved with a lag of `lag` m-tiles, GEMM2 tiles of an
+// m-tile gated on mflags[mt] (zeroed here) so the bf16 hidden rows are
+// consumed while still in L2 and the two launch tails become one.
+extern "C" size_t sida_ffn_flags_count(int n_rows, int n_listed) {
+  return static_cast<size_t>(ceil_div(n_rows, sm100::BM) + n_listed);
+}
+
+extern "C" int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, int d, int h,
+                                           const int32_t* off, int num_experts,
+                                           const int32_t* expert_slot, const int32_t* expert_list,
+                                           int n_list, const void* arena, size_t slot_stride,
+                                           int n_slots, const int32_t* row_map,
+                                           const float* alpha, const float* resid, float* out,
+                                           uint16_t* out_bf16, uint16_t* hidden,
+                                           int32_t* err_flag, int32_t* mflags, int lag,
+                                           void* stream) {
+  SIDA_REQUIRE(d % 256 == 0 && h % 256 == 0, SIDA_ERR_UNSUPPORTED,
+               "fused FFN needs d, h multiples of 256 (d=%d h=%d)", d, h);
+  SIDA_REQUIRE(n_rows >= 0 && num_experts >= 1 && n_slots >= 1 && lag >= 1, SIDA_ERR_CONTRACT,
+               "bad ffn dims rows=%d K=%d slots=%d lag=%d", n_rows, num_experts, n_slots, lag);
+  const int listed = expert_list ? n_list : num_experts;
+  SIDA_REQUIRE(listed <= sm100::kMaxListed, SIDA_ERR_UNSUPPORTED, "more than %d experts listed",
+               sm100::kMaxListed);
+  SIDA_REQUIRE(slot_stride % 16 == 0 && slot_stride >= sida_slot_bytes(d, h), SIDA_ERR_CONTRACT,
+               "slot stride %zu invalid", slot_stride);
+  SIDA_REQUIRE(err_flag && mflags && (out || out_bf16) && hidden && x_perm && off && expert_slot &&
+                   arena,
+               SIDA_ERR_CONTRACT, "null pointer passed to sida_grouped_ffn_bf16_fused");
+  if (n_rows == 0 || listed == 0) return SIDA_OK;
+  cudaStream_t s = as_stream(stream);
+  SIDA_CUDA(cudaMemsetAsync(mflags, 0, sida_ffn_flags_count(n_rows, listed) * sizeof(int32_t), s));
+  const uint8_t* ar = static_cast<const uint8_t*>(arena);
+  const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
+  sm100::GemmParams p1{};
+  p1.n_rows = n_rows; p1.kdim = d; p1.ndim = h;
+  p1.off = off; p1.num_experts = num_experts; p1.expert_slot = expert_slot;
+  p1.expert_list = expert_list; p1.n_list = n_list;
+  p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
+  p1.hidden = hidden; p1.err_flag = err_flag;
+  sm100::GemmParams p2 = p1;
+  p2.kdim = h; p2.ndim = d; p2.bias_off = b2_off;
+  p2.row_map = row_map; p2.alpha = alpha; p2.resid = resid; p2.out = out;
+  p2.out_bf16 = out_bf16;
+  const int cg = choose_cg(n_rows, listed);
+  if (cg == 2)
+    return sm100::launch_gemm<256, 3, 2>(x_perm, ar, n_slots, p1, listed, s, hidden, ar + w2_off,
+                                         &p2, mflags, lag);
+  return sm100::launch_gemm<256, 3, 1>(x_perm, ar, n_slots, p1, listed, s, hidden, ar + w2_off,
+                                       &p2, mflags, lag);
 }

@@ -35,6 +35,12 @@ from .errors import ContractError
 # A/B switch for measurements: SIDA_ATTN_CUBLAS=1 runs the attention core as
 # cuBLAS batched products + torch softmax instead of sida_attention_core.
 _ATTN_CUBLAS = bool(os.environ.get("SIDA_ATTN_CUBLAS"))
+# SIDA_FFN_FUSED=1: the two expert GEMMs as one interleaved persistent launch
+# (sida_grouped_ffn_bf16_fused) instead of two; measured slower (base-8 0.316
+# vs 0.293 ms, base-128 0.553 vs 0.461 ms), so off by default. SIDA_FFN_LAG:
+# GEMM2 lag in m-tiles.
+_FFN_FUSED = os.environ.get("SIDA_FFN_FUSED", "0") == "1"
+_FFN_LAG = int(os.environ.get("SIDA_FFN_LAG", "32"))
 # SIDA_OUTPROJ_CUBLAS=1: output projection as cuBLAS addmm (+ the FFN's row gather)
 _OUTPROJ_CUBLAS = bool(os.environ.get("SIDA_OUTPROJ_CUBLAS"))
 
@@ -484,12 +490,18 @@ class MoEModel:
             target = y if y is not None else torch.empty((rows, c.d_model), dtype=torch.float32,
                                                          device=self.device)
             resid = None
-        _lib.check(h.sida_grouped_ffn_bf16(
-            x_perm.data_ptr(), rows, c.d_model, c.expert_hidden, off.data_ptr(), c.num_experts,
-            slot_row.data_ptr(), _lib.ptr(expert_list), n_list, arena.base_ptr,
-            arena.slot_stride, arena.n_slots, perm.data_ptr(), alpha_perm.data_ptr(),
-            _lib.ptr(resid), target.data_ptr(), _lib.ptr(out_bf16 if k == 1 else None),
-            hidden.data_ptr(), err.data_ptr(), sh))
+        args = (x_perm.data_ptr(), rows, c.d_model, c.expert_hidden, off.data_ptr(),
+                c.num_experts, slot_row.data_ptr(), _lib.ptr(expert_list), n_list,
+                arena.base_ptr, arena.slot_stride, arena.n_slots, perm.data_ptr(),
+                alpha_perm.data_ptr(), _lib.ptr(resid), target.data_ptr(),
+                _lib.ptr(out_bf16 if k == 1 else None), hidden.data_ptr(), err.data_ptr())
+        if _FFN_FUSED and c.d_model % 256 == 0 and c.expert_hidden % 256 == 0:
+            listed = n_list if expert_list is not None else c.num_experts
+            flags = torch.empty(int(h.sida_ffn_flags_count(rows, listed)), dtype=torch.int32,
+                                device=self.device)
+            _lib.check(h.sida_grouped_ffn_bf16_fused(*args, flags.data_ptr(), _FFN_LAG, sh))
+        else:
+            _lib.check(h.sida_grouped_ffn_bf16(*args, sh))
         return target
 
     def combine(self, y: torch.Tensor, x: torch.Tensor, k: int, out: torch.Tensor | None = None,

@@ -392,3 +392,37 @@ def test_attention_core_contracts(cuda_device):
     with pytest.raises(NativeLibraryError):  # sequence longer than 128 tokens
         _lib.check(_lib.lib().sida_attention_core(qkv.data_ptr(), off.data_ptr(), 2, 300, 171,
                                                   128, ctx.data_ptr(), None))
+
+
+@pytest.mark.parametrize("d,hdim,K,N,k,lag", [
+    (256, 1024, 8, 1024, 1, 1), (768, 3072, 8, 9000, 1, 4), (256, 1024, 8, 700, 2, 32),
+    (256, 1024, 64, 3000, 1, 2), (768, 3072, 2, 4096, 1, 3)])
+def test_fused_ffn_launch_identical_to_two_launches(cuda_device, d, hdim, K, N, k, lag):
+    """sida_grouped_ffn_bf16_fused (GEMM1/GEMM2 tiles interleaved in one
+    persistent launch, GEMM2 gated on per-m-tile release counts) computes the
+    same tiles with the same epilogues: results bit-identical to the
+    two-launch entry point, for CTA pairs and single CTAs and any lag."""
+    from paper_2310_18859_b200 import moe as mmod
+    from paper_2310_18859_b200.offload import ExpertStore
+    from paper_2310_18859_b200.predictor import ExpertHashTable
+
+    shape, params, model = _moe_setup(d, hdim, K)
+    g = np.random.default_rng(d + N + K)
+    ids = _ids_for(N, k, K, g)
+    alphas = g.uniform(0.05, 1.0, size=ids.shape)
+    x = torch.from_numpy(g.normal(0, 1.0, (N, d))).float().cuda()
+    dt = ExpertHashTable(0, [N], ids, alphas).on_device(model)
+    store = ExpertStore.full(model)
+    outs = []
+    saved = (mmod._FFN_FUSED, mmod._FFN_LAG)
+    try:
+        for fused in (False, True):
+            mmod._FFN_FUSED, mmod._FFN_LAG = fused, lag
+            ob = torch.empty((N, d), dtype=torch.bfloat16, device="cuda")
+            outs.append((store.run_layer(model, 0, x, dt, out_bf16=ob), ob))
+            torch.cuda.synchronize()
+    finally:
+        mmod._FFN_FUSED, mmod._FFN_LAG = saved
+    assert torch.equal(outs[0][0], outs[1][0])
+    assert torch.equal(outs[0][1], outs[1][1])
+    assert store.err_flag.item() == 0
