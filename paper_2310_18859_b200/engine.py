@@ -39,25 +39,48 @@ def prepare_waves(plan, required, store: ExpertStore) -> list[list[Wave]]:
     an expert of its own layer (victim class 4, ref offload.py:14-16) is split
     into waves: each wave's FFN runs over the layer's experts resident at that
     point, before the eviction reuses their slots."""
-    out = []
-    for g in plan.groups:
-        layer = g.layer
-        need = sorted(required[layer])
-        waves, loads, done = [], [], set()
-        for op, key in g.steps:
-            if op == "evict":
-                if key[0] == layer and key[1] in required[layer]:
-                    exp = [e for e in need if (layer, e) in store.slot_of and e not in done]
-                    waves.append(Wave(layer, loads, exp, store.slot_row(layer, exp)))
-                    done.update(exp)
-                    loads = []
-                store.free_slot(key)
-            else:
-                loads.append((key, store.take_slot(key)))
-        exp = [e for e in need if e not in done]
-        waves.append(Wave(layer, loads, exp, store.slot_row(layer, exp)))
-        out.append(waves)
-    return out
+    return [prepare_group_waves(g, required, store) for g in plan.groups]
+
+
+def prepare_group_waves(g, required, store: ExpertStore) -> list[Wave]:
+    """Slot bookkeeping of one group (groups must be prepared in plan order)."""
+    layer = g.layer
+    need = sorted(required[layer])
+    waves, loads, done = [], [], set()
+    for op, key in g.steps:
+        if op == "evict":
+            if key[0] == layer and key[1] in required[layer]:
+                exp = [e for e in need if (layer, e) in store.slot_of and e not in done]
+                waves.append(Wave(layer, loads, exp, store.slot_row(layer, exp)))
+                done.update(exp)
+                loads = []
+            store.free_slot(key)
+        else:
+            loads.append((key, store.take_slot(key)))
+    exp = [e for e in need if e not in done]
+    waves.append(Wave(layer, loads, exp, store.slot_row(layer, exp)))
+    return waves
+
+
+def multi_wave(g, required) -> bool:
+    """A group that evicts an expert its own layer needs runs in waves."""
+    return any(k[0] == g.layer and k[1] in required[g.layer] for k in g.evictions)
+
+
+class _BatchPlan:
+    """Placement plan of one batch plus its issue state (groups issued, copy
+    done-events), so a batch can be planned and partly issued while the
+    previous one is still computing."""
+
+    def __init__(self, table, required, plan, waves):
+        self.table = table
+        self.required = required
+        self.plan = plan
+        self.waves = waves  # per group, prepared (slot bookkeeping) when issued
+        n = len(plan.groups)
+        self.issued = [False] * n
+        self.done: list = [None] * n
+        self.early = 0  # groups issued before this batch's forward started
 
 
 class SidaEngine:
@@ -90,6 +113,14 @@ class SidaEngine:
         self.peak = 0
         self.ffn_events: list | None = None  # set to a list to time every layer's FFN
         self.mix_events: list = []           # (filled alongside ffn_events) attention_mix
+        # hash-driven cross-batch prefetch: during the last `lookahead` layers
+        # of batch j, the (already hashed) batch j+1 is planned and its leading
+        # load groups are issued; forward(j+1) picks the plan up from here
+        self.lookahead = int(os.environ.get("SIDA_XBATCH_LOOKAHEAD", "0"))
+        # prefetch depth in layers: group g may be issued during layer l < g
+        # when none of its victims is read by layers l..g (reference: 1)
+        self.depth = int(os.environ.get("SIDA_PREFETCH_DEPTH", "1"))
+        self._pending: _BatchPlan | None = None
 
     # -- hash stream ------------------------------------------------------------------
     def hash_tokens(self, batch_id: int, tokens_dev: torch.Tensor, lengths) -> ExpertHashTable:
@@ -99,18 +130,19 @@ class SidaEngine:
 
     # -- compute stream ---------------------------------------------------------------
     def forward(self, table: ExpertHashTable, lengths, tokens_dev: torch.Tensor | None = None,
-                batch=None):
+                batch=None, next_table: ExpertHashTable | None = None):
         """Run one batch; returns (logits (n_seq, C) on the device, record dict,
-        (start_event, end_event) on the compute stream)."""
+        (start_event, end_event) on the compute stream). ``next_table`` (the
+        next batch's hash table, if already built) enables the cross-batch
+        prefetch of `_issue_ahead`."""
         model, store, state, budget = self.model, self.store, self.state, self.budget
         eb = model.expert_bytes_each()
         n_layers = model.config.num_layers
         cs = self.compute_stream
-        required = table.required_by_layer()
-        if len(required) < n_layers:
-            raise ContractError(f"missing hash entry for (layer {len(required)}, token 0)")
-        plan = plan_placement(table, state, budget, eb)
-        waves = prepare_waves(plan, required, store)
+        bp = self._pending if (self._pending is not None and self._pending.table is table) \
+            else self._plan_batch(table)
+        self._pending = None
+        required, plan, waves = bp.required, bp.plan, bp.waves
         dt = table.on_device(model, stream=self.hash_stream)
         if tokens_dev is None:
             tokens_dev = dt.tokens_for(model, batch)
@@ -119,20 +151,15 @@ class SidaEngine:
         cs.wait_event(dt.ready)
         dt.use_on(cs)
         ev0.record(cs)
-        done: list = [None] * n_layers
-        issued = [False] * n_layers
+        done, issued = bp.done, bp.issued
 
         def issue(idx: int):
-            apply_group_inplace(state, plan.groups[idx], budget.fast_tier_bytes, eb)
-            issued[idx] = True
-            self.peak = max(self.peak, state.used_bytes)
-            if len(waves[idx]) == 1:
-                done[idx] = store.enqueue_loads(waves[idx][0].loads)
+            self._issue(bp, idx)
 
         if self.prefetch == "batch":
             # every group whose victims are not read by this batch's earlier layers
             for idx, g in enumerate(plan.groups):
-                safe = len(waves[idx]) == 1 and all(
+                safe = not multi_wave(g, required) and all(
                     not (k[0] < idx and k[1] in required[k[0]]) for k in g.evictions)
                 if safe and all(issued[:idx]):
                     issue(idx)
@@ -146,6 +173,18 @@ class SidaEngine:
                 if (self.prefetch == "layer" and layer + 1 < n_layers
                         and plan.groups[layer + 1].prefetchable and not issued[layer + 1]):
                     issue(layer + 1)
+                if self.prefetch == "layer":
+                    for g_idx in range(layer + 2, min(n_layers, layer + 1 + self.depth)):
+                        if issued[g_idx]:
+                            continue
+                        g = plan.groups[g_idx]
+                        if (not all(issued[:g_idx]) or multi_wave(g, required)
+                                or any(layer <= k[0] <= g_idx for k in g.evictions)):
+                            break
+                        issue(g_idx)
+                if (next_table is not None and self._pending is None
+                        and layer >= n_layers - self.lookahead and all(issued)):
+                    self._issue_ahead(next_table, bp, layer)
                 if self.ffn_events is not None:
                     e_m = torch.cuda.Event(enable_timing=True)
                     e_m.record(cs)
@@ -183,6 +222,54 @@ class SidaEngine:
             "num_tokens": int(sum(lengths)),
             "transfer_s": plan.estimated_transfer_s,
             "expert_loads": len(plan.loads),
+            "groups_issued_ahead": bp.early,
             "utilization": util,
         }
         return logits, record, (ev0, ev1)
+
+    # -- planning / issue ---------------------------------------------------------------
+    def _plan_batch(self, table) -> _BatchPlan:
+        """ref pipeline.py:217-225: plan against the residency state left by
+        every group issued so far, and do the slot bookkeeping of all groups."""
+        n_layers = self.model.config.num_layers
+        required = table.required_by_layer()
+        if len(required) < n_layers:
+            raise ContractError(f"missing hash entry for (layer {len(required)}, token 0)")
+        plan = plan_placement(table, self.state, self.budget, self.model.expert_bytes_each())
+        return _BatchPlan(table, required, plan, [None] * len(plan.groups))
+
+    def _issue(self, bp: _BatchPlan, idx: int) -> None:
+        """ref pipeline.py:229-235 issue(): apply the group to the residency
+        state and enqueue its copies (single-wave groups; multi-wave groups
+        copy just in time inside run_waves)."""
+        g = bp.plan.groups[idx]
+        apply_group_inplace(self.state, g, self.budget.fast_tier_bytes,
+                            self.model.expert_bytes_each())
+        bp.waves[idx] = prepare_group_waves(g, bp.required, self.store)
+        bp.issued[idx] = True
+        self.peak = max(self.peak, self.state.used_bytes)
+        if len(bp.waves[idx]) == 1:
+            bp.done[idx] = self.store.enqueue_loads(bp.waves[idx][0].loads)
+
+    def _issue_ahead(self, next_table, bp: _BatchPlan, layer: int) -> None:
+        """Hash-driven cross-batch prefetch. Batch j+1's table is known while
+        batch j computes (SiDA builds tables one batch ahead), so once every
+        group of batch j is issued its plan can be made and its leading groups
+        issued now: a group goes early only if it is single-wave, prefetchable
+        (or the first), and evicts nothing batch j still reads in layers >=
+        `layer`. Copies into reused slots still wait on the slot's last
+        reader, so they overlap batch j's remaining layers."""
+        dtn = getattr(next_table, "_dev", None)
+        if dtn is not None and (dtn.hist is None or not dtn.ready.query()):
+            return  # not hashed yet: never block the compute loop on it
+        n_layers = self.model.config.num_layers
+        remaining = {(l, e) for l in range(layer, n_layers) for e in bp.required[l]}
+        nbp = self._plan_batch(next_table)
+        for idx, g in enumerate(nbp.plan.groups):
+            if multi_wave(g, nbp.required) or (idx > 0 and not g.prefetchable):
+                break
+            if any(k in remaining for k in g.evictions):
+                break
+            self._issue(nbp, idx)
+            nbp.early += 1
+        self._pending = nbp
