@@ -56,6 +56,9 @@ def parse():
                    help="CPU oracle sample size (sequences); ~1.3 s of CPU work each")
     p.add_argument("--parallel", default="dp", choices=["dp", "ep"],
                    help="N>1: data-parallel replicas (default) or expert parallel over NCCL")
+    p.add_argument("--ep-transport", default="nccl", choices=["nccl", "peer"],
+                   help="--parallel ep data exchange: NCCL all-to-all or the epilogue-fused "
+                        "peer-memory path (CUDA IPC / NVLink mappings)")
     p.add_argument("--no-streaming", action="store_true",
                    help="skip the H2D-link / budget-limited streaming measurement")
     return p.parse_args()
@@ -316,7 +319,11 @@ def run_ours(args):
     if ep_mode:
         from paper_2310_18859_b200.expert_parallel import ExpertParallelEngine
 
-        engine = ExpertParallelEngine(model, pred, budget)
+        from paper_2310_18859_b200.expert_parallel import PeerTransport
+
+        engine = ExpertParallelEngine(model, pred, budget,
+                                      transport=PeerTransport() if args.ep_transport == "peer"
+                                      else None)
         engine.compute_stream = engine.base.compute_stream
         engine.ffn_events, engine.mix_events = None, []
     else:
@@ -449,7 +456,8 @@ def run_ours(args):
                    "experts": cfg.num_experts, "d_model": cfg.d_model,
                    "expert_hidden": cfg.expert_hidden, "top_k": 1,
                    "hbm_budget_slots": slots,
-                   "parallelism": f"ep{ws}" if ep_mode else f"replicas{ws}",
+                   "parallelism": (f"ep{ws}-{args.ep_transport}" if ep_mode
+                                   else f"replicas{ws}"),
                    "l2_note": "per-step working set (activations 32768x768 fp32 + bf16 hidden "
                               "32768x3072 = 300 MB) exceeds the 126 MB L2"},
         "expert_memory": {"footprint_bytes": footprint, "slots": engine.store.peak_slots,

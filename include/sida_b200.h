@@ -195,6 +195,43 @@ int sida_unpermute_combine(const uint16_t* y_perm, const int32_t* inv, const flo
                            const float* resid, int n_tokens, int k, int d, float* out,
                            uint16_t* out_bf16, void* stream);
 
+/* Expert parallelism over peer memory: the dispatch and
+ * return all-to-alls folded into the epilogues that produce the rows.
+ * Destinations are encoded v = rank * peer_stride + row; peers (device array
+ * of world pointers) are the ranks' bf16 buffers, mapped with
+ * sida_ipc_open (NVLink peer mappings on a multi-GPU box).
+ *  - sida_out_proj_scatter_peer: as sida_out_proj_scatter, but the bf16 copy
+ *    of token t (rank r) goes to the owner's expert-major receive buffer at
+ *    map[t*k + r];
+ *  - sida_grouped_ffn_bf16_peer: the owner's grouped FFN over its received
+ *    rows (off/expert_slot over its num_experts local experts), each output
+ *    row (bf16, no alpha / residual) written back to the source rank's buffer
+ *    at row_map[j];
+ *  - sida_peer_signal / sida_peer_wait: stream-ordered release/acquire flags
+ *    (flags_q[me] = epoch on every peer q; wait for flags[0..world) >= epoch);
+ *  - sida_segment_map: out[i] = seg_val[b] + p - seg_start[b], p = index[i]
+ *    (or i), b the segment of p -- builds the destination maps on the device;
+ *  - sida_ipc_handle / sida_ipc_open / sida_ipc_close: CUDA IPC of the
+ *    allocation holding a device pointer (sida_ipc_handle_bytes() bytes per
+ *    handle, plus the pointer's offset inside the allocation). */
+int sida_out_proj_scatter_peer(const uint16_t* ctx, int n_rows, int d, const void* wo_t,
+                               const float* resid, float* out, const int32_t* map, int k,
+                               uint16_t* const* peers, int peer_stride, int32_t* err_flag,
+                               void* stream);
+int sida_grouped_ffn_bf16_peer(const uint16_t* x_loc, int n_rows, int d, int h, const int32_t* off,
+                               int num_experts, const int32_t* expert_slot, const void* arena,
+                               size_t slot_stride, int n_slots, const int32_t* row_map,
+                               uint16_t* const* peers, int peer_stride, uint16_t* hidden,
+                               int32_t* err_flag, void* stream);
+int sida_peer_signal(int32_t* const* peer_flags, int world, int me, int epoch, void* stream);
+int sida_peer_wait(const int32_t* flags, int world, int epoch, void* stream);
+int sida_segment_map(const int32_t* seg_start, const int32_t* seg_val, int n_seg,
+                     const int32_t* index, int n, int32_t* out, void* stream);
+size_t sida_ipc_handle_bytes(void);
+int sida_ipc_handle(const void* dev_ptr, void* handle_out, size_t* offset_out);
+int sida_ipc_open(const void* handle, size_t offset, void** base_out, void** ptr_out);
+int sida_ipc_close(void* base);
+
 /* k > 1 combine: out[t] = resid[t] + sum_{r=0..k-1} y[t*k + r] (ranks in
  * order, ref moe.py:252-262). */
 int sida_combine_ranks(const float* y, const float* resid, int n_tokens, int k, int d, float* out,

@@ -51,6 +51,17 @@ SIGNATURES = {
     "sida_out_proj_bytes": (_sz, [_i]),
     "sida_out_proj_scatter": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "sida_router_topk": (_i, [_vp, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "sida_out_proj_scatter_peer": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _vp,
+                                        _vp]),
+    "sida_grouped_ffn_bf16_peer": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _sz, _i, _vp, _vp,
+                                        _i, _vp, _vp, _vp]),
+    "sida_peer_signal": (_i, [_vp, _i, _i, _i, _vp]),
+    "sida_peer_wait": (_i, [_vp, _i, _i, _vp]),
+    "sida_segment_map": (_i, [_vp, _vp, _i, _vp, _i, _vp, _vp]),
+    "sida_ipc_handle_bytes": (_sz, []),
+    "sida_ipc_handle": (_i, [_vp, _vp, C.POINTER(C.c_size_t)]),
+    "sida_ipc_open": (_i, [_vp, _sz, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "sida_ipc_close": (_i, [_vp]),
     "sida_expert_copy": (_i, [_vp, _vp, _sz, _vp, _vp, _vp]),
     "sida_pack_expert_host": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp]),
     "sida_plan_placement": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp]),

@@ -83,6 +83,8 @@ struct GemmParams {
   uint16_t* out_bf16;          // GEMM2: optional bf16 copy of out (next layer's GEMM input)
   const int32_t* bf16_map;     // optional: out_bf16 row of (out row t, rank r) = map[t*k + r]
   int bf16_k;                  // ranks per out row in bf16_map (1..kMaxBf16K)
+  uint16_t* const* peer_bf16;  // optional: bf16 rows go to peer_bf16[v / peer_stride] row
+  int peer_stride;             //   v % peer_stride (expert-parallel dispatch / return)
   int32_t* err_flag;
   unsigned long long* prof;    // optional per-CTA cycle counters (sida_debug_gemm_prof)
 };
@@ -98,6 +100,16 @@ __device__ __forceinline__ unsigned long long clk() { return clock64(); }
 struct TileInfo {
   int expert, row0, row_end, ncol0, slot;
 };
+
+// Destination of bf16 output row v: local out_bf16, or a (peer rank, row)
+// pair encoded as rank * peer_stride + row into the peers' buffers.
+__device__ __forceinline__ uint16_t* bf16_row(const GemmParams& p, int v) {
+  if (p.peer_bf16) {
+    const int q = v / p.peer_stride;
+    return p.peer_bf16[q] + static_cast<size_t>(v - q * p.peer_stride) * p.ndim;
+  }
+  return p.out_bf16 + static_cast<size_t>(v) * p.ndim;
+}
 
 // First row of expert e (off == nullptr: one dense "expert" over all rows).
 __device__ __forceinline__ int expert_row(const GemmParams& p, int e) {
@@ -501,6 +513,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), q = lane & 7;
+            const int orow_r = gp.peer_bf16 ? __shfl_sync(0xffffffffu, orow, r) : 0;
             const uint4 raw = lds128(stile + r * 128 + ((q ^ (r & 7)) << 4));
             if (qrow0 + r < ti.row_end) {
               float4 o = *reinterpret_cast<const float4*>(&raw);
@@ -510,19 +523,22 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
                 o.x = x.x + o.x; o.y = x.y + o.y; o.z = x.z + o.z; o.w = x.w + o.w;
               }
               if (gp.out) *reinterpret_cast<float4*>(gp.out + at) = o;
-              if (gp.out_bf16) {
+              if (gp.out_bf16 || gp.peer_bf16) {
                 uint2 ob;
                 ob.x = bf16x2_rn(o.x, o.y);
                 ob.y = bf16x2_rn(o.z, o.w);
+                const int col = col0 + (lane & 7) * 4;
                 if (!gp.bf16_map) {
-                  *reinterpret_cast<uint2*>(gp.out_bf16 + at) = ob;
+                  if (!gp.peer_bf16)
+                    *reinterpret_cast<uint2*>(gp.out_bf16 + at) = ob;
+                  else
+                    *reinterpret_cast<uint2*>(
+                        bf16_row(gp, orow_r) + col) = ob;
                 } else {  // expert-sorted copies: one per rank of this token
-                  const size_t col = col0 + (lane & 7) * 4;
 #pragma unroll
                   for (int j = 0; j < kMaxBf16K; ++j)
                     if (j < gp.bf16_k)
-                      *reinterpret_cast<uint2*>(
-                          gp.out_bf16 + static_cast<size_t>(brow8[i][j]) * gp.ndim + col) = ob;
+                      *reinterpret_cast<uint2*>(bf16_row(gp, brow8[i][j]) + col) = ob;
                 }
               }
             }
@@ -875,4 +891,73 @@ extern "C" int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, i
                                          &p2, mflags, lag);
   return sm100::launch_gemm<256, 3, 1>(x_perm, ar, n_slots, p1, listed, s, hidden, ar + w2_off,
                                        &p2, mflags, lag);
+}
+
+// ---------------------------------------------------------------------------
+// Expert parallelism over peer memory: the two data
+// exchanges of an EP layer folded into the epilogues that produce the rows.
+//
+// Dispatch: the output projection writes each token's bf16 expert input
+// straight into the OWNER rank's expert-major receive buffer: map[t*k + r] =
+// owner * peer_stride + row, peers[q] = rank q's receive buffer (a peer /
+// IPC mapping; over NVLink on a multi-GPU box).
+extern "C" int sida_out_proj_scatter_peer(const uint16_t* ctx, int n_rows, int d,
+                                          const void* wo_t, const float* resid, float* out,
+                                          const int32_t* map, int k, uint16_t* const* peers,
+                                          int peer_stride, int32_t* err_flag, void* stream) {
+  SIDA_REQUIRE(d % 64 == 0, SIDA_ERR_UNSUPPORTED, "out projection needs d multiple of 64 (d=%d)",
+               d);
+  SIDA_REQUIRE(n_rows >= 0 && k >= 1 && k <= sm100::kMaxBf16K && peer_stride >= 1,
+               SIDA_ERR_CONTRACT, "bad out-projection dims rows=%d k=%d", n_rows, k);
+  SIDA_REQUIRE(ctx && wo_t && resid && out && err_flag && map && peers, SIDA_ERR_CONTRACT,
+               "null pointer passed to sida_out_proj_scatter_peer");
+  if (n_rows == 0) return SIDA_OK;
+  sm100::GemmParams p{};
+  p.n_rows = n_rows; p.kdim = d; p.ndim = d;
+  p.off = nullptr; p.num_experts = 1; p.expert_slot = nullptr;
+  p.arena = static_cast<const uint8_t*>(wo_t);
+  p.slot_stride = sida_out_proj_bytes(d);
+  p.bias_off = static_cast<size_t>(d) * d * 2;
+  p.resid = resid; p.out = out;
+  p.bf16_map = map; p.bf16_k = k;
+  p.peer_bf16 = peers; p.peer_stride = peer_stride;
+  p.err_flag = err_flag;
+  const int cg = n_rows >= 1024 ? 2 : 1;
+  return sm100::dispatch_gemm<2>(ctx, wo_t, 1, p, 1, cg, as_stream(stream));
+}
+
+// Return: the owner's grouped FFN writes each expert-output row (bf16, no
+// alpha / residual -- the source combines) straight back into the SOURCE
+// rank's buffer at its expert-sorted position: row_map[j] = src * peer_stride
+// + row, peers[g] = rank g's return buffer.
+extern "C" int sida_grouped_ffn_bf16_peer(const uint16_t* x_loc, int n_rows, int d, int h,
+                                          const int32_t* off, int num_experts,
+                                          const int32_t* expert_slot, const void* arena,
+                                          size_t slot_stride, int n_slots, const int32_t* row_map,
+                                          uint16_t* const* peers, int peer_stride,
+                                          uint16_t* hidden, int32_t* err_flag, void* stream) {
+  SIDA_REQUIRE(d % 64 == 0 && h % 64 == 0, SIDA_ERR_UNSUPPORTED,
+               "tcgen05 FFN needs d, h multiples of 64 (d=%d h=%d)", d, h);
+  SIDA_REQUIRE(n_rows >= 0 && num_experts >= 1 && num_experts <= sm100::kMaxListed &&
+                   n_slots >= 1 && peer_stride >= 1,
+               SIDA_ERR_CONTRACT, "bad ffn dims rows=%d K=%d slots=%d", n_rows, num_experts,
+               n_slots);
+  SIDA_REQUIRE(err_flag && hidden && x_loc && off && expert_slot && arena && row_map && peers,
+               SIDA_ERR_CONTRACT, "null pointer passed to sida_grouped_ffn_bf16_peer");
+  if (n_rows == 0) return SIDA_OK;
+  cudaStream_t s = as_stream(stream);
+  const uint8_t* ar = static_cast<const uint8_t*>(arena);
+  const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
+  const int cg = choose_cg(n_rows, num_experts);
+  sm100::GemmParams p1{};
+  p1.n_rows = n_rows; p1.kdim = d; p1.ndim = h;
+  p1.off = off; p1.num_experts = num_experts; p1.expert_slot = expert_slot;
+  p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
+  p1.hidden = hidden; p1.err_flag = err_flag;
+  int st = sm100::dispatch_gemm<1>(x_loc, ar, n_slots, p1, num_experts, cg, s);
+  if (st) return st;
+  sm100::GemmParams p2 = p1;
+  p2.kdim = h; p2.ndim = d; p2.bias_off = b2_off;
+  p2.row_map = row_map; p2.peer_bf16 = peers; p2.peer_stride = peer_stride;
+  return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, num_experts, cg, s);
 }

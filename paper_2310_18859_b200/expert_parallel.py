@@ -115,6 +115,130 @@ class GlooTransport(NcclTransport):
         return out.to(send.device)
 
 
+class PeerTransport(NcclTransport):
+    """No collective on the data path. Every rank maps
+    every other rank's expert-major receive buffers (two, by layer parity),
+    its return buffer and its flag words through CUDA IPC (NVLink peer
+    mappings on a multi-GPU box); the attention output projection writes each
+    token's expert input straight into the owner's receive buffer and the
+    owner's GEMM2 epilogue writes each expert output straight back into the
+    source's return buffer. Stream-ordered release/acquire flags
+    (sida_peer_signal / sida_peer_wait) separate producer and consumer. Only
+    the per-batch (L, K) histograms use torch.distributed (``control``)."""
+
+    peer = True
+
+    def __init__(self, control=None, group=None):
+        super().__init__(group)
+        self.control = control or NcclTransport(group)
+        self.ready = False
+        self._opened: list = []
+
+    def all_gather(self, t):
+        return self.control.all_gather(t)
+
+    def setup(self, model: MoEModel, rows_per_rank: int) -> None:
+        """Allocate and cross-map the buffers for up to ``rows_per_rank``
+        (token, rank) rows per source rank and batch."""
+        import ctypes as C
+
+        h = _lib.lib()
+        world, me = dist.get_world_size(self.group), dist.get_rank(self.group)
+        d, dev = model.config.d_model, model.device
+        self.world, self.me = world, me
+        self.cap_y = int(rows_per_rank)
+        self.cap_x = world * self.cap_y
+        self.xloc = [torch.empty((self.cap_x, d), dtype=torch.bfloat16, device=dev)
+                     for _ in range(2)]
+        self.yback = torch.empty((self.cap_y, d), dtype=torch.bfloat16, device=dev)
+        self.flags = torch.zeros(world, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)
+        nb = int(h.sida_ipc_handle_bytes())
+
+        def handle(t):
+            buf = C.create_string_buffer(nb)
+            off = C.c_size_t(0)
+            _lib.check(h.sida_ipc_handle(C.c_void_p(t.data_ptr()), buf, C.byref(off)))
+            return buf.raw, off.value
+
+        mine = [handle(t) for t in (self.xloc[0], self.xloc[1], self.yback, self.flags)]
+        allh: list = [None] * world
+        dist.all_gather_object(allh, mine, group=self.group)
+        ptrs = []
+        for q in range(world):
+            row = []
+            for i, t in enumerate((self.xloc[0], self.xloc[1], self.yback, self.flags)):
+                if q == me:
+                    row.append(t.data_ptr())
+                    continue
+                base, ptr = C.c_void_p(), C.c_void_p()
+                raw, off = allh[q][i]
+                _lib.check(h.sida_ipc_open(raw, off, C.byref(base), C.byref(ptr)))
+                self._opened.append(base.value)
+                row.append(ptr.value)
+            ptrs.append(row)
+        as_dev = lambda col: torch.tensor([ptrs[q][col] for q in range(world)],  # noqa: E731
+                                          dtype=torch.int64, device=dev)
+        self.xloc_peers = [as_dev(0), as_dev(1)]
+        self.yback_peers = as_dev(2)
+        self.flag_peers = as_dev(3)
+        self.epoch = 0
+        self.ready = True
+        dist.barrier(group=self.group)
+
+    def exchange_done(self, stream) -> None:
+        """Publish this rank's stores of the current exchange and wait for
+        every rank's (both stream-ordered, no host synchronisation)."""
+        h = _lib.lib()
+        self.epoch += 1
+        _lib.check(h.sida_peer_signal(self.flag_peers.data_ptr(), self.world, self.me, self.epoch,
+                                      stream.cuda_stream))
+        _lib.check(h.sida_peer_wait(self.flags.data_ptr(), self.world, self.epoch,
+                                    stream.cuda_stream))
+
+
+def ep_peer_maps(counts: np.ndarray, layer: int, rank: int, world: int, stride_x: int,
+                 stride_y: int):
+    """Host half of the peer exchange maps for one layer, from the (G, L, K)
+    histograms every rank holds after the per-batch all-gather:
+
+    dispatch: my expert-sorted row p of (global) expert e goes to owner
+      q = e // kl at row  loc_off_q[e - q kl] + sum_{g < me} c[g, e]  of its
+      receive buffer (expert-major, source-minor: ep_regroup's layout) ->
+      segments (start off_me[e], value q * stride_x + that row);
+    return: my received row in block (local expert el, source g) goes back to
+      g's expert-sorted position off_g[e] -> segments (block start, value
+      g * stride_y + off_g[e]);
+    plus this rank's local expert offsets (kl + 1) and received row count."""
+    kl = owner_block(counts.shape[2], world)
+    c = counts[:, layer, :].astype(np.int64)                        # (G, K)
+    K = c.shape[1]
+    off_src = np.zeros((world, K + 1), dtype=np.int64)              # each source's expert-sorted offsets
+    np.cumsum(c, axis=1, out=off_src[:, 1:])
+    tot = c.sum(axis=0)                                             # rows per expert, all sources
+    before = np.cumsum(c, axis=0) - c                               # sum_{g' < g} c[g', e]
+    d_start = off_src[rank].astype(np.int32)                        # (K + 1)
+    d_val = np.empty(K, dtype=np.int64)
+    for q in range(world):
+        blk = tot[q * kl:(q + 1) * kl]
+        loc = np.concatenate([[0], np.cumsum(blk)[:-1]])
+        d_val[q * kl:(q + 1) * kl] = q * stride_x + loc + before[rank, q * kl:(q + 1) * kl]
+    lo = rank * kl
+    off_l = np.zeros(kl + 1, dtype=np.int32)
+    np.cumsum(tot[lo:lo + kl], out=off_l[1:])
+    r_start = np.empty(kl * world + 1, dtype=np.int32)
+    r_val = np.empty(kl * world, dtype=np.int64)
+    for el in range(kl):
+        e = lo + el
+        for g in range(world):
+            b = el * world + g
+            r_start[b] = off_l[el] + before[g, e]
+            r_val[b] = g * stride_y + off_src[g, e]
+    r_start[-1] = off_l[-1]
+    return (d_start, d_val.astype(np.int32), r_start, r_val.astype(np.int32), off_l,
+            int(off_l[-1]))
+
+
 # ----------------------------------------------------------------------- engine
 class _LocalTable:
     """`required_by_layer` view restricted to this rank's experts (global ids)."""
@@ -183,6 +307,8 @@ class ExpertParallelEngine:
                 else:
                     ls.append((key, store.take_slot(key)))
             loads_by_layer.append(ls)
+        if getattr(self.transport, "peer", False):
+            return self._forward_peer(table, dt, counts, plan, loads_by_layer, lengths, tokens_dev)
         # per-layer regroup maps and local offsets, uploaded once per batch
         lo_e = self.rank * self.kl
         maps = [ep_regroup(counts, l, self.rank, self.world) for l in range(c.num_layers)]
@@ -240,6 +366,86 @@ class ExpertParallelEngine:
                     y_back.data_ptr(), dt.inv[layer].data_ptr(), alpha_perm.data_ptr(),
                     x.data_ptr(), x.shape[0], k, c.d_model, out.data_ptr(), xb.data_ptr(),
                     cs.cuda_stream))
+                x = out
+            logits = model.pool_classify(x, lay)
+        return logits
+
+    # ------------------------------------------------------------------ peer memory
+    def _forward_peer(self, table, dt, counts, plan, loads_by_layer, lengths, tokens_dev):
+        """The EP layer with both exchanges fused into the producing epilogues
+        (PeerTransport): out-projection → owners' receive buffers (by layer
+        parity) → flags → local grouped FFN whose GEMM2 epilogue writes into
+        the sources' return buffers → flags → unpermute-combine."""
+        model, store, budget, tp = self.model, self.store, self.budget, self.transport
+        c = model.config
+        h = _lib.lib()
+        eb = model.expert_bytes_each()
+        cs = self.base.compute_stream
+        k = dt.k
+        n_rows = int(sum(lengths)) * k
+        rows_max = int(counts.sum(axis=2).max())  # largest (token, rank) count of any source
+        if not tp.ready or rows_max > tp.cap_y:
+            tp.setup(model, max(rows_max, getattr(tp, "cap_y", 0)) * 2)
+        lo_e = self.rank * self.kl
+        dev = model.device
+
+        def h2d(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
+
+        with torch.cuda.stream(cs):
+            cs.wait_event(dt.ready)
+            dt.use_on(cs)
+            lay = BatchLayout(list(lengths), tokens_dev, dev)
+            x = model.embed_layout(lay)
+            xb = None
+            for layer in range(c.num_layers):
+                apply_group_inplace(self.state, plan.groups[layer], budget.fast_tier_bytes, eb)
+                self.peak = max(self.peak, self.state.used_bytes)
+                done = store.enqueue_loads(loads_by_layer[layer])
+                d_start, d_val, r_start, r_val, off_l, n_recv = ep_peer_maps(
+                    counts, layer, self.rank, self.world, tp.cap_x, tp.cap_y)
+                d_start_t, d_val_t = h2d(d_start), h2d(d_val)
+                dmap = torch.empty(n_rows, dtype=torch.int32, device=dev)
+                _lib.check(h.sida_segment_map(d_start_t.data_ptr(), d_val_t.data_ptr(), c.num_experts,
+                                              dt.inv[layer].data_ptr(), n_rows, dmap.data_ptr(),
+                                              cs.cuda_stream))
+                par = layer & 1
+                x_attn = model.attention_mix(layer, x, lay, xb=xb,
+                                             scatter=("peer", dmap, k, tp.xloc_peers[par],
+                                                      tp.cap_x))
+                tp.exchange_done(cs)  # every source's rows are in my receive buffer
+                if n_recv:
+                    r_start_t, r_val_t = h2d(r_start), h2d(r_val)
+                    rmap = torch.empty(n_recv, dtype=torch.int32, device=dev)
+                    _lib.check(h.sida_segment_map(r_start_t.data_ptr(), r_val_t.data_ptr(),
+                                                  self.kl * self.world, None, n_recv,
+                                                  rmap.data_ptr(), cs.cuda_stream))
+                    row = np.full(self.kl, -1, dtype=np.int32)
+                    for e in range(self.kl):
+                        key = (layer, lo_e + e)
+                        if key in store.slot_of:
+                            row[e] = store.slot_of[key]
+                    row_t, off_t = h2d(row), h2d(off_l)
+                    hidden = torch.empty((n_recv, c.expert_hidden), dtype=torch.bfloat16,
+                                         device=dev)
+                    if done is not None:
+                        cs.wait_event(done)
+                    _lib.check(h.sida_grouped_ffn_bf16_peer(
+                        tp.xloc[par].data_ptr(), n_recv, c.d_model, c.expert_hidden,
+                        off_t.data_ptr(), self.kl, row_t.data_ptr(), store.base_ptr,
+                        store.slot_stride, store.n_slots, rmap.data_ptr(), tp.yback_peers.data_ptr(),
+                        tp.cap_y, hidden.data_ptr(), store.err_flag.data_ptr(), cs.cuda_stream))
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    store.mark_read(row, ev)
+                tp.exchange_done(cs)  # every owner's outputs are in my return buffer
+                _, _, alpha_perm = dt.layer(layer)
+                out = torch.empty_like(x_attn)
+                xb = torch.empty(x_attn.shape, dtype=torch.bfloat16, device=dev)
+                _lib.check(h.sida_unpermute_combine(
+                    tp.yback.data_ptr(), dt.inv[layer].data_ptr(), alpha_perm.data_ptr(),
+                    x_attn.data_ptr(), x_attn.shape[0], k, c.d_model, out.data_ptr(),
+                    xb.data_ptr(), cs.cuda_stream))
                 x = out
             logits = model.pool_classify(x, lay)
         return logits

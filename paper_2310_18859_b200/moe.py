@@ -419,6 +419,14 @@ class MoEModel:
                 raise ContractError("fused expert-sorted scatter needs d % 64 == 0")
             return torch.addmm(x, ctx, self.wo[layer], out_dtype=torch.float32)
         out = torch.empty_like(x)
+        if scatter is not None and scatter[0] == "peer":
+            # expert parallel: rows go straight to the owners' receive buffers
+            _, dmap, k, peers, stride = scatter
+            _lib.check(_lib.lib().sida_out_proj_scatter_peer(
+                ctx.data_ptr(), ctx.shape[0], d, self.wo_t[layer].data_ptr(), x.data_ptr(),
+                out.data_ptr(), dmap.data_ptr(), k, peers.data_ptr(), stride,
+                self._err.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+            return out
         inv, k, x_perm = scatter if scatter is not None else (None, 0, None)
         _lib.check(_lib.lib().sida_out_proj_scatter(
             ctx.data_ptr(), ctx.shape[0], d, self.wo_t[layer].data_ptr(), x.data_ptr(),

@@ -100,3 +100,50 @@ def test_gloo_transport_world2():
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}
+
+
+def _seg_map(start, val, n_seg, index):
+    """Host mirror of sida_segment_map."""
+    out = np.empty(len(index), dtype=np.int64)
+    for i, p in enumerate(index):
+        b = int(np.searchsorted(start[:n_seg], p, side="right")) - 1
+        out[i] = val[b] + p - start[b]
+    return out
+
+
+@pytest.mark.parametrize("world,K,L", [(2, 8, 2), (4, 8, 3), (8, 64, 1), (1, 4, 2)])
+def test_peer_maps_round_trip(world, K, L):
+    """Dispatch then return (ep_peer_maps, as sida_segment_map applies them)
+    bring every source row back to its own expert-sorted position, and each
+    owner's receive buffer is expert-major / source-minor like ep_regroup."""
+    from paper_2310_18859_b200.expert_parallel import ep_peer_maps
+
+    g = np.random.default_rng(world + K + L)
+    counts = g.integers(0, 5, size=(world, L, K))
+    counts[-1, 0, :] = 0
+    sx, sy = 10_000, 1_000
+    kl = K // world
+    for layer in range(L):
+        maps = [ep_peer_maps(counts, layer, r, world, sx, sy) for r in range(world)]
+        filled = {}
+        for src in range(world):
+            d_start, d_val, *_ = maps[src]
+            n = int(counts[src, layer].sum())
+            dst = _seg_map(d_start, d_val, K, np.arange(n))
+            for p, v in enumerate(dst):
+                q, row = divmod(int(v), sx)
+                e = int(np.searchsorted(d_start, p, side="right")) - 1
+                assert q == e // kl
+                assert (q, row) not in filled
+                filled[(q, row)] = (src, p, e)
+        for q in range(world):
+            _, _, r_start, r_val, off_l, n_recv = maps[q]
+            assert sorted(r for (qq, r) in filled if qq == q) == list(range(n_recv))
+            back = _seg_map(r_start, r_val, kl * world, np.arange(n_recv))
+            keys = [filled[(q, j)] for j in range(n_recv)]
+            # expert-major, source-minor, each source's rows in its own order
+            assert keys == sorted(keys, key=lambda t: (t[2], t[0], t[1]))
+            for j, v in enumerate(back):
+                src, pos = divmod(int(v), sy)
+                assert (src, pos) == keys[j][:2]
+            assert off_l[-1] == n_recv

@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, peer=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     try:
         torch.cuda.set_device(0)
@@ -34,7 +34,8 @@ def _worker(rank, world, port, q):
         from paper_2310_18859_b200 import MemoryBudget, MoEConfig, MoEModel, PredictorConfig
         from paper_2310_18859_b200 import PredictorNet
         from paper_2310_18859_b200.engine import SidaEngine
-        from paper_2310_18859_b200.expert_parallel import ExpertParallelEngine, GlooTransport
+        from paper_2310_18859_b200.expert_parallel import (ExpertParallelEngine, GlooTransport,
+                                                           PeerTransport)
 
         shape = omoe.MoEShape(vocab_size=512, d_model=256, num_layers=2, num_experts=8,
                               expert_hidden=1024, max_seq_len=128)
@@ -48,9 +49,11 @@ def _worker(rank, world, port, q):
         lengths = [T] * B
         toks = torch.randint(0, 512, (B * T,), generator=g, device="cuda", dtype=torch.int32)
 
-        ep = ExpertParallelEngine(model, net, MemoryBudget(8 * eb), transport=GlooTransport())
-        table = ep.hash_tokens(0, toks, lengths)
-        got = ep.forward(table, lengths, tokens_dev=toks)
+        transport = PeerTransport(control=GlooTransport()) if peer else GlooTransport()
+        ep = ExpertParallelEngine(model, net, MemoryBudget(8 * eb), transport=transport)
+        for bid in range(2 if peer else 1):  # peer: a second batch reuses the mapped buffers
+            table = ep.hash_tokens(bid, toks, lengths)
+            got = ep.forward(table, lengths, tokens_dev=toks)
         torch.cuda.synchronize()
         single = SidaEngine(model, net, MemoryBudget(16 * eb))
         t2 = single.hash_tokens(0, toks, lengths)
@@ -69,11 +72,14 @@ def _worker(rank, world, port, q):
             dist.destroy_process_group()
 
 
-def test_expert_parallel_two_ranks_one_gpu(cuda_device):
+@pytest.mark.parametrize("peer", [False, True])
+def test_expert_parallel_two_ranks_one_gpu(cuda_device, peer):
+    """peer=False: NCCL-style all-to-all (gloo here); peer=True: the exchanges
+    fused into the epilogues over CUDA-IPC-mapped buffers (PeerTransport)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, peer)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
