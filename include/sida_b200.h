@@ -162,7 +162,7 @@ int sida_debug_gemm_prof(unsigned long long* out);
  * ctx = softmax(q k^T / sqrt(d)) v per sequence, single head, non-causal, on
  * tcgen05 (scores and P.V in TMEM, softmax in registers). qkv bf16
  * (n_tokens, 3d) = [q | k | v]; seq_off int32 (n_seq + 1) device offsets;
- * every sequence <= 128 tokens (max_len), d % 128 == 0; ctx bf16 (n_tokens, d). */
+ * every sequence <= 256 tokens (max_len), d % 128 == 0; ctx bf16 (n_tokens, d). */
 int sida_attention_core(const uint16_t* qkv, const int32_t* seq_off, int n_seq, int n_tokens,
                         int max_len, int d, uint16_t* ctx, void* stream);
 

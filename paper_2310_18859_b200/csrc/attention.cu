@@ -1,10 +1,13 @@
 // Fused mixing-attention core on the 5th-gen tensor cores (sm_100a):
 //   ctx = softmax(q k^T / sqrt(d)) v        per sequence, single head, non-causal
-// for sequences of at most 128 tokens (ref moe.py:220-233; the projections
+// for sequences of at most 256 tokens (ref moe.py:220-233; the projections
 // q,k,v = x W and the output projection run as GEMMs around this kernel).
 //
-// One CTA per sequence, two CTAs per SM (~105 KB smem, 256 TMEM columns
-// each), so a 256-sequence batch is resident in a single wave. Inside a CTA:
+// Up to 128 tokens: one CTA per sequence, two CTAs per SM (~105 KB smem, 256
+// TMEM columns each), so a 256-sequence batch is resident in a single wave.
+// Up to 256 tokens: one CTA per (sequence, 128-query block) over all the
+// sequence's keys (S is 128 x 256 in TMEM, P 64 KB), one CTA per SM. Inside
+// a CTA (shown for 128 keys):
 //
 //   phase 1  S = Q K^T (M=128 queries, N=128 keys, K=d) with tcgen05.mma,
 //            Q and K k-blocks streamed by TMA through a 2-slot ring,
@@ -37,17 +40,30 @@ namespace attn {
 using namespace sm100;
 
 constexpr int BM = 128;        // queries per CTA (one TMEM lane each)
-constexpr int NKEY = 128;      // keys per CTA (max sequence length here)
 constexpr int BK = 64;         // d per phase-1 k-block (one SW128 row)
 constexpr int NC = 128;        // d columns per phase-3 chunk
-constexpr int kSlot = 32 * 1024;        // Q+K k-block (16+16 KB) or V chunk (2 x 16 KB)
 constexpr int kSlots = 2;
-constexpr int kPBytes = BM * NKEY * 2;  // P: 2 K-atoms x 128 rows x 128 B
 constexpr int kStageTile = 32 * 32 * 2; // per-warp bf16 epilogue staging tile
 constexpr int kEpiWarps = 4;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr uint32_t kTmemCols = 256;
-constexpr size_t kSmem = 1024 + kSlots * kSlot + kPBytes + kEpiWarps * kStageTile + 256;
+
+// Per key-count variant (NKEY = keys per CTA = the longest sequence served):
+//   128: ring slot 32 KB (Q 16 + K 16 KB, or a V chunk 2 x 16 KB), P 32 KB,
+//        TMEM 256 columns (S [0,128), C chunks {[128,256), [0,128)}), 2 CTAs/SM
+//   256: ring slot 64 KB (Q 16 + K 32 KB, or a V chunk 2 x 32 KB), P 64 KB,
+//        TMEM 512 columns (S [0,256), C chunks {[256,384), [384,512)}), 1 CTA/SM
+template <int NKEY>
+struct Cfg {
+  static constexpr int kSlot = NKEY * 256;              // = max(QK, V) stage bytes
+  static constexpr int kQKBytes = BM * 128 + NKEY * 128;
+  static constexpr int kVBytes = NKEY * 256;
+  static constexpr int kPBytes = BM * NKEY * 2;         // NKEY/64 K-atoms x 128 rows x 128 B
+  static constexpr uint32_t kTmemCols = NKEY == 128 ? 256 : 512;
+  static constexpr uint32_t kC0 = NKEY == 128 ? 128 : 256;  // C chunk buffers (TMEM columns)
+  static constexpr uint32_t kC1 = NKEY == 128 ? 0 : 384;
+  static constexpr int kMinBlocks = NKEY == 128 ? 2 : 1;
+  static constexpr size_t kSmem = 1024 + kSlots * kSlot + kPBytes + kEpiWarps * kStageTile + 256;
+};
 
 // SWIZZLE_128B MN-major operand: 64-element MN groups `lbo` bytes apart, 8-row
 // K groups 1024 B apart.
@@ -64,9 +80,14 @@ __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
+template <int NKEY>
+__global__ void __launch_bounds__(kThreads, Cfg<NKEY>::kMinBlocks)
 attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ seq_off,
                  int d, float scale_log2e, uint16_t* __restrict__ ctx) {
+  using C = Cfg<NKEY>;
+  constexpr int kSlot = C::kSlot;
+  constexpr int kPBytes = C::kPBytes;
+  constexpr uint32_t kTmemCols = C::kTmemCols;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* ring = smem;
@@ -83,8 +104,10 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int seq = blockIdx.x;
-  const int row0 = seq_off[seq];
+  const int row0 = seq_off[seq];              // first key / token of the sequence
   const int T = seq_off[seq + 1] - row0;
+  const int q0 = blockIdx.y * BM;             // first query row of this CTA (in the sequence)
+  if (q0 >= T) return;                        // (uniform: before any barrier / TMEM use)
   const int n_kb = d / BK, n_chunks = d / NC;
 
   if (threadIdx.x == 0) {
@@ -125,16 +148,24 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
       const int n_loads = n_kb + n_chunks;
       for (int i = 0; i < n_loads; ++i) {
         mbar_wait(&empty[slot], phase ^ 1);
-        mbar_expect_tx(&full[slot], kSlot);
         uint8_t* dst = ring + slot * kSlot;
         const uint32_t fb = smem_u32(&full[slot]);
         if (i < n_kb) {
-          tma_load_2d<1>(dst, &tm_qkv, i * BK, row0, fb);                  // Q rows
-          tma_load_2d<1>(dst + kSlot / 2, &tm_qkv, d + i * BK, row0, fb);  // K rows
+          mbar_expect_tx(&full[slot], C::kQKBytes);
+          tma_load_2d<1>(dst, &tm_qkv, i * BK, row0 + q0, fb);              // Q rows
+#pragma unroll
+          for (int kh = 0; kh < NKEY / 128; ++kh)                           // K rows
+            tma_load_2d<1>(dst + BM * 128 + kh * 128 * 128, &tm_qkv, d + i * BK,
+                           row0 + kh * 128, fb);
         } else {
+          mbar_expect_tx(&full[slot], C::kVBytes);
           const int c0 = 2 * d + (i - n_kb) * NC;
-          tma_load_2d<1>(dst, &tm_qkv, c0, row0, fb);                      // V[:, c0:c0+64]
-          tma_load_2d<1>(dst + kSlot / 2, &tm_qkv, c0 + 64, row0, fb);     // V[:, +64:+128]
+#pragma unroll
+          for (int gcol = 0; gcol < 2; ++gcol)                              // V[:, c0 + 64 g ..]
+#pragma unroll
+            for (int kh = 0; kh < NKEY / 128; ++kh)
+              tma_load_2d<1>(dst + gcol * (NKEY * 128) + kh * 128 * 128, &tm_qkv,
+                             c0 + gcol * 64, row0 + kh * 128, fb);
         }
         if (++slot == kSlots) { slot = 0; phase ^= 1; }
       }
@@ -150,7 +181,7 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
         mbar_wait(&full[slot], phase);
         tc_fence_after();
         const uint32_t a0 = smem_u32(ring + slot * kSlot);
-        const uint32_t b0 = a0 + kSlot / 2;
+        const uint32_t b0 = a0 + BM * 128;
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
           umma_bf16<1>(tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc_s,
@@ -159,7 +190,7 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
         if (++slot == kSlots) { slot = 0; phase ^= 1; }
       }
       tc_commit<1>(s_full);
-      mbar_wait(p_full, 0);  // P in smem (and S fully read: TMEM cols [0,128) free)
+      mbar_wait(p_full, 0);  // P in smem (and S fully read: its TMEM columns free)
       tc_fence_after();
       const uint32_t p0 = smem_u32(sP);
       for (int j = 0; j < n_chunks; ++j) {
@@ -167,12 +198,12 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
         if (j >= 2) mbar_wait(&c_empty[b], ((j >> 1) - 1) & 1);
         mbar_wait(&full[slot], phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + (b == 0 ? 128u : 0u);
+        const uint32_t d_tmem = tmem + (b == 0 ? C::kC0 : C::kC1);
         const uint32_t v0 = smem_u32(ring + slot * kSlot);
 #pragma unroll
         for (int k = 0; k < NKEY / 16; ++k)  // 16 keys per MMA: P atom k/4, V rows 16k..
           umma_bf16<1>(d_tmem, sw128_desc(p0 + (k >> 2) * (BM * 128) + (k & 3) * 32),
-                       sw128_mn_desc(v0 + k * 16 * 128, kSlot / 2), idesc_c, k != 0);
+                       sw128_mn_desc(v0 + k * 16 * 128, NKEY * 128), idesc_c, k != 0);
         tc_commit<1>(&empty[slot]);
         tc_commit<1>(&c_full[b]);
         if (++slot == kSlots) { slot = 0; phase ^= 1; }
@@ -228,12 +259,12 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
 
     // epilogue: chunk j of C -> bf16 ctx rows, through a swizzled 32x32 tile
     const uint32_t stile = smem_u32(sOut + (warp - 2) * kStageTile);
-    const int q_row0 = row0 + quarter * 32;  // first global row of this warp
+    const int q_row0 = row0 + q0 + quarter * 32;  // first global row of this warp
     for (int j = 0; j < n_chunks; ++j) {
       const int b = j & 1;
       mbar_wait(&c_full[b], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t t_c = t_lane + (b == 0 ? 128u : 0u);
+      const uint32_t t_c = t_lane + (b == 0 ? C::kC0 : C::kC1);
 #pragma unroll
       for (int c = 0; c < NC / 32; ++c) {
         tmem_ld32_nowait(t_c + c * 32, v);
@@ -258,7 +289,7 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
         for (int i = 0; i < 4; ++i) {
           const int rr = i * 8 + (lane >> 2), q = lane & 3;
           const uint4 val = lds128(stile + rr * 64 + ((q ^ ((rr >> 1) & 3)) << 4));
-          if (quarter * 32 + rr < T)
+          if (q0 + quarter * 32 + rr < T)
             *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(q_row0 + rr) * d + j * NC +
                                       c * 32 + q * 8) = val;
         }
@@ -299,15 +330,14 @@ using namespace sida;
 
 // qkv: bf16 (n_tokens, 3d) = [q | k | v] per token (x @ [Wq|Wk|Wv]);
 // seq_off: int32 (n_seq + 1) exclusive offsets on the concatenated token axis;
-// every sequence at most 128 tokens; ctx: bf16 (n_tokens, d).
+// every sequence at most 256 tokens; ctx: bf16 (n_tokens, d).
 extern "C" int sida_attention_core(const uint16_t* qkv, const int32_t* seq_off, int n_seq,
                                    int n_tokens, int max_len, int d, uint16_t* ctx,
                                    void* stream) {
   SIDA_REQUIRE(d % attn::NC == 0 && d >= attn::NC, SIDA_ERR_UNSUPPORTED,
                "fused attention needs d multiple of %d (d=%d)", attn::NC, d);
-  SIDA_REQUIRE(max_len >= 1 && max_len <= attn::NKEY, SIDA_ERR_UNSUPPORTED,
-               "fused attention handles sequences of at most %d tokens (got %d)", attn::NKEY,
-               max_len);
+  SIDA_REQUIRE(max_len >= 1 && max_len <= 256, SIDA_ERR_UNSUPPORTED,
+               "fused attention handles sequences of at most 256 tokens (got %d)", max_len);
   SIDA_REQUIRE(n_seq >= 0 && n_tokens >= 0, SIDA_ERR_CONTRACT, "bad attention dims");
   SIDA_REQUIRE(qkv && seq_off && ctx, SIDA_ERR_CONTRACT,
                "null pointer passed to sida_attention_core");
@@ -323,16 +353,29 @@ extern "C" int sida_attention_core(const uint16_t* qkv, const int32_t* seq_off, 
                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   SIDA_REQUIRE(r == CUDA_SUCCESS, SIDA_ERR_CUDA, "tensor map encode failed: %d", (int)r);
-  static bool configured = false;
-  if (!configured) {
-    SIDA_CUDA(cudaFuncSetAttribute(attn::attn_core_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)attn::kSmem));
-    configured = true;
-  }
   const float scale_log2e = 1.4426950408889634f / sqrtf(static_cast<float>(d));
-  attn::attn_core_kernel<<<n_seq, attn::kThreads, attn::kSmem, as_stream(stream)>>>(
-      tm, seq_off, d, scale_log2e, ctx);
+  cudaStream_t s = as_stream(stream);
+  if (max_len <= 128) {
+    static bool cfg128 = false;
+    if (!cfg128) {
+      SIDA_CUDA(cudaFuncSetAttribute(attn::attn_core_kernel<128>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)attn::Cfg<128>::kSmem));
+      cfg128 = true;
+    }
+    attn::attn_core_kernel<128><<<dim3(n_seq, 1), attn::kThreads, attn::Cfg<128>::kSmem, s>>>(
+        tm, seq_off, d, scale_log2e, ctx);
+  } else {
+    static bool cfg256 = false;
+    if (!cfg256) {
+      SIDA_CUDA(cudaFuncSetAttribute(attn::attn_core_kernel<256>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)attn::Cfg<256>::kSmem));
+      cfg256 = true;
+    }
+    attn::attn_core_kernel<256><<<dim3(n_seq, ceil_div(max_len, attn::BM)), attn::kThreads,
+                                  attn::Cfg<256>::kSmem, s>>>(tm, seq_off, d, scale_log2e, ctx);
+  }
   SIDA_LAUNCH_CHECK();
   return SIDA_OK;
 }

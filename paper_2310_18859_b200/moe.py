@@ -375,7 +375,7 @@ class MoEModel:
                       xb: torch.Tensor | None = None, scatter=None) -> torch.Tensor:
         """x + softmax(q k^T / sqrt(d)) v W_o per sequence (ref moe.py:220-233).
 
-        The QKV projection is a cuBLAS bf16 GEMM. For sequences of at most 128
+        The QKV projection is a cuBLAS bf16 GEMM. For sequences of at most 256
         tokens (d % 128 == 0) the score / softmax / context core is the fused
         tcgen05 kernel sida_attention_core; longer sequences use cuBLAS batched
         products (scores with fp32 outputs) and torch softmax. The output projection is the
@@ -389,7 +389,7 @@ class MoEModel:
         if xb is None:
             xb = x.to(torch.bfloat16)
         qkv = xb @ self.wqkv[layer]
-        if d % 128 == 0 and lay.max_len <= 128 and not _ATTN_CUBLAS:
+        if d % 128 == 0 and lay.max_len <= 256 and not _ATTN_CUBLAS:
             # fused tcgen05 core: scores, softmax and P.V without HBM round trips
             ctx = torch.empty((lay.n_tokens, d), dtype=torch.bfloat16, device=x.device)
             _lib.check(_lib.lib().sida_attention_core(

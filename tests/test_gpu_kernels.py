@@ -352,7 +352,9 @@ def test_out_proj_scatter_vs_torch_fp32(cuda_device, n, d, k):
 
 # ------------------------------------------------------------- fused attention core
 @pytest.mark.parametrize("lengths,d", [([128] * 3, 768), ([1, 5, 77, 128, 64, 128], 256),
-                                       ([100] * 7 + [3], 128), ([128] * 300, 768)])
+                                       ([100] * 7 + [3], 128), ([128] * 300, 768),
+                                       ([256] * 4, 768), ([129, 3, 256, 200, 1], 256),
+                                       ([256] * 150, 768)])
 def test_attention_core_vs_torch_fp32(cuda_device, lengths, d):
     """ctx = softmax(q k^T / sqrt(d)) v per sequence (ref moe.py:220-233 core)
     against an fp32 torch reference on the same bf16 q, k, v, at the bf16 bar
@@ -387,10 +389,10 @@ def test_attention_core_contracts(cuda_device):
     from paper_2310_18859_b200.errors import NativeLibraryError
 
     qkv = torch.zeros((300, 3 * 128), dtype=torch.bfloat16, device="cuda")
-    off = torch.tensor([0, 129, 300], dtype=torch.int32, device="cuda")
+    off = torch.tensor([0, 43, 300], dtype=torch.int32, device="cuda")
     ctx = torch.empty((300, 128), dtype=torch.bfloat16, device="cuda")
-    with pytest.raises(NativeLibraryError):  # sequence longer than 128 tokens
-        _lib.check(_lib.lib().sida_attention_core(qkv.data_ptr(), off.data_ptr(), 2, 300, 171,
+    with pytest.raises(NativeLibraryError):  # sequence longer than 256 tokens
+        _lib.check(_lib.lib().sida_attention_core(qkv.data_ptr(), off.data_ptr(), 2, 300, 257,
                                                   128, ctx.data_ptr(), None))
 
 
