@@ -142,10 +142,13 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic tokens, random-init Switch-base-8-shaped weights",
-        "config": {"workload": "Switch-base-8 SiDA serving (BASELINE configs[1])",
-                   "batch": 1, "seq_len": args.seq, "layers": cfg["num_layers"],
-                   "experts": cfg["num_experts"], "d_model": cfg["d_model"],
-                   "expert_hidden": cfg["expert_hidden"], "top_k": 1},
+        "config": {"workload": "Switch-base-8 SiDA serving, 12 layers, bf16, 1 B200 (BASELINE "
+                               "configs[1])", "global_batch": args.batch * max(ws, 1),
+                   "seq_len": args.seq, "tokens_per_step_per_gpu": args.batch * args.seq,
+                   "layers": cfg["num_layers"], "experts": cfg["num_experts"],
+                   "d_model": cfg["d_model"], "expert_hidden": cfg["expert_hidden"],
+                   "top_k": 1, "parallelism": "cpu (reference algorithm, numpy f64)",
+                   "sample_per_step": f"1 sequence of {args.seq} tokens (see cpu_baseline)"},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(),
                          "blas_threads": blas_threads(), "kind": "port", "sample": detail},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
