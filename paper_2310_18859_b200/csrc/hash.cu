@@ -233,6 +233,94 @@ lstm_kernel(const double* __restrict__ xw, const double* __restrict__ tokx,
   }
 }
 
+// Gate / cell nonlinearity without divergence: sigmoid (ref numkit.py:104-110,
+// stable split) or tanh from one expm1 and one division,
+//   m = expm1(-a|x|), a = 1 (sigmoid) or 2 (tanh):
+//   sigmoid(x >= 0) = 1 / (2 + m), sigmoid(x < 0) = (1 + m) / (2 + m),
+//   tanh(x) = sign(x) * (-m) / (2 + m)            (expm1 keeps tanh accurate near 0)
+__device__ __forceinline__ double act_d(double x, bool is_tanh) {
+  const double ax = fabs(x);
+  const double m = expm1(is_tanh ? -2.0 * ax : -ax);
+  const double num = is_tanh ? -m : (x >= 0.0 ? 1.0 : 1.0 + m);
+  const double r = num / (2.0 + m);
+  return (is_tanh && x < 0.0) ? -r : r;
+}
+
+// LSTM recurrence, one sequence per CTA, quad mapping: thread t owns gate
+// q = t % 4 (i, f, g, o) of unit j = t / 4, i.e. column q*H + j of Wh (in
+// registers) and Wx. The four gates of a unit sit in one lane quad, so the
+// cell update c = f c + i g, h = o tanh(c) needs two shuffles and no shared
+// memory; one barrier per step publishes h. (ref predictor.py:174-196)
+template <int H, bool FOLD>
+__global__ void __launch_bounds__(4 * H)
+lstm_quad_kernel(const double* __restrict__ xw, const double* __restrict__ tokx,
+                 const double* __restrict__ posx, const double* __restrict__ cx,
+                 const int32_t* __restrict__ tokens, const double* __restrict__ wh,
+                 const double* __restrict__ b, const int32_t* __restrict__ seq_off, int n_seq,
+                 double* __restrict__ h_out) {
+  constexpr int G = 4 * H;
+  __shared__ double s_h[2][H];
+  const int t = threadIdx.x;
+  const int j = t >> 2, q = t & 3;
+  const int col = q * H + j;
+  const bool is_tanh = q == 2;
+  const int seq = blockIdx.x;
+  const int base = seq_off[seq];
+  const int len = seq_off[seq + 1] - base;
+  double wcol[H];
+#pragma unroll
+  for (int i = 0; i < H; ++i) wcol[i] = wh[(size_t)i * G + col];
+  const double bg = b[col];
+  const double cg = FOLD ? cx[col] : 0.0;
+  for (int i = t; i < H; i += blockDim.x) s_h[0][i] = 0.0;
+  double c_state = 0.0;
+  // x_t fetched ahead: token ids two steps, table rows one step (see lstm_kernel)
+  auto tok_at = [&](int tt) -> int { return (FOLD && tt < len) ? __ldg(tokens + base + tt) : 0; };
+  double xa = 0.0, xb = 0.0;
+  auto load_parts = [&](int tt, int tok) {
+    xa = xb = 0.0;
+    if (tt >= len) return;
+    if (FOLD) {
+      xa = __ldg(tokx + (size_t)tok * G + col);
+      xb = __ldg(posx + (size_t)tt * G + col);
+    } else {
+      xa = __ldg(xw + (size_t)(base + tt) * G + col);
+    }
+  };
+  load_parts(0, tok_at(0));
+  int tok1 = tok_at(1);
+  __syncthreads();
+  for (int tt = 0; tt < len; ++tt) {
+    const double* hp = s_h[tt & 1];
+    const double x = FOLD ? (xa + xb) + cg : xa;
+    const int tok2 = tok_at(tt + 2);
+    load_parts(tt + 1, tok1);
+    tok1 = tok2;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+    for (int i = 0; i < H; i += 4) {
+      a0 = fma(hp[i], wcol[i], a0);
+      if (i + 1 < H) a1 = fma(hp[i + 1], wcol[i + 1], a1);
+      if (i + 2 < H) a2 = fma(hp[i + 2], wcol[i + 2], a2);
+      if (i + 3 < H) a3 = fma(hp[i + 3], wcol[i + 3], a3);
+    }
+    const double pre = (x + ((a0 + a1) + (a2 + a3))) + bg;
+    const double gv = act_d(pre, is_tanh);
+    // gather the unit's i, f, g, o inside the quad (every lane gets all four)
+    const double gi = __shfl_sync(0xffffffffu, gv, 0, 4);
+    const double gf = __shfl_sync(0xffffffffu, gv, 1, 4);
+    const double gg = __shfl_sync(0xffffffffu, gv, 2, 4);
+    const double go = __shfl_sync(0xffffffffu, gv, 3, 4);
+    c_state = gf * c_state + gi * gg;
+    const double hv = go * act_d(c_state, true);
+    if (q == 0) {
+      s_h[(tt + 1) & 1][j] = hv;
+      h_out[(size_t)(base + tt) * H + j] = hv;
+    }
+    __syncthreads();
+  }
+}
+
 // C (N x M) = A (N x Kd) @ B (Kd x M), fp64. Block = 64 rows; A and B in smem;
 // 256 threads as a 16 x 16 grid, each 4 rows x (M/16) columns.
 constexpr int kRG_Rows = 64;
@@ -1016,6 +1104,9 @@ static int launch_lstm(const double* xw, const double* tokx, const double* posx,
   else if (S == 2)
     lstm_kernel<MAXH, 2, FOLD><<<ceil_div(n_seq, 2), 4 * MAXH, 0, s>>>(
         xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out);
+  else if (H == MAXH && !getenv("SIDA_LSTM_SPLIT"))
+    lstm_quad_kernel<MAXH, FOLD><<<n_seq, 4 * MAXH, 0, s>>>(xw, tokx, posx, cx, tokens, wh, b,
+                                                           seq_off, n_seq, h_out);
   else
     lstm_kernel<MAXH, 1, FOLD><<<n_seq, 4 * MAXH, 0, s>>>(xw, tokx, posx, cx, tokens, wh, b,
                                                           seq_off, n_seq, H, h_out);
