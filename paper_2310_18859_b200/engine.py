@@ -15,9 +15,7 @@ hash stream one batch ahead.
 from __future__ import annotations
 
 import os
-import time
 
-import numpy as np
 import torch
 
 from .errors import ContractError, UnservableError

@@ -4,12 +4,9 @@ the same logits as the oracle on the bf16 weights, and save_moe writes back
 exactly the bf16 values (byte-identical to the container of the rounded
 parameters)."""
 
-import os
-
 import numpy as np
 import pytest
 
-from conftest import GOLDEN
 from oracle import moe as omoe
 from oracle import numkit as onk
 from oracle import predictor as opred

@@ -6,7 +6,6 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import load_golden
 from test_gpu_kernels import _hash_fixture, close_rms
 
 pytestmark = pytest.mark.gpu
