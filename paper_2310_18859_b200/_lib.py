@@ -94,7 +94,10 @@ def load(path: str = LIB_PATH) -> C.CDLL:
 
 
 def lib(device: int | None = None) -> C.CDLL:
-    """The loaded library, after checking the CUDA device is sm_100."""
+    """The loaded library, after checking the CUDA device is sm_100 (once per
+    device; later calls return at once -- this sits on the per-launch path)."""
+    if _handle is not None and _device_checked and device is None:
+        return _handle
     h = load()
     import torch
 

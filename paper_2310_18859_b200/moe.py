@@ -275,10 +275,16 @@ class MoEModel:
                 _lib.check(h.sida_pack_expert_host(*(a.ctypes.data for a in arrs), c.d_model,
                                                    c.expert_hidden, dst.data_ptr()))
 
+    def _stream_handle(self) -> int:
+        """Raw handle of the current stream of this model's device."""
+        return torch.cuda.current_stream(self._dev_index).cuda_stream
+
     def _prepare_out_proj(self):
         """Per layer W_o^T (K-major) + a zero bias row: the B operand of the
         fused output projection (sida_out_proj_scatter); tcgen05 shapes only."""
         d = self.config.d_model
+        self._dev_index = self.device.index if self.device.index is not None else \
+            torch.cuda.current_device()
         self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.wo_t = None
         if d % 64 or _OUTPROJ_CUBLAS:
@@ -394,7 +400,7 @@ class MoEModel:
             ctx = torch.empty((lay.n_tokens, d), dtype=torch.bfloat16, device=x.device)
             _lib.check(_lib.lib().sida_attention_core(
                 qkv.data_ptr(), lay.seq_off.data_ptr(), lay.n_seq, lay.n_tokens, lay.max_len, d,
-                ctx.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+                ctx.data_ptr(), self._stream_handle()))
             return self._out_proj(layer, x, ctx, scatter)
         if lay.uniform:
             qkv = qkv.view(lay.n_seq, lay.max_len, 3 * d)
@@ -425,13 +431,13 @@ class MoEModel:
             _lib.check(_lib.lib().sida_out_proj_scatter_peer(
                 ctx.data_ptr(), ctx.shape[0], d, self.wo_t[layer].data_ptr(), x.data_ptr(),
                 out.data_ptr(), dmap.data_ptr(), k, peers.data_ptr(), stride,
-                self._err.data_ptr(), torch.cuda.current_stream(self.device).cuda_stream))
+                self._err.data_ptr(), self._stream_handle()))
             return out
         inv, k, x_perm = scatter if scatter is not None else (None, 0, None)
         _lib.check(_lib.lib().sida_out_proj_scatter(
             ctx.data_ptr(), ctx.shape[0], d, self.wo_t[layer].data_ptr(), x.data_ptr(),
             out.data_ptr(), _lib.ptr(inv), k, _lib.ptr(x_perm), self._err.data_ptr(),
-            torch.cuda.current_stream(self.device).cuda_stream))
+            self._stream_handle()))
         return out
 
     def pool_classify(self, x: torch.Tensor, lay: BatchLayout) -> torch.Tensor:

@@ -111,18 +111,20 @@ def plan_placement(table, state: ResidencyState, budget: MemoryBudget,
     if expert_bytes > budget.fast_tier_bytes:
         raise UnservableError(
             f"expert of {expert_bytes} bytes exceeds budget {budget.fast_tier_bytes}")
-    required = [set(int(e) for e in s) for s in table.required_by_layer()]
+    required = table.required_by_layer()
     n_layers = len(required)
-    keys = list(state.fifo_order)
-    if any(state.resident.get(k) != expert_bytes for k in keys) or len(keys) != len(state.resident):
+    keys = state.fifo_order
+    sizes = set(state.resident.values())
+    if (sizes and sizes != {expert_bytes}) or len(keys) != len(state.resident):
         raise ContractError("residency state holds experts of another size")
-    max_e = max([e for s in required for e in s] + [k[1] for k in keys] + [0])
+    kv = np.array(keys, dtype=np.int64).reshape(-1, 2)
+    max_e = max([max(s) for s in required if s] + [int(kv[:, 1].max()) if len(kv) else 0, 0])
     K = max_e + 1
     req = np.zeros((max(n_layers, 1), K), dtype=np.uint8)
     for layer, s in enumerate(required):
         if s:
-            req[layer, sorted(s)] = 1
-    fifo = np.array([l * K + e for l, e in keys], dtype=np.int32)
+            req[layer, np.fromiter(s, dtype=np.int64, count=len(s))] = 1
+    fifo = (kv[:, 0] * K + kv[:, 1]).astype(np.int32)
     cap = 2 * n_layers * K + len(keys) + 1
     steps = np.empty(cap, dtype=np.int32)
     goff = np.empty(n_layers + 1, dtype=np.int32)
@@ -232,6 +234,34 @@ class Wave:
     slot_row: np.ndarray
 
 
+class RowUploader:
+    """Small int32 rows (expert -> slot maps, expert lists) to the device
+    through a pinned ring, without a pinned allocation per call: slot i's host
+    row is rewritten only after the copy that last used it has completed."""
+
+    def __init__(self, device, width: int, slots: int = 64):
+        self.host = torch.empty((slots, max(width, 1)), dtype=torch.int32).pin_memory()
+        self.host_np = self.host.numpy()
+        self.dev = torch.empty((slots, max(width, 1)), dtype=torch.int32, device=device)
+        self.events: list = [None] * slots
+        self.i = 0
+
+    def upload(self, arr: np.ndarray, stream) -> torch.Tensor:
+        i = self.i
+        self.i = (i + 1) % len(self.events)
+        ev = self.events[i]
+        if ev is not None and not ev.query():
+            ev.synchronize()
+        n = len(arr)
+        self.host_np[i, :n] = arr
+        with torch.cuda.stream(stream):
+            self.dev[i, :n].copy_(self.host[i, :n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+        self.events[i] = ev
+        return self.dev[i, :n]
+
+
 class ExpertStore:
     """HBM slot arena + pinned expert images + copy stream.
 
@@ -258,6 +288,7 @@ class ExpertStore:
         self.n_loads = 0
         self.bytes_loaded = 0
         self.peak_slots = 0
+        self.rows = RowUploader(dev, model.config.num_experts)
 
     @classmethod
     def full(cls, model) -> "ExpertStore":
@@ -364,12 +395,11 @@ def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=N
             stream.wait_event(done)
         if not wave.experts:
             continue
+        row = store.rows.upload(wave.slot_row, stream)
+        elist = None
+        if multi:
+            elist = store.rows.upload(np.asarray(wave.experts, dtype=np.int32), stream)
         with torch.cuda.stream(stream):
-            row = torch.from_numpy(wave.slot_row).pin_memory().to(x.device, non_blocking=True)
-            elist = None
-            if multi:
-                elist = torch.from_numpy(np.asarray(wave.experts, dtype=np.int32)).pin_memory().to(
-                    x.device, non_blocking=True)
             model.moe_apply_rows(tables, x, k, store, row, expert_list=elist, out=out, y=y,
                                  stream=stream, out_bf16=out_bf16, x_perm=x_perm)
         ev = torch.cuda.Event()
