@@ -40,7 +40,6 @@ wt = torch.randint(0, cfg.vocab_size, (sum(wl),), device="cuda", dtype=torch.int
 for i in range(2):
     eng.forward(eng.hash_tokens(i, wt, wl), wl, tokens_dev=wt)
 torch.cuda.synchronize()
-assert eng.store.n_slots >= len(eng.store.slot_of) == cfg.num_layers * cfg.num_experts
 rows = []
 for T in [int(v) for v in a.seqs.split(",")]:
     for B in [int(v) for v in a.batches.split(",")]:
