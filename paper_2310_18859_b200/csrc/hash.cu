@@ -897,69 +897,97 @@ attn_block_kernel(const BlockArgs ba) {
         __syncthreads();
         continue;
       }
-      // warp per (row, layer of the chunk): lanes over the chunk's experts
-      for (int pr = wib; pr < rows * nl; pr += 8) {
-        const int r = pr / nl, l = l0 + pr % nl;
-        const int cw = K <= kBT ? K : ncol;                  // experts in this slice
-        const double* zr = sS + r * kSP + (l - l0) * (K <= kBT ? K : 0);
-        const double* hb = a.hb + (size_t)l * K + c0;
-        double z[4];
-        double zmax = -INFINITY;
+      if (K <= kBT) {
+        // 32 < K <= 128: eight lanes per (row, layer), 16 logits per lane, four
+        // pairs per warp in flight (a warp per pair left the fp64 exp /
+        // shuffle chains latency-bound at 8 warps per SM)
+        const int grp = lane >> 3, gl = lane & 7;
+        const int npairs = rows * nl;
+        for (int pb = wib * 4; pb < npairs; pb += 32) {
+          const int pr = pb + grp;
+          const bool valid = pr < npairs;
+          const int r = valid ? pr / nl : 0, l = l0 + (valid ? pr % nl : 0);
+          const double* zr = sS + r * kSP + (l - l0) * K;
+          const double* hb = a.hb + (size_t)l * K;
+          double p[16];
+          double zmax = -INFINITY;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          const int e = lane + 32 * m;
-          z[m] = e < cw ? zr[e] + hb[e] : -INFINITY;
-          zmax = fmax(zmax, z[m]);
-        }
+          for (int m = 0; m < 16; ++m) {
+            const int e = gl + 8 * m;
+            p[m] = (valid && e < K) ? zr[e] + hb[e] : -INFINITY;
+            zmax = fmax(zmax, p[m]);
+          }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
-        if (K <= kBT) {
-          // whole row here: softmax then top-k on the probabilities, exactly
-          // ref numkit.py:28-33 / :87-93 (descending, ties to the lower index)
-          double p[4], ssum = 0.0;
+          for (int o = 4; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+          double ssum = 0.0;
 #pragma unroll
-          for (int m = 0; m < 4; ++m) {
-            p[m] = lane + 32 * m < cw ? exp(z[m] - zmax) : 0.0;
+          for (int m = 0; m < 16; ++m) {
+            p[m] = (valid && gl + 8 * m < K) ? exp(p[m] - zmax) : 0.0;
             ssum += p[m];
           }
-          ssum = warp_sum(ssum);
 #pragma unroll
-          for (int m = 0; m < 4; ++m) p[m] = lane + 32 * m < cw ? p[m] / ssum : -2.0;
+          for (int o = 4; o > 0; o >>= 1) ssum += __shfl_xor_sync(0xffffffffu, ssum, o);
+#pragma unroll
+          for (int m = 0; m < 16; ++m) p[m] = (valid && gl + 8 * m < K) ? p[m] / ssum : -2.0;
           for (int rk = 0; rk < a.topk; ++rk) {
             double best = -1.0;
             int bi = 0x7fffffff;
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-              if (p[m] > best) { best = p[m]; bi = lane + 32 * m; }
-            seg_argmax(best, bi, 32);
-            if (lane == 0) emit(a, l, base + r0 + r, rk, bi, best);
+            for (int m = 0; m < 16; ++m)  // ascending expert ids: first max = lowest id
+              if (p[m] > best) { best = p[m]; bi = gl + 8 * m; }
+            seg_argmax(best, bi, 8);
+            if (valid && gl == 0) emit(a, l, base + r0 + r, rk, bi, best);
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-              if (lane + 32 * m == bi) p[m] = -2.0;
+            for (int m = 0; m < 16; ++m)
+              if (gl + 8 * m == bi) p[m] = -2.0;
           }
-        } else {
-          // online state: st[r] = {max, sum, (logit, id) x topk}, ids ranked
-          // by logit (= probability order), ties to the lower index
-          double* srow = st + r * kStatePitch;
-          double esum = 0.0;
-          double M = zmax;
-          if (ch > 0) M = fmax(srow[0], zmax);
+        }
+        __syncthreads();
+        continue;
+      }
+      // K > 128 (one layer, a 128-expert slice per chunk): eight lanes per row,
+      // 16 logits per lane, four rows per warp in flight; online state per
+      // row st[r] = {max, sum, (logit, id) x topk}, ids ranked by logit
+      // (= probability order), ties to the lower index
+      {
+        const int grp = lane >> 3, gl = lane & 7;
+        const int l = l0;
+        const double* hb = a.hb + (size_t)l * K + c0;
+        for (int pb = wib * 4; pb < rows; pb += 32) {
+          const int r = pb + grp;
+          const bool valid = r < rows;
+          const double* zr = sS + (valid ? r : 0) * kSP;
+          double z[16];
+          double zmax = -INFINITY;
 #pragma unroll
-          for (int m = 0; m < 4; ++m)
-            if (lane + 32 * m < cw) esum += exp(z[m] - M);
-          esum = warp_sum(esum);
-          const double S = ch > 0 ? srow[1] * exp(srow[0] - M) + esum : esum;
+          for (int m = 0; m < 16; ++m) {
+            const int e = gl + 8 * m;
+            z[m] = (valid && e < ncol) ? zr[e] + hb[e] : -INFINITY;
+            zmax = fmax(zmax, z[m]);
+          }
+#pragma unroll
+          for (int o = 4; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
+          double* srow = st + (valid ? r : 0) * kStatePitch;
+          const double prevM = (valid && ch > 0) ? srow[0] : -INFINITY;
+          const double M = fmax(prevM, zmax);
+          double esum = 0.0;
+#pragma unroll
+          for (int m = 0; m < 16; ++m)
+            if (valid && gl + 8 * m < ncol) esum += exp(z[m] - M);
+#pragma unroll
+          for (int o = 4; o > 0; o >>= 1) esum += __shfl_xor_sync(0xffffffffu, esum, o);
+          const double S = (valid && ch > 0) ? srow[1] * exp(prevM - M) + esum : esum;
           for (int rk = 0; rk < a.topk; ++rk) {
             double best = -INFINITY;
             int bi = 0x7fffffff;
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-              if (lane + 32 * m < cw && z[m] > best) { best = z[m]; bi = lane + 32 * m; }
-            seg_argmax(best, bi, 32);
+            for (int m = 0; m < 16; ++m)
+              if (gl + 8 * m < ncol && z[m] > best) { best = z[m]; bi = gl + 8 * m; }
+            seg_argmax(best, bi, 8);
 #pragma unroll
-            for (int m = 0; m < 4; ++m)
-              if (lane + 32 * m == bi) z[m] = -INFINITY;
-            if (lane == 0 && bi != 0x7fffffff) {
+            for (int m = 0; m < 16; ++m)
+              if (gl + 8 * m == bi) z[m] = -INFINITY;
+            if (valid && gl == 0 && bi != 0x7fffffff) {
               // insert (best, c0 + bi) into the ranked list (earlier slices
               // hold lower ids, so equal logits keep the earlier entry first)
               double* lst = srow + 2;
@@ -976,7 +1004,7 @@ attn_block_kernel(const BlockArgs ba) {
               }
             }
           }
-          if (lane == 0) {
+          if (valid && gl == 0) {
             srow[0] = M;
             srow[1] = S;
             if (ch == cpl - 1)
