@@ -257,7 +257,10 @@ lstm_quad_kernel(const double* __restrict__ xw, const double* __restrict__ tokx,
                  const double* __restrict__ posx, const double* __restrict__ cx,
                  const int32_t* __restrict__ tokens, const double* __restrict__ wh,
                  const double* __restrict__ b, const int32_t* __restrict__ seq_off, int n_seq,
-                 double* __restrict__ h_out) {
+                 double* __restrict__ h_out, int t0, int t1, double* __restrict__ c_buf) {
+  // steps [t0, t1) of every sequence: the recurrence is cut into short
+  // launches (state c in c_buf, h from h_out) so its CTAs never hold SMs for
+  // long -- the persistent compute-stream GEMMs then find their SMs free
   constexpr int G = 4 * H;
   __shared__ double s_h[2][H];
   const int t = threadIdx.x;
@@ -267,13 +270,16 @@ lstm_quad_kernel(const double* __restrict__ xw, const double* __restrict__ tokx,
   const int seq = blockIdx.x;
   const int base = seq_off[seq];
   const int len = seq_off[seq + 1] - base;
+  if (t0 >= len) return;  // (uniform per CTA, before any barrier)
+  const int tend = min(t1, len);
   double wcol[H];
 #pragma unroll
   for (int i = 0; i < H; ++i) wcol[i] = wh[(size_t)i * G + col];
   const double bg = b[col];
   const double cg = FOLD ? cx[col] : 0.0;
-  for (int i = t; i < H; i += blockDim.x) s_h[0][i] = 0.0;
-  double c_state = 0.0;
+  for (int i = t; i < H; i += blockDim.x)
+    s_h[t0 & 1][i] = t0 > 0 ? h_out[(size_t)(base + t0 - 1) * H + i] : 0.0;
+  double c_state = t0 > 0 ? c_buf[(size_t)seq * H + j] : 0.0;
   // x_t fetched ahead: token ids two steps, table rows one step (see lstm_kernel)
   auto tok_at = [&](int tt) -> int { return (FOLD && tt < len) ? __ldg(tokens + base + tt) : 0; };
   double xa = 0.0, xb = 0.0;
@@ -287,10 +293,10 @@ lstm_quad_kernel(const double* __restrict__ xw, const double* __restrict__ tokx,
       xa = __ldg(xw + (size_t)(base + tt) * G + col);
     }
   };
-  load_parts(0, tok_at(0));
-  int tok1 = tok_at(1);
+  load_parts(t0, tok_at(t0));
+  int tok1 = tok_at(t0 + 1);
   __syncthreads();
-  for (int tt = 0; tt < len; ++tt) {
+  for (int tt = t0; tt < tend; ++tt) {
     const double* hp = s_h[tt & 1];
     const double x = FOLD ? (xa + xb) + cg : xa;
     const int tok2 = tok_at(tt + 2);
@@ -319,6 +325,7 @@ lstm_quad_kernel(const double* __restrict__ xw, const double* __restrict__ tokx,
     }
     __syncthreads();
   }
+  if (q == 0 && tend < len) c_buf[(size_t)seq * H + j] = c_state;
 }
 
 // C (N x M) = A (N x Kd) @ B (Kd x M), fp64. Block = 64 rows; A and B in smem;
@@ -1116,13 +1123,23 @@ extern "C" size_t sida_hash_workspace_bytes(int n_tokens, int n_seq, int max_len
   (void)max_len; (void)d; (void)cd; (void)L; (void)K;
   const size_t n = (size_t)n_tokens;
   return ws_align(n * 4 * H * 8) + 2 * ws_align(n * H * 8) + ws_align(n * 3 * H * 8) +
-         ws_align(((size_t)n_seq + 1) * 4) + 256;
+         ws_align(((size_t)n_seq + 1) * 4) + ws_align((size_t)n_seq * H * 8) + 256;
+}
+
+static int lstm_chunk() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SIDA_LSTM_CHUNK");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
 }
 
 template <int MAXH, bool FOLD>
 static int launch_lstm(const double* xw, const double* tokx, const double* posx, const double* cx,
                        const int32_t* tokens, const double* wh, const double* b,
-                       const int32_t* seq_off, int n_seq, int H, double* h_out, cudaStream_t s) {
+                       const int32_t* seq_off, int n_seq, int H, double* h_out, cudaStream_t s,
+                       int max_len, double* c_buf) {
   int S = 1;
   if (n_seq >= 4 * kNumSMs) S = 4;
   else if (n_seq >= 2 * kNumSMs) S = 2;
@@ -1132,9 +1149,12 @@ static int launch_lstm(const double* xw, const double* tokx, const double* posx,
   else if (S == 2)
     lstm_kernel<MAXH, 2, FOLD><<<ceil_div(n_seq, 2), 4 * MAXH, 0, s>>>(
         xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out);
-  else if (H == MAXH && !getenv("SIDA_LSTM_SPLIT"))
-    lstm_quad_kernel<MAXH, FOLD><<<n_seq, 4 * MAXH, 0, s>>>(xw, tokx, posx, cx, tokens, wh, b,
-                                                           seq_off, n_seq, h_out);
+  else if (H == MAXH && !getenv("SIDA_LSTM_SPLIT")) {
+    const int chunk = lstm_chunk() > 0 ? lstm_chunk() : max_len;
+    for (int t0 = 0; t0 < max_len; t0 += chunk)
+      lstm_quad_kernel<MAXH, FOLD><<<n_seq, 4 * MAXH, 0, s>>>(
+          xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, h_out, t0, t0 + chunk, c_buf);
+  }
   else
     lstm_kernel<MAXH, 1, FOLD><<<n_seq, 4 * MAXH, 0, s>>>(xw, tokx, posx, cx, tokens, wh, b,
                                                           seq_off, n_seq, H, h_out);
@@ -1146,11 +1166,11 @@ template <bool FOLD>
 static int lstm_dispatch(const double* xw, const double* tokx, const double* posx,
                          const double* cx, const int32_t* tokens, const double* wh,
                          const double* b, const int32_t* seq_off, int n_seq, int H, double* h_out,
-                         cudaStream_t s) {
-  if (H <= 16) return launch_lstm<16, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s);
-  if (H <= 32) return launch_lstm<32, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s);
-  if (H <= 48) return launch_lstm<48, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s);
-  return launch_lstm<64, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s);
+                         cudaStream_t s, int max_len, double* c_buf) {
+  if (H <= 16) return launch_lstm<16, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s, max_len, c_buf);
+  if (H <= 32) return launch_lstm<32, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s, max_len, c_buf);
+  if (H <= 48) return launch_lstm<48, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s, max_len, c_buf);
+  return launch_lstm<64, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s, max_len, c_buf);
 }
 
 static int rows_gemm(const double* A, int n, int Kd, const double* B, int M, double* C,
@@ -1209,7 +1229,8 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
   double* h1 = reinterpret_cast<double*>(ws); ws += ws_align(n * H * 8);
   double* h2 = reinterpret_cast<double*>(ws); ws += ws_align(n * H * 8);
   double* qkv = reinterpret_cast<double*>(ws); ws += ws_align(n * 3 * H * 8);
-  int32_t* blk_off = reinterpret_cast<int32_t*>(ws);
+  int32_t* blk_off = reinterpret_cast<int32_t*>(ws); ws += ws_align(((size_t)n_seq + 1) * 4);
+  double* c_buf = reinterpret_cast<double*>(ws);
 
   int st;
   if (emb_f64) {
@@ -1217,15 +1238,15 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
                                                               w.cb, w.wx1, xw);
     SIDA_LAUNCH_CHECK();
     st = lstm_dispatch<false>(xw, nullptr, nullptr, nullptr, nullptr, w.wh1, w.b1, seq_off, n_seq,
-                              H, h1, s);
+                              H, h1, s, max_len, c_buf);
   } else {
     st = lstm_dispatch<true>(nullptr, tb.tokx, tb.posx, tb.cx, tokens, w.wh1, w.b1, seq_off,
-                             n_seq, H, h1, s);
+                             n_seq, H, h1, s, max_len, c_buf);
   }
   if (st) return st;
   if ((st = rows_gemm(h1, n_tokens, H, w.wx2, G, xw, s))) return st;
   if ((st = lstm_dispatch<false>(xw, nullptr, nullptr, nullptr, nullptr, w.wh2, w.b2, seq_off,
-                                 n_seq, H, h2, s)))
+                                 n_seq, H, h2, s, max_len, c_buf)))
     return st;
   if ((st = rows_gemm(h2, n_tokens, H, tb.wqkv, 3 * H, qkv, s))) return st;
   // blocked path (register-tiled fp64 GEMM shapes, K/V streamed in chunks):

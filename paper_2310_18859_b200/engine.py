@@ -81,6 +81,56 @@ class _BatchPlan:
         self.early = 0  # groups issued before this batch's forward started
 
 
+class _StaticTable:
+    """The per-layer permutation arrays a captured forward reads."""
+
+    def __init__(self, dt):
+        self.k = dt.k
+        self.off, self.perm = dt.off.clone(), dt.perm.clone()
+        self.inv, self.alpha_perm = dt.inv.clone(), dt.alpha_perm.clone()
+
+    def layer(self, layer: int):
+        return self.off[layer], self.perm[layer], self.alpha_perm[layer]
+
+
+class _GraphEntry:
+    """One captured forward for a fixed lengths signature: static token and
+    permutation buffers, per-layer expert -> slot rows on the device, the
+    graph and its logits buffer (graph-private memory pool)."""
+
+    def __init__(self, eng: "SidaEngine", lengths, dt, tokens_dev, waves):
+        model, cs = eng.model, eng.compute_stream
+        self.tokens = tokens_dev.clone()
+        self.table = _StaticTable(dt)
+        self.lay = BatchLayout(list(lengths), self.tokens, model.device)
+        self.row_host = [w[0].slot_row.copy() for w in waves]
+        self.rows = [eng.store.rows.upload(r, cs).clone() for r in self.row_host]
+        # one eager pass first (library handles, lazily loaded kernels), then capture
+        eng._graph_body(self.lay, self.table, waves, self.rows)
+        # (capture_begin/end directly: torch.cuda.graph() would also run a
+        # full gc.collect() and empty the caching allocator on every capture)
+        self.graph = torch.cuda.CUDAGraph()
+        cs.synchronize()
+        with torch.cuda.stream(cs):
+            self.graph.capture_begin(capture_error_mode="thread_local")
+            try:
+                self.logits = eng._graph_body(self.lay, self.table, waves, self.rows)
+            finally:
+                self.graph.capture_end()
+
+    def load(self, dt, tokens_dev, waves, store, cs) -> None:
+        t = self.table
+        self.tokens.copy_(tokens_dev, non_blocking=True)
+        for dst, src in ((t.off, dt.off), (t.perm, dt.perm), (t.inv, dt.inv),
+                         (t.alpha_perm, dt.alpha_perm)):
+            dst.copy_(src, non_blocking=True)
+        for layer, w in enumerate(waves):
+            r = w[0].slot_row
+            if len(r) != len(self.row_host[layer]) or (r != self.row_host[layer]).any():
+                self.rows[layer][: len(r)].copy_(store.rows.upload(r, cs))
+                self.row_host[layer] = r.copy()
+
+
 class SidaEngine:
     """Streams, HBM slot arena and residency state of one serving instance."""
 
@@ -119,6 +169,14 @@ class SidaEngine:
         # when none of its victims is read by layers l..g (reference: 1)
         self.depth = int(os.environ.get("SIDA_PREFETCH_DEPTH", "1"))
         self._pending: _BatchPlan | None = None
+        # CUDA-graph replay of whole forwards (see _forward_graph): batches of
+        # at most `graph_max_tokens` tokens whose experts are all resident; a
+        # lengths signature is captured the second time it is seen
+        self.graph_max_tokens = int(os.environ.get("SIDA_GRAPH_MAX_TOKENS", "16384"))
+        self.graph_cap = 8
+        self._graphs: dict = {}
+        self._graph_seen: dict = {}
+        self.graph_replays = 0
 
     # -- hash stream ------------------------------------------------------------------
     def hash_tokens(self, batch_id: int, tokens_dev: torch.Tensor, lengths) -> ExpertHashTable:
@@ -150,6 +208,10 @@ class SidaEngine:
         dt.use_on(cs)
         ev0.record(cs)
         done, issued = bp.done, bp.issued
+        if self._graphable(bp, dt, lengths):
+            logits = self._forward_graph(bp, dt, lengths, tokens_dev)
+            ev1.record(cs)
+            return logits, self._record(table, lengths, bp), (ev0, ev1)
 
         def issue(idx: int):
             self._issue(bp, idx)
@@ -211,10 +273,14 @@ class SidaEngine:
                     self.ffn_events.append((e_a, e_b, x.shape[0], len(required[layer])))
             logits = model.pool_classify(x, lay)
         ev1.record(cs)
+        return logits, self._record(table, lengths, bp), (ev0, ev1)
+
+    def _record(self, table, lengths, bp: _BatchPlan) -> dict:
+        state, plan = self.state, bp.plan
         resident_req = [k for k in table.required_experts() if k in state.resident]
         util = (sum(state.resident[k] for k in resident_req) / state.used_bytes
                 if state.used_bytes else 1.0)
-        record = {
+        return {
             "batch_id": table.batch_id,
             "num_samples": len(lengths),
             "num_tokens": int(sum(lengths)),
@@ -223,7 +289,64 @@ class SidaEngine:
             "groups_issued_ahead": bp.early,
             "utilization": util,
         }
-        return logits, record, (ev0, ev1)
+
+    # -- CUDA-graph replay ---------------------------------------------------------------
+    def _graphable(self, bp: _BatchPlan, dt, lengths) -> bool:
+        """Small batches are host-bound (~0.2 ms of Python + launches per
+        layer against a few us of GPU work), so a forward that moves no
+        expert runs as one graph launch. Eligible: no copies in the plan (all
+        required experts resident), single-wave layers, the fused
+        out-projection path, no per-layer timing requested."""
+        n_tok = int(sum(lengths))
+        if (n_tok > self.graph_max_tokens or self.ffn_events is not None
+                or self.model.wo_t is None or dt.k > 4 or bp.plan.loads):
+            return False
+        key = (tuple(int(n) for n in lengths), dt.k)
+        if key not in self._graphs:
+            self._graph_seen[key] = self._graph_seen.get(key, 0) + 1
+            if self._graph_seen[key] < 2:
+                return False  # one-off shapes stay eager
+        for idx in range(len(bp.plan.groups)):
+            if not bp.issued[idx]:
+                self._issue(bp, idx)  # bookkeeping only: the plan has no loads
+        return all(len(w) == 1 for w in bp.waves)
+
+    def _graph_body(self, lay: BatchLayout, dt, waves, rows):
+        model, cs = self.model, self.compute_stream
+        x = model.embed_layout(lay)
+        xb = None
+        for layer in range(model.config.num_layers):
+            x_perm = torch.empty((lay.n_tokens * dt.k, model.config.d_model),
+                                 dtype=torch.bfloat16, device=x.device)
+            x = model.attention_mix(layer, x, lay, xb=xb, scatter=(dt.inv[layer], dt.k, x_perm))
+            xb = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
+            x = run_waves(model, waves[layer], x, dt, self.store, cs, out_bf16=xb,
+                          x_perm=x_perm, rows_dev=[rows[layer]])
+        return model.pool_classify(x, lay)
+
+    def _forward_graph(self, bp: _BatchPlan, dt, lengths, tokens_dev):
+        """Copy the batch's tokens and permutation into the graph's static
+        buffers, refresh any expert -> slot row that changed, replay. The
+        slots read are marked with one event after the replay."""
+        cs, store = self.compute_stream, self.store
+        key = (tuple(int(n) for n in lengths), dt.k)
+        ent = self._graphs.pop(key, None)
+        with torch.cuda.stream(cs):
+            if ent is None:
+                ent = _GraphEntry(self, lengths, dt, tokens_dev, bp.waves)
+                if len(self._graphs) >= self.graph_cap:
+                    self._graphs.pop(next(iter(self._graphs)))
+            else:
+                ent.load(dt, tokens_dev, bp.waves, store, cs)
+            self._graphs[key] = ent  # most recently used last
+            ent.graph.replay()
+            logits = ent.logits.clone()
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        for w in bp.waves:
+            store.mark_read(w[0].slot_row, ev)
+        self.graph_replays += 1
+        return logits
 
     # -- planning / issue ---------------------------------------------------------------
     def _plan_batch(self, table) -> _BatchPlan:

@@ -372,14 +372,17 @@ class ExpertStore:
 
 
 def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=None,
-              issue=None, out_bf16=None, table_layer: int | None = None, x_perm=None):
+              issue=None, out_bf16=None, table_layer: int | None = None, x_perm=None,
+              rows_dev=None):
     """Execute one layer as a sequence of waves on ``stream``: wait for each
     wave's copies, run the grouped FFN over its experts, record the reader
     event. ``issue(wave)`` (optional) enqueues a wave's copies just in time and
     returns their done event. ``out_bf16`` (optional) receives the layer
     output rounded to bf16 from the same epilogue. ``x_perm`` (optional) is
     the layer input already in expert-sorted bf16 rows (written by the fused
-    attention output projection); without it each wave gathers."""
+    attention output projection); without it each wave gathers. ``rows_dev``
+    (optional, per wave) are device-resident expert -> slot rows: no upload,
+    no reader event (the graph-replay path records those around the replay)."""
     c = model.config
     k = dev_table.k
     layer = waves[0].layer
@@ -395,16 +398,18 @@ def run_waves(model, waves, x, dev_table, store: ExpertStore, stream, pre_done=N
             stream.wait_event(done)
         if not wave.experts:
             continue
-        row = store.rows.upload(wave.slot_row, stream)
+        row = (rows_dev[i] if rows_dev is not None
+               else store.rows.upload(wave.slot_row, stream))
         elist = None
         if multi:
             elist = store.rows.upload(np.asarray(wave.experts, dtype=np.int32), stream)
         with torch.cuda.stream(stream):
             model.moe_apply_rows(tables, x, k, store, row, expert_list=elist, out=out, y=y,
                                  stream=stream, out_bf16=out_bf16, x_perm=x_perm)
-        ev = torch.cuda.Event()
-        ev.record(stream)
-        store.mark_read(wave.slot_row, ev)
+        if rows_dev is None:
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            store.mark_read(wave.slot_row, ev)
     if k > 1:
         with torch.cuda.stream(stream):
             out = model.combine(y, x, k, out=out, stream=stream, out_bf16=out_bf16)
