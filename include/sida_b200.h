@@ -158,6 +158,15 @@ int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, int d, int h
  * out: uint64 [2 GEMMs][148 CTAs][8]. Synchronises the device. */
 int sida_debug_gemm_prof(unsigned long long* out);
 
+/* Expert-FFN tile family for sida_grouped_ffn_bf16: -1 auto, 0 token-M
+ * tiles for both GEMMs (128/256 token rows x BN features), 1 token-N tiles
+ * for both (swap-AB: 256 features x 16..256 token rows in steps of 16),
+ * 2 token-M GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2.
+ * Process-wide; the initial value comes from SIDA_FFN_SWAP.
+ * sida_get_ffn_tiles returns the current mode. */
+int sida_set_ffn_tiles(int mode);
+int sida_get_ffn_tiles(void);
+
 /* Fused mixing-attention core (ref moe.py:220-233 without the projections):
  * ctx = softmax(q k^T / sqrt(d)) v per sequence, single head, non-causal, on
  * tcgen05 (scores and P.V in TMEM, softmax in registers). qkv bf16

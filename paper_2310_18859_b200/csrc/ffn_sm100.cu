@@ -584,6 +584,279 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   }
 }
 
+// ------------------------------------------------------------ token-N tiles
+// Swap-AB variant for experts holding few rows (many-expert layers): the
+// expert's weight rows are the UMMA M side (256 output features per CTA pair,
+// cta_group::2) and its token rows the N side, sized per expert in steps of 16
+// (tcgen05 cost is proportional to N), so an expert of R rows wastes at most
+// 15 rows per tile instead of up to 127 (BM = 128 token tiles: 2.5 tiles of
+// MMA for 2 tiles of work at 256 rows per expert). D in TMEM is
+// (feature lane, token column): each epilogue thread owns one output feature
+// and walks 32 tokens per tcgen05.ld, so for a fixed token a warp's stores
+// cover 32 consecutive features (64 B bf16 / 128 B fp32 row segments) and
+// need no shared-memory transpose.
+constexpr int kTnMax = 256;     // tokens per tile (UMMA N, pair)
+constexpr int kTnBox = 64;      // token rows per TMA box
+constexpr int kTnStages = 6;    // {A 16 KB, B <= 16 KB} per CTA
+
+// Token tiles of an expert with R rows: count tiles of `base` rows (multiple
+// of 16, <= 256), balanced so the last tile is not a sliver.
+__device__ __forceinline__ void tn_split(int R, int& base, int& count) {
+  if (R <= 0) { base = 16; count = 0; return; }
+  const int n = ceil_div(R, kTnMax);
+  base = min(kTnMax, (ceil_div(R, n) + 15) & ~15);
+  count = ceil_div(R, base);
+}
+
+__device__ __forceinline__ uint32_t idesc_bf16_rt(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+struct TnTile {
+  int expert, row0, nrows, nmma, f0, slot;
+};
+
+template <int STAGE>
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature, slot), box 64x128
+                       const __grid_constant__ CUtensorMap tmX,  // (k, row), box 64x32
+                       const GemmParams p) {
+  // STAGE 1: hidden = relu(X W1^T + b1); STAGE 2: out = alpha (H W2^T + b2) + resid
+  constexpr uint32_t kABytes = 128 * BK * 2;
+  constexpr uint32_t kBBytes = (kTnMax / 2) * BK * 2;
+  constexpr uint32_t kBoxBytes = kTnBox * BK * 2;
+  constexpr uint32_t kTmemCols = 2 * kTnMax;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + kTnStages * kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + kTnStages * kBBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kTnStages;
+  uint64_t* tmem_full = bars + 2 * kTnStages;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  int32_t* s_prefix = reinterpret_cast<int32_t*>(s_tmem + 4);
+  int32_t* s_expert = s_prefix + kMaxListed + 1;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_list = p.expert_list ? p.n_list : p.num_experts;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x >> 1, n_units = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < n_list; ++i) {
+      const int e = p.expert_list ? p.expert_list[i] : i;
+      int base, cnt;
+      tn_split(expert_row(p, e + 1) - expert_row(p, e), base, cnt);
+      s_expert[i] = e;
+      s_prefix[i] = acc;
+      acc += cnt;
+    }
+    s_prefix[n_list] = acc;
+    for (int i = 0; i < kTnStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  const int n_ft = p.ndim / 256;  // feature tiles per expert (M = 256 per pair)
+  const int total = s_prefix[n_list] * n_ft;
+  const int nkb = p.kdim / BK;
+  auto get_tile = [&](int it) -> TnTile {
+    const int mt = it / n_ft;
+    const int nt = it - mt * n_ft;
+    int lo = 0, hi = n_list - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_prefix[mid] <= mt) lo = mid; else hi = mid - 1;
+    }
+    TnTile t;
+    t.expert = s_expert[lo];
+    const int seg0 = expert_row(p, t.expert);
+    const int R = expert_row(p, t.expert + 1) - seg0;
+    int base, cnt;
+    tn_split(R, base, cnt);
+    const int j = mt - s_prefix[lo];
+    t.row0 = seg0 + j * base;
+    t.nrows = min(base, R - j * base);
+    t.nmma = (t.nrows + 15) & ~15;
+    t.f0 = nt * 256;
+    t.slot = p.expert_slot ? p.expert_slot[t.expert] : 0;
+    return t;
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs): own 128 weight rows, own half of the tokens
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = unit; it < total; it += n_units) {
+        const TnTile t = get_tile(it);
+        if (t.slot < 0) continue;
+        const int half_rows = t.nmma >> 1;
+        const int nbox = ceil_div(half_rows, kTnBox);
+        const int xrow = t.row0 + static_cast<int>(rank) * half_rows;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          const uint32_t fb = map_rank(smem_u32(&full[stage]), 0);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBoxBytes));
+          tma_load_3d<2>(sA + stage * kABytes, &tmW, kb * BK, t.f0 + rank * 128, t.slot, fb);
+          for (int b = 0; b < nbox; ++b)
+            tma_load_2d<2>(sB + stage * kBBytes + b * kBoxBytes, &tmX, kb * BK, xrow + b * kTnBox,
+                           fb);
+          if (++stage == kTnStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader CTA, one lane): M = 256 features x N = nmma tokens
+    if (lane == 0 && leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int it = unit; it < total; it += n_units) {
+        const TnTile t = get_tile(it);
+        if (t.slot < 0) {
+          atomicExch(p.err_flag, 1);
+          continue;
+        }
+        const uint32_t idesc = idesc_bf16_rt(256, t.nmma);
+        mbar_wait_cluster(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kTnMax;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * kABytes);
+          const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k)
+            umma_bf16<2>(d_tmem, sw128_desc(a0 + k * UMMA_K * 2), sw128_desc(b0 + k * UMMA_K * 2),
+                         idesc, (kb | k) != 0);
+          tc_commit<2>(&empty[stage]);
+          if (++stage == kTnStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit<2>(&tmem_full[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ===== epilogue: warp owns TMEM lanes 32*(w%4).. (32 features of this
+    // CTA's 128) and every other 32-token chunk of the tile
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int it = unit; it < total; it += n_units) {
+      const TnTile t = get_tile(it);
+      if (t.slot < 0) continue;
+      const int f = t.f0 + static_cast<int>(rank) * 128 + quarter * 32 + lane;
+      const uint16_t* bias = reinterpret_cast<const uint16_t*>(
+          p.arena + static_cast<size_t>(t.slot) * p.slot_stride + p.bias_off);
+      const float b = bf16_to_f32(bias[f]);
+      const int nch = ceil_div(t.nrows, 32);
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kTnMax;
+      for (int c = half; c < nch; c += 2) {
+        uint32_t v[32];
+        tmem_ld32_nowait(t_lane + c * 32, v);
+        const int tok0 = t.row0 + c * 32;
+        const int cnt = min(32, t.nrows - c * 32);
+        if (STAGE == 1) {
+          tmem_wait_ld();
+          // lane pairs (f, f+1) trade halves so each lane stores one bf16x2
+          // word per token pair: even lanes the even tokens, odd lanes the odd
+          // ones (a warp store covers two 64 B row segments)
+          const bool odd = lane & 1;
+          uint32_t* dst = reinterpret_cast<uint32_t*>(
+              p.hidden + static_cast<size_t>(tok0 + (odd ? 1 : 0)) * p.ndim + (f & ~1));
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float y0 = fmaxf(__uint_as_float(v[j]) + b, 0.f);
+            const float y1 = fmaxf(__uint_as_float(v[j + 1]) + b, 0.f);
+            const float other = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
+            const uint32_t w = odd ? bf16x2_rn(other, y1) : bf16x2_rn(y0, other);
+            if (j + (odd ? 1 : 0) < cnt) dst[static_cast<size_t>(j) * (p.ndim >> 1)] = w;
+          }
+        } else {
+          // per-token row map / alpha: lane j holds token tok0 + j's, broadcast by shuffles
+          const int my_tok = tok0 + lane;
+          int orow_l = my_tok;
+          float a_l = 1.f;
+          if (lane < cnt) {
+            if (p.row_map) orow_l = p.row_map[my_tok];
+            if (p.alpha) a_l = p.alpha[my_tok];
+          }
+          float x[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int o = __shfl_sync(0xffffffffu, orow_l, j);
+            x[j] = (p.resid && j < cnt) ? __ldg(p.resid + static_cast<size_t>(o) * p.ndim + f) : 0.f;
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int o = __shfl_sync(0xffffffffu, orow_l, j);
+            const float a = __shfl_sync(0xffffffffu, a_l, j);
+            if (j < cnt) {
+              const float y = x[j] + (__uint_as_float(v[j]) + b) * a;
+              const size_t at = static_cast<size_t>(o) * p.ndim + f;
+              if (p.out) p.out[at] = y;
+              if (p.out_bf16) p.out_bf16[at] = __bfloat16_as_ushort(__float2bfloat16_rn(y));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(&tmem_empty[acc]), 0));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+constexpr size_t tn_smem_bytes() {
+  return 1024 + kTnStages * (128 * BK * 2 + (kTnMax / 2) * BK * 2) + (2 * kTnStages + 4) * 8 + 16 +
+         (2 * kMaxListed + 2) * 4;
+}
+
 template <int BN, int STAGE, int CG>
 constexpr size_t smem_bytes() {
   return 1024 + stages_for<BN, STAGE, CG>() * (BM * BK * 2 + (BN / CG) * BK * 2) +
@@ -717,6 +990,42 @@ static int dispatch_bn(const void* a_base, const void* b_base, int n_slots, cons
   return launch_gemm<64, STAGE, CG>(a_base, b_base, n_slots, p, n_listed, s);
 }
 
+// Token-N (swap-AB) launch: a_base = token rows (x_perm / hidden), b_base =
+// the weight arena at this GEMM's matrix offset.
+template <int STAGE>
+static int launch_tn(const void* x_base, const void* w_base, int n_slots, const GemmParams& p,
+                     int n_listed, cudaStream_t s) {
+  auto kern = grouped_gemm_tn_kernel<STAGE>;
+  static bool configured = false;
+  if (!configured) {
+    SIDA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)tn_smem_bytes()));
+    configured = true;
+  }
+  CUtensorMap tw, tx;
+  int st = make_map_3d(&tw, w_base, p.kdim, p.ndim, n_slots, p.slot_stride, 128);
+  if (st) return st;
+  if ((st = make_map_2d(&tx, x_base, p.kdim, p.n_rows, kTnBox))) return st;
+  const int max_tiles = (ceil_div(p.n_rows, kTnMax) + n_listed) * (p.ndim / 256);
+  const int units = std::max(1, std::min(max_tiles, kNumSMs / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units * 2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = tn_smem_bytes();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, tw, tx, p));
+  return SIDA_OK;
+}
+
 // CTA-pair (M=256) tiles when experts hold enough rows to fill them.
 template <int STAGE>
 static int dispatch_gemm(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
@@ -766,6 +1075,48 @@ static int choose_cg(int n_rows, int listed) {
   return n_rows >= 1024 * listed ? 2 : 1;
 }
 
+// Tile family per expert GEMM (sida_set_ffn_tiles, or SIDA_FFN_SWAP at load):
+// -1 auto, 0 token-M for both GEMMs, 1 token-N (swap-AB) for both, 2 token-M
+// GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2. Auto picks token-N
+// per GEMM where it measured faster (tools/ffn_probe.py, profiles/r1): only
+// GEMM2 (K = h: long k-loop, fp32 residual epilogue) and only while the
+// listed experts average [SIDA_FFN_SWAP_LO, SIDA_FFN_SWAP_HI) rows.
+static int g_tn_mode = -2;
+static int g_tn_lo = 192, g_tn_hi = 384;
+
+static void tn_init() {
+  if (g_tn_mode != -2) return;
+  const char* e = getenv("SIDA_FFN_SWAP");
+  g_tn_mode = e ? atoi(e) : -1;
+  if (const char* r = getenv("SIDA_FFN_SWAP_LO")) g_tn_lo = atoi(r);
+  if (const char* r = getenv("SIDA_FFN_SWAP_HI")) g_tn_hi = atoi(r);
+}
+
+static bool choose_tn(int gemm, int n_rows, int listed, int d, int h) {
+  tn_init();
+  if (d % 256 != 0 || h % 256 != 0) return false;
+  switch (g_tn_mode) {
+    case 0: return false;
+    case 1: return true;
+    case 2: return gemm == 2;
+    case 3: return gemm == 1;
+    default: break;
+  }
+  return gemm == 2 && n_rows >= g_tn_lo * listed && n_rows < g_tn_hi * listed;
+}
+
+extern "C" int sida_set_ffn_tiles(int mode) {
+  SIDA_REQUIRE(mode >= -1 && mode <= 3, SIDA_ERR_CONTRACT, "ffn tile mode %d not in -1..3", mode);
+  tn_init();
+  g_tn_mode = mode;
+  return SIDA_OK;
+}
+
+extern "C" int sida_get_ffn_tiles(void) {
+  tn_init();
+  return g_tn_mode;
+}
+
 extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h,
                                      const int32_t* off, int num_experts,
                                      const int32_t* expert_slot, const int32_t* expert_list,
@@ -797,7 +1148,8 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   p1.expert_list = expert_list; p1.n_list = n_list;
   p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
   p1.hidden = hidden; p1.err_flag = err_flag; p1.prof = prof_buffer(0);
-  int st = sm100::dispatch_gemm<1>(x_perm, ar, n_slots, p1, listed, cg, s);
+  int st = choose_tn(1, n_rows, listed, d, h) ? sm100::launch_tn<1>(x_perm, ar, n_slots, p1, listed, s)
+              : sm100::dispatch_gemm<1>(x_perm, ar, n_slots, p1, listed, cg, s);
   if (st) return st;
 
   sm100::GemmParams p2 = p1;
@@ -805,6 +1157,7 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   p2.row_map = row_map; p2.alpha = alpha; p2.resid = resid; p2.out = out;
   p2.out_bf16 = out_bf16;
   p2.prof = prof_buffer(1);
+  if (choose_tn(2, n_rows, listed, d, h)) return sm100::launch_tn<2>(hidden, ar + w2_off, n_slots, p2, listed, s);
   return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, listed, cg, s);
 }
 

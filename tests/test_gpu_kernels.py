@@ -139,12 +139,32 @@ def _ids_for(N, k, K, g, skew=True):
     return np.stack([np.stack([g.permutation(K)[:k] for _ in range(N)])])[None][0]
 
 
+@pytest.fixture
+def ffn_tiles():
+    """Set the expert-FFN tile family (sida_set_ffn_tiles) for one test."""
+    _l, h = _lib()
+    prev = h.sida_get_ffn_tiles()
+
+    def set_mode(mode):
+        _l.check(h.sida_set_ffn_tiles(mode))
+
+    yield set_mode
+    _l.check(h.sida_set_ffn_tiles(prev))
+
+
+@pytest.mark.parametrize("tiles", [-1, 0, 1, 2, 3])
 @pytest.mark.parametrize("d,hdim,K,N,k", [
     (64, 128, 4, 300, 1), (256, 1024, 8, 1024, 1), (768, 3072, 8, 2048, 1),
-    (128, 256, 8, 700, 2), (768, 3072, 4, 257, 3)])
-def test_grouped_ffn_bf16_vs_oracle(cuda_device, d, hdim, K, N, k):
+    (128, 256, 8, 700, 2), (768, 3072, 4, 257, 3), (256, 1024, 32, 1500, 1),
+    (768, 3072, 64, 6000, 1), (512, 1024, 16, 900, 2)])
+def test_grouped_ffn_bf16_vs_oracle(cuda_device, ffn_tiles, tiles, d, hdim, K, N, k):
+    """tiles: -1 auto, 0 token-M (128/256-row token tiles), 1 token-N
+    (swap-AB: 256 features x 16..256 tokens), 2/3 mixed per GEMM; token-N
+    needs d, h % 256."""
     from paper_2310_18859_b200.offload import ExpertStore
     from paper_2310_18859_b200.predictor import ExpertHashTable
+
+    ffn_tiles(tiles)
 
     shape, params, model = _moe_setup(d, hdim, K)
     g = np.random.default_rng(d + N)
@@ -399,7 +419,8 @@ def test_attention_core_contracts(cuda_device):
 @pytest.mark.parametrize("d,hdim,K,N,k,lag", [
     (256, 1024, 8, 1024, 1, 1), (768, 3072, 8, 9000, 1, 4), (256, 1024, 8, 700, 2, 32),
     (256, 1024, 64, 3000, 1, 2), (768, 3072, 2, 4096, 1, 3)])
-def test_fused_ffn_launch_identical_to_two_launches(cuda_device, d, hdim, K, N, k, lag):
+def test_fused_ffn_launch_identical_to_two_launches(cuda_device, ffn_tiles, d, hdim, K, N, k,
+                                                    lag):
     """sida_grouped_ffn_bf16_fused (GEMM1/GEMM2 tiles interleaved in one
     persistent launch, GEMM2 gated on per-m-tile release counts) computes the
     same tiles with the same epilogues: results bit-identical to the
@@ -408,6 +429,7 @@ def test_fused_ffn_launch_identical_to_two_launches(cuda_device, d, hdim, K, N, 
     from paper_2310_18859_b200.offload import ExpertStore
     from paper_2310_18859_b200.predictor import ExpertHashTable
 
+    ffn_tiles(0)  # the fused launch interleaves token-M tiles
     shape, params, model = _moe_setup(d, hdim, K)
     g = np.random.default_rng(d + N + K)
     ids = _ids_for(N, k, K, g)
@@ -427,4 +449,39 @@ def test_fused_ffn_launch_identical_to_two_launches(cuda_device, d, hdim, K, N, 
         mmod._FFN_FUSED, mmod._FFN_LAG = saved
     assert torch.equal(outs[0][0], outs[1][0])
     assert torch.equal(outs[0][1], outs[1][1])
+    assert store.err_flag.item() == 0
+
+
+@pytest.mark.parametrize("K,N,skew", [(128, 32768, False), (8, 32768, False), (256, 20000, True),
+                                      (64, 4097, True)])
+def test_ffn_token_n_tiles_match_token_m_tiles(cuda_device, ffn_tiles, K, N, skew):
+    """Switch-base shapes: the token-N (swap-AB) and token-M tile families
+    compute the same layer (fp32 accumulation in a different MMA shape: equal
+    within 1e-3 * rms), including skewed routing with empty and one-row experts."""
+    from paper_2310_18859_b200.offload import ExpertStore
+    from paper_2310_18859_b200.predictor import ExpertHashTable
+
+    d, hdim = 768, 3072
+    from paper_2310_18859_b200.moe import MoEConfig, MoEModel
+
+    cfg = MoEConfig(vocab_size=64, d_model=d, num_layers=1, num_experts=K, expert_hidden=hdim,
+                    max_seq_len=16)
+    model = MoEModel.synthetic(cfg, 0)
+    g = np.random.default_rng(K + N)
+    ids = _ids_for(N, 1, K, g, skew=skew) if skew else g.integers(0, K, size=(1, N, 1))
+    alphas = g.uniform(0.05, 1.0, size=ids.shape)
+    x = torch.from_numpy(g.normal(0, 1.0, (N, d))).float().cuda()
+    dt = ExpertHashTable(0, [N], ids, alphas).on_device(model)
+    store = ExpertStore.full(model)
+    outs = []
+    for mode in (0, 1, 2, 3):
+        ffn_tiles(mode)
+        ob = torch.empty((N, d), dtype=torch.bfloat16, device="cuda")
+        outs.append((store.run_layer(model, 0, x, dt, out_bf16=ob), ob))
+        torch.cuda.synchronize()
+    ref = outs[0][0] - x
+    rms = ref.pow(2).mean().sqrt().item()
+    for out, ob in outs[1:]:
+        assert (out - x - ref).abs().max().item() <= 1e-3 * rms
+        assert torch.equal(ob, out.bfloat16())
     assert store.err_flag.item() == 0

@@ -42,7 +42,7 @@ out = store.run_layer(model, 0, x, dt)  # loads experts
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 from paper_2310_18859_b200.offload import Wave, run_waves  # noqa: E402
-need = list(range(K))
+need = [int(e) for e in np.nonzero(hist[0])[0]]
 wave = Wave(0, [], need, store.slot_row(0, need))
 if a.alias_slots:
     wave.slot_row = (wave.slot_row % a.alias_slots).astype(np.int32)
