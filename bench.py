@@ -58,6 +58,8 @@ def parse():
     p.add_argument("--ep-transport", default="nccl", choices=["nccl", "peer"],
                    help="--parallel ep data exchange: NCCL all-to-all or the epilogue-fused "
                         "peer-memory path (CUDA IPC / NVLink mappings)")
+    p.add_argument("--no-north-star", action="store_true",
+                   help="skip the base-128 grouped-FFN roofline measurement")
     p.add_argument("--no-streaming", action="store_true",
                    help="skip the H2D-link / budget-limited streaming measurement")
     return p.parse_args()
@@ -289,6 +291,59 @@ def measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms, steps=3,
                     "reloads about (all - slots) experts, issued one layer ahead"}
 
 
+def measure_ffn_shape(experts: int, n_tok: int, peaks: dict, iters: int = 10) -> dict:
+    """One Switch-shaped MoE layer with `experts` experts at `n_tok` tokens
+    (uniform random routing, every expert resident): the grouped FFN (GEMM1 +
+    GEMM2) timed with CUDA events on the launching stream against SURVEY
+    §8(d)'s roofline max(4 d h N / bf16 sustained, min bytes / HBM)."""
+    import torch
+
+    from paper_2310_18859_b200 import MoEConfig, MoEModel
+    from paper_2310_18859_b200.offload import ExpertStore, Wave, run_waves
+    from paper_2310_18859_b200.predictor import DeviceTable
+
+    cfg = MoEConfig(**dict(BASE8, num_layers=1, num_experts=experts, vocab_size=64,
+                           max_seq_len=16))
+    model = MoEModel.synthetic(cfg, 0)
+    store = ExpertStore.full(model)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(3)  # SURVEY §8(d): balanced synthetic ids, seed 3
+    ids = torch.randint(0, experts, (1, n_tok, 1), device="cuda", dtype=torch.int32, generator=g)
+    al = torch.rand((1, n_tok, 1), device="cuda", dtype=torch.float64, generator=g)
+    dt = DeviceTable(ids, al, al.float(), n_tok, 1)
+    st = torch.cuda.current_stream()
+    dt.permute(experts, st)
+    x = torch.randn(n_tok, cfg.d_model, device="cuda", generator=g)
+    torch.cuda.synchronize()
+    hist = dt.hist.cpu().numpy()[0]
+    store.run_layer(model, 0, x, dt)
+    need = [int(e) for e in np.nonzero(hist)[0]]
+    wave = Wave(0, [], need, store.slot_row(0, need))
+    for _ in range(3):
+        run_waves(model, [wave], x, dt, store, st)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(iters):
+        run_waves(model, [wave], x, dt, store, st)
+    e1.record(st)
+    torch.cuda.synchronize()
+    avg_ms = e0.elapsed_time(e1) / iters
+    d_, h_ = cfg.d_model, cfg.expert_hidden
+    flops = 4.0 * n_tok * d_ * h_
+    min_bytes = len(need) * (2 * d_ * h_ + h_ + d_) * 2 + 3.0 * n_tok * d_ * 2
+    t_tensor = flops / (peaks.get("bf16_tflops_sustained", 1373.4) * 1e12) * 1e3
+    t_hbm = min_bytes / (peaks.get("hbm_gbs", 6549.4) * 1e9) * 1e3
+    out = {"experts": experts, "tokens": n_tok, "rows_per_expert": n_tok / experts,
+           "avg_ms": avg_ms, "tflops": flops / (avg_ms / 1e3) / 1e12,
+           "tensor_ms": t_tensor, "hbm_ms": t_hbm,
+           "bound": "tensor" if t_tensor >= t_hbm else "hbm",
+           "frac": max(t_tensor, t_hbm) / avg_ms}
+    del model, store, dt, x
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -445,6 +500,14 @@ def run_ours(args):
         cpu = {"value": rate, "unit": "tokens/s", "cores": os.cpu_count(),
                "blas_threads": blas_threads(), "kind": "port",
                "sample": detail + f" ({work:.1f} s of CPU work)"}
+    # ---- north-star target (BASELINE.json: Switch-base-128 grouped FFN at
+    # >= 70 % of its roofline on one B200): one base-128 layer at the bench
+    # batch (32K tokens, ~256 rows per expert: at the HBM/tensor ridge) and at
+    # 1024 x 128 tokens per batch
+    north = None
+    if rank == 0 and ws == 1 and not args.no_north_star:
+        north = {"target_frac": 0.70,
+                 "shapes": [measure_ffn_shape(128, n, peaks) for n in (32768, 131072)]}
     footprint = engine.store.peak_slots * eb
     line = {
         "metric": "MoE inference tokens/sec (SiDA serving, base-8)",
@@ -478,6 +541,7 @@ def run_ours(args):
                      "avg_ms": ffn_avg_ms,
                      "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms if ffn_avg_ms else None,
                      "attention_mix_avg_ms": float(np.mean(mix_ms)) if mix_ms else None},
+        "north_star_ffn": north,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": n_tok * 4 + (B + 1) * 4,
                 "d2h_bytes_per_step": B * cfg.num_classes * 4 + cfg.num_layers * cfg.num_experts * 4,

@@ -161,7 +161,9 @@ int sida_debug_gemm_prof(unsigned long long* out);
 /* Expert-FFN tile family for sida_grouped_ffn_bf16: -1 auto, 0 token-M
  * tiles for both GEMMs (128/256 token rows x BN features), 1 token-N tiles
  * for both (swap-AB: 256 features x 16..256 token rows in steps of 16),
- * 2 token-M GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2.
+ * 2 token-M GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2,
+ * 4 both GEMMs fused per <= 128-row token tile with the bf16 hidden kept in
+ * shared memory (d % 256 == 0, d <= 768; otherwise as 1).
  * Process-wide; the initial value comes from SIDA_FFN_SWAP.
  * sida_get_ffn_tiles returns the current mode. */
 int sida_set_ffn_tiles(int mode);

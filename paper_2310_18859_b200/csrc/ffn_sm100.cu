@@ -852,6 +852,377 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
   }
 }
 
+// ------------------------------------------------------------ fused FFN (token-N)
+// Both expert GEMMs of a token tile in one CTA pair, the hidden activations
+// never leaving the SMs. Work item = (expert, tile of <= 128 of its rows).
+// For every 256-wide slice c of h:
+//   GEMM1(c): acc1 (TMEM, 256 h-features x N tokens, M = 256 per pair) =
+//             W1^T[c] X^T over K = d (weights and token rows streamed by TMA)
+//   epi1(c):  relu(acc1 + b1) -> bf16, written by the epilogue warps straight
+//             into the SW128 K-major B-operand layout of GEMM2 in shared
+//             memory (token rows split between the two CTAs: half of every
+//             warp's stores go to the peer over DSMEM), double-buffered
+//   GEMM2(c): out (TMEM, d x N, d/256 accumulators) += W2^T[:, c] H[c]^T
+// MMA order G1(c), G2(c-1), G1(c+1), ...: epi1(c) overlaps G2(c-1), so the
+// single acc1 buffer never stalls the tensor core. After the last slice the
+// epilogue applies b2, alpha, the residual and the unpermute (row_map) as
+// the token-N GEMM2 epilogue does. HBM traffic = weights + x + residual +
+// outputs (no hidden round trip: 2 x N x h x 2 bytes per layer saved).
+// TMEM: d/256 accumulators of 128 columns + acc1 (128 columns) <= 512, so
+// d <= 768.
+constexpr int kFxTok = 128;                    // max tokens per item (UMMA N)
+constexpr int kFxStages = 6;
+constexpr uint32_t kFxW = 128 * BK * 2;        // weight slice per CTA per stage (16 KB)
+constexpr uint32_t kFxX = 64 * BK * 2;         // token slice per CTA per stage (8 KB)
+constexpr uint32_t kFxStage = kFxW + kFxX;
+constexpr uint32_t kFxHid = 4 * 64 * 128;      // hidden slice per CTA: 4 k-blocks x 64 rows
+
+__device__ __forceinline__ void fx_split(int R, int& base, int& count) {
+  if (R <= 0) { base = 16; count = 0; return; }
+  const int n = ceil_div(R, kFxTok);
+  base = min(kFxTok, (ceil_div(R, n) + 15) & ~15);
+  count = ceil_div(R, base);
+}
+
+struct FxParams {
+  int n_rows, d, h;
+  const int32_t* off;
+  int num_experts;
+  const int32_t* expert_slot;
+  const int32_t* expert_list;
+  int n_list;
+  const uint8_t* arena;
+  size_t slot_stride, b1_off, b2_off;
+  const int32_t* row_map;
+  const float* alpha;
+  const float* resid;
+  float* out;
+  uint16_t* out_bf16;
+  int32_t* err_flag;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+fused_ffn_tn_kernel(const __grid_constant__ CUtensorMap tmW1,  // (d, h, slot), box 64x128
+                    const __grid_constant__ CUtensorMap tmW2,  // (h, d, slot), box 64x128
+                    const __grid_constant__ CUtensorMap tmX,   // (d, rows), box 64x64
+                    const FxParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sStage = smem;
+  uint8_t* sHid = smem + kFxStages * kFxStage;  // 2 buffers
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sHid + 2 * kFxHid);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kFxStages;
+  uint64_t* acc1_full = bars + 2 * kFxStages;
+  uint64_t* acc1_empty = acc1_full + 1;
+  uint64_t* hid_full = acc1_empty + 1;   // [2]
+  uint64_t* hid_empty = hid_full + 2;    // [2]
+  uint64_t* out_full = hid_empty + 2;
+  uint64_t* out_empty = out_full + 1;
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(out_empty + 1);
+  int32_t* s_prefix = reinterpret_cast<int32_t*>(s_tmem + 4);
+  int32_t* s_expert = s_prefix + kMaxListed + 1;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_list = p.expert_list ? p.n_list : p.num_experts;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int unit = blockIdx.x >> 1, n_units = gridDim.x >> 1;
+  const int n_c = p.h / 256, n_dt = p.d / 256, n_kd = p.d / BK;
+
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int i = 0; i < n_list; ++i) {
+      const int e = p.expert_list ? p.expert_list[i] : i;
+      const int R = (p.off[e + 1] - p.off[e]);
+      int base, cnt;
+      fx_split(R, base, cnt);
+      s_expert[i] = e;
+      s_prefix[i] = acc;
+      acc += cnt;
+    }
+    s_prefix[n_list] = acc;
+    for (int i = 0; i < kFxStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(acc1_full, 1);
+    mbar_init(acc1_empty, 2 * kEpiWarps);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&hid_full[i], 2 * kEpiWarps);
+      mbar_init(&hid_empty[i], 1);
+    }
+    mbar_init(out_full, 1);
+    mbar_init(out_empty, 2 * kEpiWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW1)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW2)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(s_tmem)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+  const uint32_t acc1_col = 384;  // out accumulators at columns 0, 128, 256
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  const int total = s_prefix[n_list];
+  auto get_item = [&](int it, int& row0, int& nrows, int& slot) {
+    int lo = 0, hi = n_list - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_prefix[mid] <= it) lo = mid; else hi = mid - 1;
+    }
+    const int e = s_expert[lo];
+    const int seg0 = p.off[e];
+    const int R = p.off[e + 1] - seg0;
+    int base, cnt;
+    fx_split(R, base, cnt);
+    const int j = it - s_prefix[lo];
+    row0 = seg0 + j * base;
+    nrows = min(base, R - j * base);
+    slot = p.expert_slot[e];
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      auto next_stage = [&]() {
+        if (++stage == kFxStages) { stage = 0; phase ^= 1; }
+      };
+      for (int it = unit; it < total; it += n_units) {
+        int row0, nrows, slot;
+        get_item(it, row0, nrows, slot);
+        if (slot < 0) continue;
+        const int half = ((nrows + 15) & ~15) >> 1;
+        const int xrow = row0 + static_cast<int>(rank) * half;
+        for (int c = 0; c <= n_c; ++c) {
+          if (c < n_c) {  // GEMM1(c): W1^T rows c*256 + rank*128, token rows
+            for (int kb = 0; kb < n_kd; ++kb) {
+              mbar_wait(&empty[stage], phase ^ 1);
+              const uint32_t fb = map_rank(smem_u32(&full[stage]), 0);
+              if (leader) mbar_expect_tx(&full[stage], 2 * kFxStage);
+              uint8_t* st = sStage + stage * kFxStage;
+              tma_load_3d<2>(st, &tmW1, kb * BK, c * 256 + rank * 128, slot, fb);
+              tma_load_2d<2>(st + kFxW, &tmX, kb * BK, xrow, fb);
+              next_stage();
+            }
+          }
+          if (c > 0) {  // GEMM2(c-1): W2^T rows mt*256 + rank*128, h cols (c-1)*256 + kb*64
+            for (int mt = 0; mt < n_dt; ++mt)
+              for (int kb = 0; kb < 4; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                const uint32_t fb = map_rank(smem_u32(&full[stage]), 0);
+                if (leader) mbar_expect_tx(&full[stage], 2 * kFxW);
+                tma_load_3d<2>(sStage + stage * kFxStage, &tmW2, (c - 1) * 256 + kb * BK,
+                               mt * 256 + rank * 128, slot, fb);
+                next_stage();
+              }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader CTA, one lane)
+    if (lane == 0 && leader) {
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t u_acc1 = 0, u_hid[2] = {0, 0}, u_out = 0;
+      for (int it = unit; it < total; it += n_units) {
+        int row0, nrows, slot;
+        get_item(it, row0, nrows, slot);
+        if (slot < 0) {
+          atomicExch(p.err_flag, 1);
+          continue;
+        }
+        const uint32_t idesc = idesc_bf16_rt(256, (nrows + 15) & ~15);
+        for (int c = 0; c <= n_c; ++c) {
+          if (c < n_c) {
+            mbar_wait_cluster(acc1_empty, (u_acc1 & 1) ^ 1);
+            ++u_acc1;
+            tc_fence_after();
+            for (int kb = 0; kb < n_kd; ++kb) {
+              mbar_wait(&full[stage], phase);
+              tc_fence_after();
+              const uint32_t a0 = smem_u32(sStage + stage * kFxStage);
+              const uint32_t b0 = a0 + kFxW;
+#pragma unroll
+              for (int k = 0; k < BK / UMMA_K; ++k)
+                umma_bf16<2>(tmem_base + acc1_col, sw128_desc(a0 + k * UMMA_K * 2),
+                             sw128_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0);
+              tc_commit<2>(&empty[stage]);
+              if (++stage == kFxStages) { stage = 0; phase ^= 1; }
+            }
+            tc_commit<2>(acc1_full);
+          }
+          if (c > 0) {
+            const int cc = c - 1, buf = cc & 1;
+            mbar_wait_cluster(&hid_full[buf], u_hid[buf] & 1);
+            ++u_hid[buf];
+            if (cc == 0) {
+              mbar_wait_cluster(out_empty, (u_out & 1) ^ 1);
+              ++u_out;
+            }
+            tc_fence_after();
+            const uint32_t hb = smem_u32(sHid + buf * kFxHid);
+            for (int mt = 0; mt < n_dt; ++mt)
+              for (int kb = 0; kb < 4; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(sStage + stage * kFxStage);
+#pragma unroll
+                for (int k = 0; k < BK / UMMA_K; ++k)
+                  umma_bf16<2>(tmem_base + mt * 128, sw128_desc(a0 + k * UMMA_K * 2),
+                               sw128_desc(hb + kb * 8192 + k * UMMA_K * 2), idesc,
+                               (cc | kb | k) != 0);
+                tc_commit<2>(&empty[stage]);
+                if (++stage == kFxStages) { stage = 0; phase ^= 1; }
+              }
+            tc_commit<2>(&hid_empty[buf]);
+          }
+        }
+        tc_commit<2>(out_full);
+      }
+    }
+  } else {
+    // ===== epilogue warps (both CTAs): quarter q = TMEM lanes 32q.., half hh
+    // = token columns [64 hh, 64 hh + 64)
+    const int q = warp & 3;
+    const int hh = (warp - 2) >> 2;
+    const bool odd = lane & 1;
+    uint32_t u_acc1 = 0, u_hid[2] = {0, 0}, u_out = 0;
+    for (int it = unit; it < total; it += n_units) {
+      int row0, nrows, slot;
+      get_item(it, row0, nrows, slot);
+      if (slot < 0) continue;
+      const int nmma = (nrows + 15) & ~15;
+      const int half = nmma >> 1;
+      const int nch = ceil_div(nmma, 32);
+      const uint8_t* sbase = p.arena + static_cast<size_t>(slot) * p.slot_stride;
+      const uint16_t* b1 = reinterpret_cast<const uint16_t*>(sbase + p.b1_off);
+      const uint16_t* b2 = reinterpret_cast<const uint16_t*>(sbase + p.b2_off);
+      const int f_loc = static_cast<int>(rank) * 128 + q * 32 + lane;  // within a 256 slice
+      const int kb2 = f_loc >> 6;
+      const int fin = f_loc & 63;
+      for (int c = 0; c < n_c; ++c) {
+        const int buf = c & 1;
+        const float bias = bf16_to_f32(b1[c * 256 + f_loc]);
+        mbar_wait(acc1_full, u_acc1 & 1);
+        ++u_acc1;
+        tc_fence_after();
+        uint32_t v[2][32];
+        const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc1_col;
+        const int c0 = hh * 2;
+        if (c0 < nch) tmem_ld32_nowait(t_lane + c0 * 32, v[0]);
+        if (c0 + 1 < nch) tmem_ld32_nowait(t_lane + (c0 + 1) * 32, v[1]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        // TMEM reads are ordered by the tcgen05 fence: a plain arrive (a
+        // .release.cluster one would first drain this warp's pending stores)
+        if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(acc1_empty), 0));
+        // hidden buffer `buf` free (GEMM2(c-2) done reading it)
+        mbar_wait(&hid_empty[buf], (u_hid[buf] & 1) ^ 1);
+        ++u_hid[buf];
+        const uint32_t hbuf = smem_u32(sHid + buf * kFxHid) + kb2 * 8192;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          if (c0 + i >= nch) break;
+#pragma unroll
+          for (int j = 0; j < 32; j += 2) {
+            const float y0 = fmaxf(__uint_as_float(v[i][j]) + bias, 0.f);
+            const float y1 = fmaxf(__uint_as_float(v[i][j + 1]) + bias, 0.f);
+            const float other = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
+            const uint32_t w = odd ? bf16x2_rn(other, y1) : bf16x2_rn(y0, other);
+            const int tcol = (c0 + i) * 32 + j + (odd ? 1 : 0);
+            if (tcol < nmma) {
+              const int dst = tcol >= half ? 1 : 0;
+              const int r = tcol - dst * half;
+              const int fe = fin & ~1;
+              const uint32_t a = hbuf + r * 128 + ((((fe >> 3) ^ (r & 7))) << 4) + (fe & 7) * 2;
+              asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(map_rank(a, dst)), "r"(w)
+                           : "memory");
+            }
+          }
+        }
+        // the DSMEM stores -> the tensor core's (async proxy) reads of both CTAs
+        asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(&hid_full[buf]), 0));
+      }
+      // ---- output: alpha (acc + b2) + resid, unpermuted (as the token-N GEMM2)
+      mbar_wait(out_full, u_out & 1);
+      ++u_out;
+      tc_fence_after();
+      const int nv = ceil_div(nrows, 32);
+      for (int mt = 0; mt < n_dt; ++mt) {
+        const int f = mt * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
+        const float bias = bf16_to_f32(b2[f]);
+        for (int ch = hh; ch < nv; ch += 2) {
+          uint32_t v[32];
+          tmem_ld32_nowait(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + mt * 128 + ch * 32,
+                           v);
+          const int tok0 = row0 + ch * 32;
+          const int cnt = min(32, nrows - ch * 32);
+          const int my_tok = tok0 + lane;
+          int orow_l = my_tok;
+          float a_l = 1.f;
+          if (lane < cnt) {
+            if (p.row_map) orow_l = p.row_map[my_tok];
+            if (p.alpha) a_l = p.alpha[my_tok];
+          }
+          float x[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int o = __shfl_sync(0xffffffffu, orow_l, j);
+            x[j] = (p.resid && j < cnt) ? __ldg(p.resid + static_cast<size_t>(o) * p.d + f) : 0.f;
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int o = __shfl_sync(0xffffffffu, orow_l, j);
+            const float a = __shfl_sync(0xffffffffu, a_l, j);
+            if (j < cnt) {
+              const float y = x[j] + (__uint_as_float(v[j]) + bias) * a;
+              const size_t at = static_cast<size_t>(o) * p.d + f;
+              if (p.out) p.out[at] = y;
+              if (p.out_bf16) p.out_bf16[at] = __bfloat16_as_ushort(__float2bfloat16_rn(y));
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(out_empty), 0));
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(512));
+  }
+}
+
+constexpr size_t fx_smem_bytes() {
+  return 1024 + kFxStages * kFxStage + 2 * kFxHid + (2 * kFxStages + 8) * 8 + 16 +
+         (2 * kMaxListed + 2) * 4;
+}
+
 constexpr size_t tn_smem_bytes() {
   return 1024 + kTnStages * (128 * BK * 2 + (kTnMax / 2) * BK * 2) + (2 * kTnStages + 4) * 8 + 16 +
          (2 * kMaxListed + 2) * 4;
@@ -1026,6 +1397,42 @@ static int launch_tn(const void* x_base, const void* w_base, int n_slots, const 
   return SIDA_OK;
 }
 
+// Fused token-N FFN launch (both GEMMs, hidden kept on chip).
+static int launch_fx(const void* x_perm, const uint8_t* arena, int n_slots, const FxParams& p,
+                     int n_listed, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    SIDA_CUDA(cudaFuncSetAttribute(fused_ffn_tn_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)fx_smem_bytes()));
+    configured = true;
+  }
+  const size_t w2_off = (size_t)p.h * p.d * 2;
+  CUtensorMap tw1, tw2, tx;
+  int st = make_map_3d(&tw1, arena, p.d, p.h, n_slots, p.slot_stride, 128);
+  if (st) return st;
+  if ((st = make_map_3d(&tw2, arena + w2_off, p.h, p.d, n_slots, p.slot_stride, 128))) return st;
+  if ((st = make_map_2d(&tx, x_perm, p.d, p.n_rows, 64))) return st;
+  const int max_items = ceil_div(p.n_rows, kFxTok) + n_listed;
+  const int units = std::max(1, std::min(max_items, kNumSMs / 2));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(units * 2);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = fx_smem_bytes();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  SIDA_CUDA(cudaLaunchKernelEx(&cfg, fused_ffn_tn_kernel, tw1, tw2, tx, p));
+  return SIDA_OK;
+}
+
 // CTA-pair (M=256) tiles when experts hold enough rows to fill them.
 template <int STAGE>
 static int dispatch_gemm(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
@@ -1100,13 +1507,21 @@ static bool choose_tn(int gemm, int n_rows, int listed, int d, int h) {
     case 1: return true;
     case 2: return gemm == 2;
     case 3: return gemm == 1;
+    case 4: return true;  // (when the fused launch does not apply)
     default: break;
   }
   return gemm == 2 && n_rows >= g_tn_lo * listed && n_rows < g_tn_hi * listed;
 }
 
+// Mode 4: both GEMMs fused per token tile (fused_ffn_tn_kernel), d <= 768.
+static bool choose_fx(int n_rows, int listed, int d, int h) {
+  tn_init();
+  (void)n_rows; (void)listed;
+  return g_tn_mode == 4 && d % 256 == 0 && d <= 768 && h % 256 == 0;
+}
+
 extern "C" int sida_set_ffn_tiles(int mode) {
-  SIDA_REQUIRE(mode >= -1 && mode <= 3, SIDA_ERR_CONTRACT, "ffn tile mode %d not in -1..3", mode);
+  SIDA_REQUIRE(mode >= -1 && mode <= 4, SIDA_ERR_CONTRACT, "ffn tile mode %d not in -1..4", mode);
   tn_init();
   g_tn_mode = mode;
   return SIDA_OK;
@@ -1141,6 +1556,17 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   const uint8_t* ar = static_cast<const uint8_t*>(arena);
   const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
   const int cg = choose_cg(n_rows, listed);
+
+  if (choose_fx(n_rows, listed, d, h)) {
+    sm100::FxParams f{};
+    f.n_rows = n_rows; f.d = d; f.h = h;
+    f.off = off; f.num_experts = num_experts; f.expert_slot = expert_slot;
+    f.expert_list = expert_list; f.n_list = n_list;
+    f.arena = ar; f.slot_stride = slot_stride; f.b1_off = b1_off; f.b2_off = b2_off;
+    f.row_map = row_map; f.alpha = alpha; f.resid = resid; f.out = out; f.out_bf16 = out_bf16;
+    f.err_flag = err_flag;
+    return sm100::launch_fx(x_perm, ar, n_slots, f, listed, s);
+  }
 
   sm100::GemmParams p1{};
   p1.n_rows = n_rows; p1.kdim = d; p1.ndim = h;

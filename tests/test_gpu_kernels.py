@@ -152,15 +152,15 @@ def ffn_tiles():
     _l.check(h.sida_set_ffn_tiles(prev))
 
 
-@pytest.mark.parametrize("tiles", [-1, 0, 1, 2, 3])
+@pytest.mark.parametrize("tiles", [-1, 0, 1, 2, 3, 4])
 @pytest.mark.parametrize("d,hdim,K,N,k", [
     (64, 128, 4, 300, 1), (256, 1024, 8, 1024, 1), (768, 3072, 8, 2048, 1),
     (128, 256, 8, 700, 2), (768, 3072, 4, 257, 3), (256, 1024, 32, 1500, 1),
     (768, 3072, 64, 6000, 1), (512, 1024, 16, 900, 2)])
 def test_grouped_ffn_bf16_vs_oracle(cuda_device, ffn_tiles, tiles, d, hdim, K, N, k):
     """tiles: -1 auto, 0 token-M (128/256-row token tiles), 1 token-N
-    (swap-AB: 256 features x 16..256 tokens), 2/3 mixed per GEMM; token-N
-    needs d, h % 256."""
+    (swap-AB: 256 features x 16..256 tokens), 2/3 mixed per GEMM, 4 fused
+    per token tile (hidden on chip); token-N needs d, h % 256."""
     from paper_2310_18859_b200.offload import ExpertStore
     from paper_2310_18859_b200.predictor import ExpertHashTable
 
@@ -474,7 +474,7 @@ def test_ffn_token_n_tiles_match_token_m_tiles(cuda_device, ffn_tiles, K, N, ske
     dt = ExpertHashTable(0, [N], ids, alphas).on_device(model)
     store = ExpertStore.full(model)
     outs = []
-    for mode in (0, 1, 2, 3):
+    for mode in (0, 1, 2, 3, 4):
         ffn_tiles(mode)
         ob = torch.empty((N, d), dtype=torch.bfloat16, device="cuda")
         outs.append((store.run_layer(model, 0, x, dt, out_bf16=ob), ob))
