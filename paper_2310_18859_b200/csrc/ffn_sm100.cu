@@ -1470,26 +1470,31 @@ extern "C" int sida_debug_gemm_prof(unsigned long long* out) {
   return SIDA_OK;
 }
 
-// CTA-group choice: SIDA_FFN_CG=1|2 forces it; default pairs (M=256 tiles)
-// once the average expert holds >= 1024 rows (padding waste < 1/8).
-static int choose_cg(int n_rows, int listed) {
+// CTA-group choice per GEMM: SIDA_FFN_CG=1|2 forces it; by default GEMM1
+// (K = d: short k-loop) pairs up (M=256 tiles) once the average expert holds
+// >= 1024 rows, GEMM2 (K = h) already at >= 192 rows: its pair tiles halve
+// the weight re-reads, which outweighs their padding down to ~256 rows per
+// expert (ncu, profiles/r1/ffn_tile_families.txt: base-128 GEMM2 197 vs
+// 220 us, base-64 164 vs 177 us; at 128 rows both are equal).
+static int choose_cg(int gemm, int n_rows, int listed) {
   static int forced = -1;
   if (forced < 0) {
     const char* e = getenv("SIDA_FFN_CG");
     forced = e ? atoi(e) : 0;
   }
   if (forced == 1 || forced == 2) return forced;
-  return n_rows >= 1024 * listed ? 2 : 1;
+  return n_rows >= (gemm == 1 ? 1024 : 192) * listed ? 2 : 1;
 }
 
 // Tile family per expert GEMM (sida_set_ffn_tiles, or SIDA_FFN_SWAP at load):
 // -1 auto, 0 token-M for both GEMMs, 1 token-N (swap-AB) for both, 2 token-M
-// GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2. Auto picks token-N
-// per GEMM where it measured faster (tools/ffn_probe.py, profiles/r1): only
-// GEMM2 (K = h: long k-loop, fp32 residual epilogue) and only while the
-// listed experts average [SIDA_FFN_SWAP_LO, SIDA_FFN_SWAP_HI) rows.
+// GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2, 4 fused. Auto is
+// token-M with the per-GEMM CTA-group choice above, which measured fastest
+// everywhere (profiles/r1/ffn_tile_families.txt); token-N is used in auto
+// mode only inside [SIDA_FFN_SWAP_LO, SIDA_FFN_SWAP_HI) rows per expert for
+// GEMM2 (empty by default).
 static int g_tn_mode = -2;
-static int g_tn_lo = 192, g_tn_hi = 384;
+static int g_tn_lo = 0, g_tn_hi = 0;
 
 static void tn_init() {
   if (g_tn_mode != -2) return;
@@ -1555,7 +1560,6 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   cudaStream_t s = as_stream(stream);
   const uint8_t* ar = static_cast<const uint8_t*>(arena);
   const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
-  const int cg = choose_cg(n_rows, listed);
 
   if (choose_fx(n_rows, listed, d, h)) {
     sm100::FxParams f{};
@@ -1575,7 +1579,8 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
   p1.hidden = hidden; p1.err_flag = err_flag; p1.prof = prof_buffer(0);
   int st = choose_tn(1, n_rows, listed, d, h) ? sm100::launch_tn<1>(x_perm, ar, n_slots, p1, listed, s)
-              : sm100::dispatch_gemm<1>(x_perm, ar, n_slots, p1, listed, cg, s);
+              : sm100::dispatch_gemm<1>(x_perm, ar, n_slots, p1, listed,
+                                        choose_cg(1, n_rows, listed), s);
   if (st) return st;
 
   sm100::GemmParams p2 = p1;
@@ -1584,7 +1589,8 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   p2.out_bf16 = out_bf16;
   p2.prof = prof_buffer(1);
   if (choose_tn(2, n_rows, listed, d, h)) return sm100::launch_tn<2>(hidden, ar + w2_off, n_slots, p2, listed, s);
-  return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, listed, cg, s);
+  return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, listed,
+                                 choose_cg(2, n_rows, listed), s);
 }
 
 // Mixing-attention output projection with the residual and the next FFN's
@@ -1652,6 +1658,7 @@ extern "C" int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, i
   if (n_rows == 0 || listed == 0) return SIDA_OK;
   cudaStream_t s = as_stream(stream);
   SIDA_CUDA(cudaMemsetAsync(mflags, 0, sida_ffn_flags_count(n_rows, listed) * sizeof(int32_t), s));
+  const int cg = choose_cg(1, n_rows, listed);  // one tile shape for both interleaved GEMMs
   const uint8_t* ar = static_cast<const uint8_t*>(arena);
   const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
   sm100::GemmParams p1{};
@@ -1664,7 +1671,6 @@ extern "C" int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, i
   p2.kdim = h; p2.ndim = d; p2.bias_off = b2_off;
   p2.row_map = row_map; p2.alpha = alpha; p2.resid = resid; p2.out = out;
   p2.out_bf16 = out_bf16;
-  const int cg = choose_cg(n_rows, listed);
   if (cg == 2)
     return sm100::launch_gemm<256, 3, 2>(x_perm, ar, n_slots, p1, listed, s, hidden, ar + w2_off,
                                          &p2, mflags, lag);
@@ -1727,16 +1733,17 @@ extern "C" int sida_grouped_ffn_bf16_peer(const uint16_t* x_loc, int n_rows, int
   cudaStream_t s = as_stream(stream);
   const uint8_t* ar = static_cast<const uint8_t*>(arena);
   const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
-  const int cg = choose_cg(n_rows, num_experts);
   sm100::GemmParams p1{};
   p1.n_rows = n_rows; p1.kdim = d; p1.ndim = h;
   p1.off = off; p1.num_experts = num_experts; p1.expert_slot = expert_slot;
   p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
   p1.hidden = hidden; p1.err_flag = err_flag;
-  int st = sm100::dispatch_gemm<1>(x_loc, ar, n_slots, p1, num_experts, cg, s);
+  int st = sm100::dispatch_gemm<1>(x_loc, ar, n_slots, p1, num_experts,
+                                   choose_cg(1, n_rows, num_experts), s);
   if (st) return st;
   sm100::GemmParams p2 = p1;
   p2.kdim = h; p2.ndim = d; p2.bias_off = b2_off;
   p2.row_map = row_map; p2.peer_bf16 = peers; p2.peer_stride = peer_stride;
-  return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, num_experts, cg, s);
+  return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, num_experts,
+                                 choose_cg(2, n_rows, num_experts), s);
 }
