@@ -1173,8 +1173,108 @@ static int lstm_dispatch(const double* xw, const double* tokx, const double* pos
   return launch_lstm<64, FOLD>(xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out, s, max_len, c_buf);
 }
 
+// C (N x M) = A (N x Kd) @ B (Kd x M), fp64 on the FP64 tensor cores (DMMA
+// m8n8k4). CTA = 64 rows x all M (<= 192) columns, 8 warps: warp w owns rows
+// 16 (w % 4) .. +15 (two 8-row m-tiles) and n-tiles 12 (w / 4) .. +11, i.e.
+// 24 DMMA accumulators (48 doubles) per thread. A and B are staged in shared
+// memory zero-padded to k % 4 == 0 and n % 8 == 0, with row strides = 4 mod
+// 16 doubles so every fragment load is conflict-free (each 16-lane half hits
+// 16 distinct double banks).
+constexpr int kDR_Rows = 64;
+constexpr int kDR_MaxK = 48, kDR_MaxM = 192;
+
+__device__ __forceinline__ int dr_stride(int v) { return (v + 11) / 16 * 16 + 4; }  // >= v, = 4 mod 16
+
+__global__ void __launch_bounds__(256)
+rows_dmma_kernel(const double* __restrict__ A, int n_rows, int Kd, const double* __restrict__ B,
+                 int M, double* __restrict__ C) {
+  extern __shared__ double smem_d[];
+  const int KP = (Kd + 3) & ~3, MP = (M + 7) & ~7;
+  const int SA = dr_stride(KP), SB = dr_stride(MP);
+  double* s_a = smem_d;                   // kDR_Rows x SA
+  double* s_b = smem_d + kDR_Rows * SA;   // KP x SB
+  const int r0 = blockIdx.x * kDR_Rows;
+  for (int i = threadIdx.x; i < KP * MP; i += blockDim.x) {
+    const int k = i / MP, c = i - k * MP;
+    s_b[k * SB + c] = (k < Kd && c < M) ? B[(size_t)k * M + c] : 0.0;
+  }
+  for (int i = threadIdx.x; i < kDR_Rows * KP; i += blockDim.x) {
+    const int r = i / KP, k = i - r * KP;
+    s_a[r * SA + k] = (r0 + r < n_rows && k < Kd) ? A[(size_t)(r0 + r) * Kd + k] : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int m0 = (warp & 3) * 16;
+  const int nt0 = (warp >> 2) * 12;
+  const int n_nt = min(12, max(0, MP / 8 - nt0));
+  if (n_nt == 0) return;
+  double acc[2][12][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 12; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int k0 = 0; k0 < KP; k0 += 4) {
+    const double a0 = s_a[(m0 + g) * SA + k0 + t];
+    const double a1 = s_a[(m0 + 8 + g) * SA + k0 + t];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      if (j < n_nt) {
+        const double b = s_b[(k0 + t) * SB + (nt0 + j) * 8 + g];
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[0][j][0]), "+d"(acc[0][j][1])
+                     : "d"(a0), "d"(b));
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                     : "+d"(acc[1][j][0]), "+d"(acc[1][j][1])
+                     : "d"(a1), "d"(b));
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int r = r0 + m0 + i * 8 + g;
+    if (r >= n_rows) continue;
+#pragma unroll
+    for (int j = 0; j < 12; ++j) {
+      if (j >= n_nt) continue;
+      const int c = (nt0 + j) * 8 + 2 * t;
+      double* dst = C + (size_t)r * M + c;
+      if (c + 1 < M && (M & 1) == 0) {
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else {
+        if (c < M) dst[0] = acc[i][j][0];
+        if (c + 1 < M) dst[1] = acc[i][j][1];
+      }
+    }
+  }
+}
+
+// SIDA_HASH_DMMA=0: the CUDA-core fp64 kernel below (A/B switch)
+static int use_dmma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SIDA_HASH_DMMA");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 static int rows_gemm(const double* A, int n, int Kd, const double* B, int M, double* C,
                      cudaStream_t s) {
+  if (use_dmma() && Kd <= kDR_MaxK && M <= kDR_MaxM) {
+    const int KP = (Kd + 3) & ~3, MP = (M + 7) & ~7;
+    const int SA = (KP + 11) / 16 * 16 + 4, SB = (MP + 11) / 16 * 16 + 4;
+    const size_t smem = ((size_t)kDR_Rows * SA + (size_t)KP * SB) * sizeof(double);
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+      SIDA_CUDA(cudaFuncSetAttribute(rows_dmma_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      configured = smem;
+    }
+    rows_dmma_kernel<<<ceil_div(n, kDR_Rows), 256, smem, s>>>(A, n, Kd, B, M, C);
+    SIDA_LAUNCH_CHECK();
+    return SIDA_OK;
+  }
   SIDA_REQUIRE(M >= 1 && M <= 192, SIDA_ERR_UNSUPPORTED, "rows_gemm width %d", M);
   const size_t smem = ((size_t)Kd * M + (size_t)kRG_Rows * (Kd + 1)) * sizeof(double);
   static size_t configured = 0;
