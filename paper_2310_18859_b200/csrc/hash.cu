@@ -679,7 +679,9 @@ attn_heads_kernel(const AttnArgs a) {
 // The arithmetic per element is the same as attn_heads_kernel; only the
 // schedule changes (independent accumulators instead of dependent chains).
 constexpr int kBT = 128;       // key / logit chunk
-constexpr int kQP = 49;        // pitch (doubles) of Q / K / R rows
+constexpr int kQP = 52;        // pitch (doubles) of Q / K / R rows (= 4 mod 16: DMMA
+                               // fragment loads are bank-conflict free)
+constexpr int kWP = kBT + 4;   // pitch of the staged head-weight rows (= 4 mod 16)
 constexpr int kMaxBlockTop = 8;                    // eval_top_k of the blocked path
 constexpr int kStatePitch = 2 + 2 * kMaxBlockTop;   // online heads state per row
 template <int BR, int TMAX>
@@ -691,6 +693,48 @@ struct BlockArgs {
   AttnArgs a;
   const double* hwp;  // heads packed (H, L*K): hwp[i][l*K + e] = head_w[l][i][e]
 };
+
+__device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// out[BR x 128] (pitch op) = A[BR x KP] (pitch kQP) * B, B(k, n) = Bt[n * bn + k * bk]
+// on the FP64 tensor cores. 8 warps: BR/16 row groups x 128 / (8 * NTW) column
+// groups, NTW 8-wide n-tiles per warp; KP = H rounded up to 4 (zero padded).
+template <int BR>
+__device__ __forceinline__ void block_dmma(const double* __restrict__ sA, const double* __restrict__ sB,
+                                           int bn, int bk, int KP, double* __restrict__ out,
+                                           int op) {
+  constexpr int RG = BR / 16, CG = 8 / RG, NTW = 16 / CG;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int m0 = (warp % RG) * 16, c0 = (warp / RG) * NTW * 8;
+  double acc[2][NTW][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int k0 = 0; k0 < KP; k0 += 4) {
+    const double a0 = sA[(m0 + g) * kQP + k0 + t];
+    const double a1 = sA[(m0 + 8 + g) * kQP + k0 + t];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) {
+      const double b = sB[(c0 + j * 8 + g) * bn + (k0 + t) * bk];
+      dmma_884(acc[0][j][0], acc[0][j][1], a0, b);
+      dmma_884(acc[1][j][0], acc[1][j][1], a1, b);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) {
+      double* o = out + (m0 + i * 8 + g) * op + c0 + j * 8 + 2 * t;
+      o[0] = acc[i][j][0];
+      o[1] = acc[i][j][1];
+    }
+}
 
 template <int BR, int TMAX>
 __global__ void __launch_bounds__(256, 1)
@@ -719,38 +763,20 @@ attn_block_kernel(const BlockArgs ba) {
   const int r0 = (b - a.blk_off[lo]) * BR;
   const int rows = min(T - r0, BR);
 
-  for (int i = tid; i < rows * H; i += 256) {
-    const int r = i / H, c = i % H;
-    sQ[r * kQP + c] = a.qkv[(size_t)(base + r0 + r) * H3 + c];
+  const int KP = (H + 3) & ~3;  // DMMA k extent (columns H..KP-1 zero)
+  for (int i = tid; i < BR * KP; i += 256) {
+    const int r = i / KP, c = i % KP;
+    sQ[r * kQP + c] = (r < rows && c < H) ? a.qkv[(size_t)(base + r0 + r) * H3 + c] : 0.0;
   }
-  // ---- S = Q K^T over key chunks: rows ty*RT + i, columns kc + tx + 16 m (m < 8)
+  // ---- S = Q K^T over key chunks on the FP64 tensor cores (block_dmma)
   for (int kc = 0; kc < T; kc += kBT) {
     const int nk = min(kBT, T - kc);
-    for (int i = tid; i < nk * H; i += 256) {
-      const int j = i / H, c = i % H;
-      sK[j * kQP + c] = a.qkv[(size_t)(base + kc + j) * H3 + H + c];
+    for (int i = tid; i < kBT * KP; i += 256) {
+      const int j = i / KP, c = i % KP;
+      sK[j * kQP + c] = (j < nk && c < H) ? a.qkv[(size_t)(base + kc + j) * H3 + H + c] : 0.0;
     }
     __syncthreads();
-    double acc[RT][8];
-#pragma unroll
-    for (int i = 0; i < RT; ++i)
-#pragma unroll
-      for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
-    for (int c = 0; c < H; ++c) {
-      double q[RT], k[8];
-#pragma unroll
-      for (int i = 0; i < RT; ++i) q[i] = sQ[(ty * RT + i) * kQP + c];
-#pragma unroll
-      for (int m = 0; m < 8; ++m) k[m] = sK[(tx + 16 * m) * kQP + c];
-#pragma unroll
-      for (int i = 0; i < RT; ++i)
-#pragma unroll
-        for (int m = 0; m < 8; ++m) acc[i][m] = fma(q[i], k[m], acc[i][m]);
-    }
-#pragma unroll
-    for (int i = 0; i < RT; ++i)
-#pragma unroll
-      for (int m = 0; m < 8; ++m) sS[(ty * RT + i) * kSP + kc + tx + 16 * m] = acc[i][m];
+    block_dmma<BR>(sQ, sK, kQP, 1, KP, sS + kc, kSP);
     __syncthreads();
   }
 
@@ -847,32 +873,13 @@ attn_block_kernel(const BlockArgs ba) {
       // the (H x ncol) weight slice is staged in the (dead) key buffer
       {
         const double* W = ba.hwp + (size_t)l0 * K + c0;
-        double* sW = sK;  // H x kBT
-        for (int i = tid; i < H * kBT; i += 256) {
+        double* sW = sK;  // KP x kWP (rows H..KP-1 zero)
+        for (int i = tid; i < KP * kBT; i += 256) {
           const int c = i / kBT, j = i % kBT;
-          sW[i] = j < ncol ? __ldg(W + (size_t)c * LK + j) : 0.0;
+          sW[c * kWP + j] = (j < ncol && c < H) ? __ldg(W + (size_t)c * LK + j) : 0.0;
         }
         __syncthreads();
-        double acc[RT][8];
-#pragma unroll
-        for (int i = 0; i < RT; ++i)
-#pragma unroll
-          for (int m = 0; m < 8; ++m) acc[i][m] = 0.0;
-        for (int c = 0; c < H; ++c) {
-          double rr[RT], w[8];
-#pragma unroll
-          for (int i = 0; i < RT; ++i) rr[i] = sQ[(ty * RT + i) * kQP + c];
-#pragma unroll
-          for (int m = 0; m < 8; ++m) w[m] = sW[c * kBT + tx + 16 * m];
-#pragma unroll
-          for (int i = 0; i < RT; ++i)
-#pragma unroll
-            for (int m = 0; m < 8; ++m) acc[i][m] = fma(rr[i], w[m], acc[i][m]);
-        }
-#pragma unroll
-        for (int i = 0; i < RT; ++i)
-#pragma unroll
-          for (int m = 0; m < 8; ++m) sS[(ty * RT + i) * kSP + tx + 16 * m] = acc[i][m];
+        block_dmma<BR>(sQ, sW, 1, kWP, KP, sS, kSP);
       }
       __syncthreads();
       if (K <= 32) {
