@@ -507,7 +507,18 @@ def run_ours(args):
     north = None
     if rank == 0 and ws == 1 and not args.no_north_star:
         north = {"target_frac": 0.70,
-                 "shapes": [measure_ffn_shape(128, n, peaks) for n in (32768, 131072)]}
+                 "shapes": [measure_ffn_shape(128, n, peaks) for n in (32768, 131072)],
+                 "balanced_base8": measure_ffn_shape(8, n_tok, peaks)}
+    # routing the timed FFNs saw (random-init predictor: report the
+    # per-layer histogram; the balanced case is north_star_ffn.balanced_base8)
+    routing = None
+    if not ep_mode and (n_steps in tables):
+        hist = tables[n_steps].on_device(model).hist.cpu().numpy()
+        torch.cuda.synchronize()
+        routing = {"source": "random-init predictor (Rng(1)), last hashed batch",
+                   "hist_per_layer": hist.tolist(),
+                   "max_over_mean_per_layer": [round(float(h.max() / max(h.mean(), 1e-9)), 3)
+                                               for h in hist]}
     footprint = engine.store.peak_slots * eb
     line = {
         "metric": "MoE inference tokens/sec (SiDA serving, base-8)",
@@ -542,6 +553,7 @@ def run_ours(args):
                      "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms if ffn_avg_ms else None,
                      "attention_mix_avg_ms": float(np.mean(mix_ms)) if mix_ms else None},
         "north_star_ffn": north,
+        "routing": routing,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": n_tok * 4 + (B + 1) * 4,
                 "d2h_bytes_per_step": B * cfg.num_classes * 4 + cfg.num_layers * cfg.num_experts * 4,
