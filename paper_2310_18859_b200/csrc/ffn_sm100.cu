@@ -1623,6 +1623,24 @@ extern "C" int sida_out_proj_scatter(const uint16_t* ctx, int n_rows, int d, con
   p.out_bf16 = k ? x_perm : nullptr; p.bf16_map = k ? inv : nullptr; p.bf16_k = k;
   p.err_flag = err_flag;
   const int cg = n_rows >= 1024 ? 2 : 1;
+  // N tile 192 when it divides d: at d = 768 the 32K-row projection is 512
+  // tiles (6.9 persistent rounds of 74 pairs) instead of 384 (5.2 rounds), and
+  // this epilogue-bound GEMM gains more from the fuller last round than it
+  // loses to the narrower tile (tools/proj_probe.py: 98 -> 92 us).
+  // SIDA_OUTPROJ_BN=256|128 overrides (A/B).
+  static int bn = -1;
+  if (bn < 0) {
+    const char* e = getenv("SIDA_OUTPROJ_BN");
+    bn = e ? atoi(e) : 192;
+  }
+  if (bn == 192 && d % 192 == 0) {
+    if (cg == 2) return sm100::launch_gemm<192, 2, 2>(ctx, wo_t, 1, p, 1, as_stream(stream));
+    return sm100::launch_gemm<192, 2, 1>(ctx, wo_t, 1, p, 1, as_stream(stream));
+  }
+  if (bn == 128 && d % 128 == 0) {
+    if (cg == 2) return sm100::launch_gemm<128, 2, 2>(ctx, wo_t, 1, p, 1, as_stream(stream));
+    return sm100::launch_gemm<128, 2, 1>(ctx, wo_t, 1, p, 1, as_stream(stream));
+  }
   return sm100::dispatch_gemm<2>(ctx, wo_t, 1, p, 1, cg, as_stream(stream));
 }
 
@@ -1708,6 +1726,24 @@ extern "C" int sida_out_proj_scatter_peer(const uint16_t* ctx, int n_rows, int d
   p.peer_bf16 = peers; p.peer_stride = peer_stride;
   p.err_flag = err_flag;
   const int cg = n_rows >= 1024 ? 2 : 1;
+  // N tile 192 when it divides d: at d = 768 the 32K-row projection is 512
+  // tiles (6.9 persistent rounds of 74 pairs) instead of 384 (5.2 rounds), and
+  // this epilogue-bound GEMM gains more from the fuller last round than it
+  // loses to the narrower tile (tools/proj_probe.py: 98 -> 92 us).
+  // SIDA_OUTPROJ_BN=256|128 overrides (A/B).
+  static int bn = -1;
+  if (bn < 0) {
+    const char* e = getenv("SIDA_OUTPROJ_BN");
+    bn = e ? atoi(e) : 192;
+  }
+  if (bn == 192 && d % 192 == 0) {
+    if (cg == 2) return sm100::launch_gemm<192, 2, 2>(ctx, wo_t, 1, p, 1, as_stream(stream));
+    return sm100::launch_gemm<192, 2, 1>(ctx, wo_t, 1, p, 1, as_stream(stream));
+  }
+  if (bn == 128 && d % 128 == 0) {
+    if (cg == 2) return sm100::launch_gemm<128, 2, 2>(ctx, wo_t, 1, p, 1, as_stream(stream));
+    return sm100::launch_gemm<128, 2, 1>(ctx, wo_t, 1, p, 1, as_stream(stream));
+  }
   return sm100::dispatch_gemm<2>(ctx, wo_t, 1, p, 1, cg, as_stream(stream));
 }
 
