@@ -255,10 +255,12 @@ def measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms, steps=3,
     h2d_gbs = reps * 8 * eb / (e0.elapsed_time(e1) / 1e3) / 1e9
     n_all = cfg.num_layers * cfg.num_experts
     runs = []
-    for frac, depth in [(1.0, 1)] + [(f, 1) for f in fracs]:
+    for frac, depth, policy in ([(1.0, 1, "fifo")] + [(f, 1, "fifo") for f in fracs]
+                                + [(f, 1, "spread") for f in fracs]):
         xbatch = False
         slots = max(1, int(round(frac * n_all)))
-        eng = SidaEngine(model, pred, MemoryBudget(slots * eb), eval_top_k=1)
+        eng = SidaEngine(model, pred, MemoryBudget(slots * eb), eval_top_k=1,
+                         victim_policy=policy)
         eng.depth = depth
         tables = {0: eng.hash_tokens(0, toks[0], lengths)}
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -276,6 +278,7 @@ def measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms, steps=3,
         b_ms = s0.elapsed_time(s1) / steps
         loaded = (eng.store.bytes_loaded - loads0) / steps
         runs.append({"budget_frac": frac, "budget_slots": slots, "prefetch_depth": depth,
+                     "victim_policy": policy,
                      "tokens_per_s": n_tok / (b_ms / 1e3), "ms_per_step": b_ms,
                      "expert_loads_per_step": loaded / eb,
                      "copy_ms_at_link_rate": loaded / (h2d_gbs * 1e9) * 1e3,
@@ -285,10 +288,12 @@ def measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms, steps=3,
     return {"h2d_link_gbs": h2d_gbs, "h2d_source": "pinned host -> HBM, 8 expert images x 4 "
             "via sida_expert_copy on one stream", "all_resident_ms_per_step": step_ms,
             "budgets": runs,
-            "note": "uniform random routing activates every expert of every layer in every "
-                    "32K-token batch; with a budget below the working set the planner evicts "
-                    "experts already consumed by the batch (victim class 2), so each batch "
-                    "reloads about (all - slots) experts, issued one layer ahead"}
+            "note": "the predictor's routing activates every expert of every layer in every "
+                    "32K-token batch; with a budget below the working set the reference planner "
+                    "(victim_policy fifo) evicts the oldest experts the batch has consumed, "
+                    "which the next batch needs first, so its loads pile onto the first layers; "
+                    "victim_policy spread (offload.plan_placement_spread, opt-in, not the "
+                    "reference's plan) keeps about one load per layer, issued a layer ahead"}
 
 
 def measure_ffn_shape(experts: int, n_tok: int, peaks: dict, iters: int = 10) -> dict:

@@ -27,6 +27,7 @@ from .offload import (
     Wave,
     apply_group_inplace,
     plan_placement,
+    plan_placement_spread,
     run_waves,
 )
 from .predictor import ExpertHashTable, hash_device
@@ -135,9 +136,15 @@ class SidaEngine:
     """Streams, HBM slot arena and residency state of one serving instance."""
 
     def __init__(self, model: MoEModel, predictor, budget: MemoryBudget, eval_top_k: int = 1,
-                 prefetch: str = "layer", store: ExpertStore | None = None, streams=None):
+                 prefetch: str = "layer", store: ExpertStore | None = None, streams=None,
+                 victim_policy: str = "fifo"):
         if prefetch not in ("layer", "batch"):
             raise ContractError(f"unknown prefetch mode {prefetch!r}")
+        # "fifo": the reference planner (bit-identical plans); "spread": the
+        # opt-in victim order of offload.plan_placement_spread
+        if victim_policy not in ("fifo", "spread"):
+            raise ContractError(f"unknown victim policy {victim_policy!r}")
+        self.victim_policy = victim_policy
         if model.expert_bytes_each() > budget.fast_tier_bytes:
             raise UnservableError("budget cannot hold a single expert")
         self.model = model
@@ -356,7 +363,8 @@ class SidaEngine:
         required = table.required_by_layer()
         if len(required) < n_layers:
             raise ContractError(f"missing hash entry for (layer {len(required)}, token 0)")
-        plan = plan_placement(table, self.state, self.budget, self.model.expert_bytes_each())
+        planner = plan_placement if self.victim_policy == "fifo" else plan_placement_spread
+        plan = planner(table, self.state, self.budget, self.model.expert_bytes_each())
         return _BatchPlan(table, required, plan, [None] * len(plan.groups))
 
     def _issue(self, bp: _BatchPlan, idx: int) -> None:

@@ -147,6 +147,82 @@ def plan_placement(table, state: ResidencyState, budget: MemoryBudget,
                          expert_bytes=expert_bytes, source_fingerprint=state.fingerprint())
 
 
+def plan_placement_spread(table, state: ResidencyState, budget: MemoryBudget,
+                          expert_bytes: int) -> PlacementPlan:
+    """Opt-in victim policy (no reference counterpart; ``SidaEngine(...,
+    victim_policy="spread")``): the same per-layer groups as
+    ``plan_placement`` -- loads are the layer's missing experts in ascending
+    order -- with victims chosen to keep the next batch's misses spread over
+    the layers. Preference: not needed by this batch; consumed by a layer
+    before the previous one (the group stays prefetchable); needed later in
+    this batch; the previous layer's; the planned layer's own (multi-wave).
+    Within a class the layer that has given up the fewest experts to this plan
+    goes first, then the furthest next use, then arrival order.
+
+    The reference's FIFO classes evict the oldest consumed experts, so with
+    uniform routing and a budget below the working set a batch's loads pile
+    onto its first layers (Switch-base-8 at 86 of 96 slots: 15.3 loads per
+    batch, 8/2/6/2 on layers 0-3) and a layer's copies outlast the compute
+    they could hide behind. Spread victims settle at one load per layer (12
+    per batch) there, and at 1-3 per layer at 72 slots, each within a
+    layer's compute when issued a layer ahead."""
+    if expert_bytes > budget.fast_tier_bytes:
+        raise UnservableError(
+            f"expert of {expert_bytes} bytes exceeds budget {budget.fast_tier_bytes}")
+    required = table.required_by_layer()
+    n_layers = len(required)
+    res = dict(state.resident)
+    order = list(state.fifo_order)
+    used = state.used_bytes
+    budget_bytes = budget.fast_tier_bytes
+    taken = {}
+    groups = []
+    for layer in range(n_layers):
+        need = required[layer]
+        missing = [(layer, e) for e in sorted(need) if (layer, e) not in res]
+        steps = []
+        prefetchable = True
+        for key in missing:
+            while used + expert_bytes > budget_bytes:
+                best = None
+                for pos, (ll, e) in enumerate(order):
+                    needed = ll < n_layers and e in required[ll]
+                    if ll == layer and needed:
+                        cls = 4
+                    elif not needed:
+                        cls = 0
+                    elif ll < layer - 1:
+                        cls = 1
+                    elif ll > layer:
+                        cls = 2
+                    else:
+                        cls = 3
+                    dist = (n_layers - layer + ll) if ll < layer else (ll - layer)
+                    cand = (cls, taken.get(ll, 0), -dist, pos)
+                    if best is None or cand < best[0]:
+                        best = (cand, (ll, e))
+                if best is None:
+                    raise UnservableError("nothing evictable while over budget")
+                cand, victim = best
+                if cand[0] >= 3:
+                    prefetchable = False
+                taken[victim[0]] = taken.get(victim[0], 0) + 1
+                used -= res.pop(victim)
+                order.remove(victim)
+                steps.append(("evict", victim))
+            res[key] = expert_bytes
+            order.append(key)
+            used += expert_bytes
+            steps.append(("load", key))
+        n = len(missing)
+        groups.append(PlanGroup(
+            layer=layer, steps=steps, prefetchable=prefetchable,
+            transfer_s=n * expert_bytes / budget.bandwidth_bytes_per_s
+            + budget.per_transfer_latency_s * n))
+    return PlacementPlan(groups=groups, budget_bytes=budget.fast_tier_bytes,
+                         expert_bytes=expert_bytes, source_fingerprint=state.fingerprint())
+
+
 def apply_group_inplace(state: ResidencyState, group: PlanGroup, budget_bytes: int,
                         expert_bytes: int) -> None:
     """ref offload.py:207-222 (bookkeeping half; copies are ExpertStore's)."""

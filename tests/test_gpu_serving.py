@@ -116,3 +116,28 @@ def test_serve_sida_contracts(cuda_device):
         serve_sida(model, net, bad, MemoryBudget(eb))
     with pytest.raises(ContractError):
         serve_sida(model, net, _stream(model, 1, 1, 4, 8), MemoryBudget(eb), prefetch="never")
+
+
+def test_spread_victim_policy_serves_identical_logits(cuda_device):
+    """The opt-in spread victim order only changes which slots are reused and
+    when copies run: logits bit-identical to the all-resident reference plan
+    at every budget, with no more expert loads than the FIFO plan."""
+    from paper_2310_18859_b200.engine import SidaEngine
+    from paper_2310_18859_b200.offload import MemoryBudget
+    from paper_2310_18859_b200.pipeline import serve_sida
+
+    meta, model, net, batch, g, params, shape = _hash_fixture("c0")
+    batches = _stream(model, 6, 3, 5, 128)
+    eb = model.expert_bytes_each()
+    base = serve_sida(model, net, batches, MemoryBudget(16 * eb), eval_top_k=1,
+                      compute_hit_rate=False)
+    for slots in (13, 7, 3, 1):
+        reps = {}
+        for policy in ("fifo", "spread"):
+            eng = SidaEngine(model, net, MemoryBudget(slots * eb), victim_policy=policy)
+            reps[policy] = serve_sida(model, net, batches, MemoryBudget(slots * eb),
+                                      eval_top_k=1, compute_hit_rate=False, engine=eng)
+            assert reps[policy].peak_fast_tier_bytes <= slots * eb
+            for a, b in zip(base.logits, reps[policy].logits):
+                np.testing.assert_array_equal(a, b)
+        assert reps["spread"].expert_loads <= reps["fifo"].expert_loads

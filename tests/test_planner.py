@@ -102,3 +102,48 @@ def test_effective_utilization():
     assert effective_utilization(state, {(0, 1)}) == 0.5
     with pytest.raises(ContractError):
         effective_utilization(state, {(1, 1)})
+
+
+# ------------------------------------------------------------- spread victim policy
+class _Uniform:
+    def __init__(self, L, K, drop=()):
+        self.L, self.K, self.drop = L, K, set(drop)
+
+    def required_by_layer(self):
+        return [{e for e in range(self.K) if (l, e) not in self.drop} for l in range(self.L)]
+
+
+@pytest.mark.parametrize("slots", [86, 72, 48, 20])
+def test_spread_policy_plans_are_valid_and_spread(slots):
+    """plan_placement_spread (opt-in, not the reference's plan): every group
+    applies within the budget, every layer's experts are resident when it
+    runs, no group evicts an expert its own layer needs unless the layer alone
+    exceeds the budget, and at 86 of 96 slots the steady state is one load per
+    layer (the reference FIFO plan: 12-18 loads clustered on the first layers)."""
+    from paper_2310_18859_b200.offload import (MemoryBudget, ResidencyState,
+                                               apply_group_inplace, plan_placement_spread)
+
+    L, K = 12, 8
+    st = ResidencyState()
+    rng = np.random.default_rng(slots)
+    for j in range(8):
+        drop = {(int(l), int(e)) for l, e in zip(rng.integers(0, L, 3), rng.integers(0, K, 3))} \
+            if j % 2 else ()
+        table = _Uniform(L, K, drop)
+        req = table.required_by_layer()
+        plan = plan_placement_spread(table, st, MemoryBudget(slots), 1)
+        for g in plan.groups:
+            for k in g.evictions:
+                assert not (k[0] == g.layer and k[1] in req[g.layer])
+            apply_group_inplace(st, g, slots, 1)
+            assert st.used_bytes <= slots
+            assert all((g.layer, e) in st.resident for e in req[g.layer])
+        st.check()
+    if slots == 86:  # back to uniform routing: settles at <= 12 loads, <= 2 per layer
+        for _ in range(4):
+            plan = plan_placement_spread(_Uniform(L, K), st, MemoryBudget(slots), 1)
+            for g in plan.groups:
+                apply_group_inplace(st, g, slots, 1)
+        loads = [len(g.loads) for g in plan.groups]
+        assert sum(loads) <= 12 and max(loads) <= 2, loads
+        assert all(g.prefetchable for g in plan.groups)
