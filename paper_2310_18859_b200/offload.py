@@ -171,47 +171,76 @@ def plan_placement_spread(table, state: ResidencyState, budget: MemoryBudget,
             f"expert of {expert_bytes} bytes exceeds budget {budget.fast_tier_bytes}")
     required = table.required_by_layer()
     n_layers = len(required)
-    res = dict(state.resident)
-    order = list(state.fifo_order)
+    keys = list(state.fifo_order)
+    n_keys = len(keys)
+    n_missing = sum(len(r) for r in required)
+    cap = n_keys + n_missing + 1
+    # resident keys in arrival order (loads appended), as arrays for one
+    # vectorised argmin per eviction
+    kl = np.zeros(cap, dtype=np.int64)
+    ke = np.zeros(cap, dtype=np.int64)
+    if n_keys:
+        kv = np.array(keys, dtype=np.int64).reshape(-1, 2)
+        kl[:n_keys], ke[:n_keys] = kv[:, 0], kv[:, 1]
+    alive = np.zeros(cap, dtype=bool)
+    alive[:n_keys] = True
+    n_pos = n_keys
+    max_e = max([max(r) for r in required if r] + [int(ke[:n_keys].max()) if n_keys else 0, 0])
+    req = np.zeros((max(n_layers, int(kl[:n_keys].max()) + 1 if n_keys else 0, 1), max_e + 1),
+                   dtype=bool)
+    for layer, r in enumerate(required):
+        if r:
+            req[layer, np.fromiter(r, dtype=np.int64, count=len(r))] = True
+    resident = set(keys)
     used = state.used_bytes
     budget_bytes = budget.fast_tier_bytes
-    taken = {}
+    taken = np.zeros(req.shape[0], dtype=np.int64)
+    pos_all = np.arange(cap, dtype=np.int64)
     groups = []
     for layer in range(n_layers):
         need = required[layer]
-        missing = [(layer, e) for e in sorted(need) if (layer, e) not in res]
+        missing = [(layer, e) for e in sorted(need) if (layer, e) not in resident]
         steps = []
         prefetchable = True
+        cand = None  # per-group candidate arrays (this group's loads are never its victims)
         for key in missing:
             while used + expert_bytes > budget_bytes:
-                best = None
-                for pos, (ll, e) in enumerate(order):
-                    needed = ll < n_layers and e in required[ll]
-                    if ll == layer and needed:
-                        cls = 4
-                    elif not needed:
-                        cls = 0
-                    elif ll < layer - 1:
-                        cls = 1
-                    elif ll > layer:
-                        cls = 2
-                    else:
-                        cls = 3
-                    dist = (n_layers - layer + ll) if ll < layer else (ll - layer)
-                    cand = (cls, taken.get(ll, 0), -dist, pos)
-                    if best is None or cand < best[0]:
-                        best = (cand, (ll, e))
-                if best is None:
+                if cand is None:
+                    idx = np.nonzero(alive[:n_pos])[0]
+                    ll = kl[idx]
+                    needed = req[ll, ke[idx]]
+                    cls = np.where(~needed, 0,
+                                   np.where(ll == layer, 4,
+                                            np.where(ll < layer - 1, 1,
+                                                     np.where(ll > layer, 2, 3))))
+                    dist = np.where(ll < layer, n_layers - layer + ll, ll - layer)
+                    # (class, evictions already taken from the layer, furthest
+                    # next use, arrival order) as one lexicographic integer key
+                    hi = cls * 4096
+                    lo = (255 - np.clip(dist, 0, 255)) * 65536 + pos_all[idx]
+                    free = np.ones(idx.size, dtype=bool)
+                    cand = (idx, ll, cls, hi, lo, free)
+                idx, ll, cls, hi, lo, free = cand
+                score = (hi + np.minimum(taken[ll], 4095)) * (256 * 65536) + lo
+                score[~free] = np.iinfo(np.int64).max
+                i = int(np.argmin(score))
+                if not free[i]:
                     raise UnservableError("nothing evictable while over budget")
-                cand, victim = best
-                if cand[0] >= 3:
+                free[i] = False
+                j = int(idx[i])
+                vcls = int(cls[i])
+                victim = (int(kl[j]), int(ke[j]))
+                if vcls >= 3:
                     prefetchable = False
-                taken[victim[0]] = taken.get(victim[0], 0) + 1
-                used -= res.pop(victim)
-                order.remove(victim)
+                taken[victim[0]] += 1
+                alive[j] = False
+                resident.discard(victim)
+                used -= expert_bytes
                 steps.append(("evict", victim))
-            res[key] = expert_bytes
-            order.append(key)
+            kl[n_pos], ke[n_pos] = key
+            alive[n_pos] = True
+            n_pos += 1
+            resident.add(key)
             used += expert_bytes
             steps.append(("load", key))
         n = len(missing)
