@@ -374,10 +374,20 @@ def run_ours(args):
     from paper_2310_18859_b200.engine import SidaEngine
 
     ws, rank, local = dist_env()
+    # SIDA_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo plumbing -- a
+    # functional check of the multi-rank path on a one-GPU box (timings of
+    # ranks sharing a GPU are not a scaling measurement)
+    share = os.environ.get("SIDA_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if share else dev
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = MoEConfig(**dict(BASE8, num_experts=args.experts))
     model = MoEModel.synthetic(cfg, seed=0, device=dev)
     pred = PredictorNet(PredictorConfig(), cfg.d_model, cfg.num_layers, cfg.num_experts, Rng(1))
@@ -445,7 +455,7 @@ def run_ours(args):
     engine.ffn_events = None
     engine.mix_events = []
     if ws > 1:
-        t = torch.tensor([ms], device=dev)
+        t = torch.tensor([ms], device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = ws * args.steps * n_tok / (ms / 1e3)
@@ -466,7 +476,7 @@ def run_ours(args):
         barrier()
         e2e_s = time.perf_counter() - t0
         if ws > 1:
-            t = torch.tensor([e2e_s], device=dev)
+            t = torch.tensor([e2e_s], device=red_dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
         e2e = ws * args.steps * n_tok / e2e_s
@@ -541,7 +551,8 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic uniform tokens, random-init Switch-base-8-shaped weights (GPU RNG)",
         "config": {"workload": "Switch-base-8 SiDA serving with expert offload, 12 layers, "
-                               "bf16, 1 B200 (BASELINE configs[1])", "global_batch": B * ws, "seq_len": T,
+                               f"bf16, {ws} B200 (BASELINE configs[1])", "global_batch": B * ws,
+                   "seq_len": T,
                    "tokens_per_step_per_gpu": n_tok, "layers": cfg.num_layers,
                    "experts": cfg.num_experts, "d_model": cfg.d_model,
                    "expert_hidden": cfg.expert_hidden, "top_k": 1,
