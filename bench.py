@@ -401,9 +401,14 @@ def run_ours(args):
 
         from paper_2310_18859_b200.expert_parallel import PeerTransport
 
-        engine = ExpertParallelEngine(model, pred, budget,
-                                      transport=PeerTransport() if args.ep_transport == "peer"
-                                      else None)
+        if share:  # gloo plumbing (collectives staged through host memory)
+            from paper_2310_18859_b200.expert_parallel import GlooTransport
+
+            transport = (PeerTransport(control=GlooTransport()) if args.ep_transport == "peer"
+                         else GlooTransport())
+        else:
+            transport = PeerTransport() if args.ep_transport == "peer" else None
+        engine = ExpertParallelEngine(model, pred, budget, transport=transport)
         engine.compute_stream = engine.base.compute_stream
         engine.ffn_events, engine.mix_events = None, []
     else:
