@@ -202,9 +202,13 @@ def plan_placement_spread(table, state: ResidencyState, budget: MemoryBudget,
         missing = [(layer, e) for e in sorted(need) if (layer, e) not in resident]
         steps = []
         prefetchable = True
-        cand = None  # per-group candidate arrays (this group's loads are never its victims)
+        cand = None  # per-group candidate arrays, rebuilt only when they run dry
         for key in missing:
             while used + expert_bytes > budget_bytes:
+                if cand is not None and not cand[5].any():
+                    # only when one layer's experts exceed the budget (multi-wave):
+                    # this group's own loads become candidates (class 4)
+                    cand = None
                 if cand is None:
                     idx = np.nonzero(alive[:n_pos])[0]
                     ll = kl[idx]

@@ -147,3 +147,23 @@ def test_spread_policy_plans_are_valid_and_spread(slots):
         loads = [len(g.loads) for g in plan.groups]
         assert sum(loads) <= 12 and max(loads) <= 2, loads
         assert all(g.prefetchable for g in plan.groups)
+
+
+@pytest.mark.parametrize("slots", [1, 3, 7])
+def test_spread_policy_tiny_budgets(slots):
+    """Budgets below one layer's working set (multi-wave layers): the spread
+    planner evicts the layer's own earlier loads like the FIFO planner's class
+    4, stays within the budget and loads every required expert."""
+    from paper_2310_18859_b200.offload import (MemoryBudget, ResidencyState,
+                                               apply_group_inplace, plan_placement_spread)
+
+    st = ResidencyState()
+    table = _Uniform(2, 8)
+    for _ in range(3):
+        plan = plan_placement_spread(table, st, MemoryBudget(slots), 1)
+        for g in plan.groups:
+            assert sorted(k[1] for k in g.loads) == sorted(
+                e for e in range(8) if (g.layer, e) not in st.resident)
+            apply_group_inplace(st, g, slots, 1)
+            assert st.used_bytes <= slots
+        st.check()
