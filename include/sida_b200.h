@@ -37,6 +37,10 @@ enum {
 /* Library identity and the device check (fails unless cc 10.0 / sm_100). */
 int sida_abi_version(void);
 const char* sida_last_error(void);
+/* Number of kernels this library has launched in the process (every entry
+ * point counts its own launches; library calls such as cudaMemcpyAsync are
+ * not kernels and are not counted). */
+unsigned long long sida_launch_count(void);
 int sida_device_check(int device);
 
 /* ---------------------------------------------------------------------
@@ -93,14 +97,16 @@ int sida_debug_hash_prof(unsigned long long* out);
  * ids: int32 (L, n_rows) with n_rows = n_tokens*k, row = token*k + rank.
  * Outputs per layer: hist (L,K), off (L,K+1), perm (L,n_rows) stable by
  * row within expert, inv (L,n_rows) with inv[perm[p]] = p; alpha_perm
- * (optional, L x n_rows float32) = alpha_rows[perm[p]].
+ * (optional, L x n_rows float32) = alpha_rows[perm[p]]. err_flag (int32, set to 1
+ * when an id lies outside [0, K); never cleared here: the caller zeroes it
+ * and reads it at its next synchronisation point -> ContractError).
  * Replaces the implicit grouping of ref moe.py:253-256 (w1[ids] gather).
  * ------------------------------------------------------------------- */
 size_t sida_permute_workspace_bytes(int n_layers, int n_rows, int num_experts);
 int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, int num_experts,
                       const float* alpha_rows, int32_t* hist, int32_t* off, int32_t* perm,
-                      int32_t* inv, float* alpha_perm, void* workspace, size_t workspace_bytes,
-                      void* stream);
+                      int32_t* inv, float* alpha_perm, int32_t* err_flag, void* workspace,
+                      size_t workspace_bytes, void* stream);
 
 /* x_perm[p, :] = bf16(x[perm[p] / k, :]), x float32 (n_tokens, d), 128-bit
  * coalesced. (The row gather half of A13.) */
@@ -260,6 +266,31 @@ int sida_combine_ranks(const float* y, const float* resid, int n_tokens, int k, 
 int sida_router_topk(const float* x, int n_tokens, int d, const float* w_r, int num_experts,
                      int k, float* probs, int32_t* ids, double* alpha, float* alpha_f32,
                      void* stream);
+
+/* ---------------------------------------------------------------------
+ * Numeric API of the reference on the GPU, fp64, one CTA per row
+ * (the drop-in's utility entry points; the hot path fuses the same math).
+ *  - sida_softmax_rows_f64: out = exp(z - max) / sum per row of n
+ *    (ref numkit.py:28-33; a few ulp from numpy's);
+ *  - sida_sparsemax_rows_f64: the sorted closed form of ref numkit.py:42-60,
+ *    bit-identical (n <= 8192);
+ *  - sida_topk_rows_f64: idx (rows, k) int64 = argsort(-z, stable)[:k]
+ *    (ref numkit.py:76-93), bit-identical;
+ *  - sida_router_scores_f64: probs (rows, K) = softmax(x_r @ w_r), x (rows, d),
+ *    w_r (d, K) (ref moe.py:108-115 per embedding);
+ *  - sida_moe_token_f64: out (d) = sum_i alphas_i (relu(x w1_i + b1_i) w2_i + b2_i)
+ *    over the m selected experts packed in selection order, w1 (m, d, h),
+ *    b1 (m, h), w2 (m, h, d), b2 (m, d); hidden (m, h) workspace
+ *    (ref moe.py:118-146, Eq. 1, no residual).
+ * ------------------------------------------------------------------- */
+int sida_softmax_rows_f64(const double* z, int rows, int n, double* out, void* stream);
+int sida_sparsemax_rows_f64(const double* z, int rows, int n, double* out, void* stream);
+int sida_topk_rows_f64(const double* z, int rows, int n, int k, int64_t* idx, void* stream);
+int sida_router_scores_f64(const double* x, int rows, int d, const double* w_r, int K,
+                           double* probs, void* stream);
+int sida_moe_token_f64(const double* x, int m, const double* alphas, const double* w1,
+                       const double* b1, const double* w2, const double* b2, int d, int h,
+                       double* hidden, double* out, void* stream);
 
 /* ---------------------------------------------------------------------
  * (2) Expert streaming: one pinned-host expert image -> one HBM slot on the

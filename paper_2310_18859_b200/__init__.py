@@ -8,7 +8,18 @@ loop. Compute runs in the hand-written CUDA library `_sida_b200.so`
 """
 
 from .errors import ContractError, CoverageError, NativeLibraryError, TrainingDiverged, UnservableError
-from .moe import ActivationTrace, BatchLayout, MoEConfig, MoEModel, Rng, SequenceBatch, model_forward
+from .moe import (
+    ActivationTrace,
+    BatchLayout,
+    MoEConfig,
+    MoEModel,
+    Rng,
+    SequenceBatch,
+    model_forward,
+    moe_layer_forward,
+    router_scores,
+)
+from .numkit import check_finite, softmax, sparsemax, topk, topk_rows
 from .predictor import (
     DeviceTable,
     ExpertHashTable,

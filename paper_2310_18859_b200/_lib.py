@@ -24,6 +24,7 @@ _vp, _i, _sz = C.c_void_p, C.c_int, C.c_size_t
 SIGNATURES = {
     "sida_abi_version": (_i, []),
     "sida_last_error": (C.c_char_p, []),
+    "sida_launch_count": (C.c_ulonglong, []),
     "sida_device_check": (_i, [_i]),
     "sida_hash_param_count": (_sz, [_i, _i, _i, _i, _i]),
     "sida_hash_workspace_bytes": (_sz, [_i, _i, _i, _i, _i, _i, _i, _i]),
@@ -33,7 +34,8 @@ SIGNATURES = {
                                _i, _vp, _vp, _vp, _vp, _sz, _vp]),
     "sida_debug_hash_prof": (_i, [_vp]),
     "sida_permute_workspace_bytes": (_sz, [_i, _i, _i]),
-    "sida_permute_hist": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "sida_permute_hist": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                               _vp]),
     "sida_gather_rows_bf16": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp]),
     "sida_slot_bytes": (_sz, [_i, _i]),
     "sida_grouped_ffn_bf16": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _i, _vp, _sz, _i, _vp, _vp,
@@ -64,6 +66,11 @@ SIGNATURES = {
     "sida_ipc_handle": (_i, [_vp, _vp, C.POINTER(C.c_size_t)]),
     "sida_ipc_open": (_i, [_vp, _sz, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "sida_ipc_close": (_i, [_vp]),
+    "sida_softmax_rows_f64": (_i, [_vp, _i, _i, _vp, _vp]),
+    "sida_sparsemax_rows_f64": (_i, [_vp, _i, _i, _vp, _vp]),
+    "sida_topk_rows_f64": (_i, [_vp, _i, _i, _i, _vp, _vp]),
+    "sida_router_scores_f64": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp]),
+    "sida_moe_token_f64": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
     "sida_expert_copy": (_i, [_vp, _vp, _sz, _vp, _vp, _vp]),
     "sida_pack_expert_host": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp]),
     "sida_plan_placement": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp]),

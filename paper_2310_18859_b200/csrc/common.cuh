@@ -12,6 +12,8 @@
 namespace sida {
 
 void set_error(const char* fmt, ...);
+// Process-wide count of this library's kernel launches (sida_launch_count).
+void count_launch();
 
 // Return-on-failure helpers for the extern "C" wrappers.
 #define SIDA_REQUIRE(cond, code, ...)        \
@@ -34,6 +36,7 @@ void set_error(const char* fmt, ...);
 
 #define SIDA_LAUNCH_CHECK()                                                        \
   do {                                                                             \
+    ::sida::count_launch();                                                        \
     cudaError_t _e = cudaGetLastError();                                           \
     if (_e != cudaSuccess) {                                                       \
       ::sida::set_error("kernel launch failed: %s (%s:%d)", cudaGetErrorString(_e), \

@@ -1334,6 +1334,7 @@ static int launch_gemm(const void* a_base, const void* b_base, int n_slots, cons
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p, ta2, tb2, q2, mflags, lag));
+  count_launch();
   return SIDA_OK;
 }
 
@@ -1394,6 +1395,7 @@ static int launch_tn(const void* x_base, const void* w_base, int n_slots, const 
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, tw, tx, p));
+  count_launch();
   return SIDA_OK;
 }
 
@@ -1430,6 +1432,7 @@ static int launch_fx(const void* x_perm, const uint8_t* arena, int n_slots, cons
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   SIDA_CUDA(cudaLaunchKernelEx(&cfg, fused_ffn_tn_kernel, tw1, tw2, tx, p));
+  count_launch();
   return SIDA_OK;
 }
 

@@ -1158,9 +1158,11 @@ static int launch_lstm(const double* xw, const double* tokx, const double* posx,
         xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, H, h_out);
   else if (H == MAXH && !getenv("SIDA_LSTM_SPLIT")) {
     const int chunk = lstm_chunk() > 0 ? lstm_chunk() : max_len;
-    for (int t0 = 0; t0 < max_len; t0 += chunk)
+    for (int t0 = 0; t0 < max_len; t0 += chunk) {
+      if (t0 > 0) count_launch();  // SIDA_LAUNCH_CHECK below counts one launch
       lstm_quad_kernel<MAXH, FOLD><<<n_seq, 4 * MAXH, 0, s>>>(
           xw, tokx, posx, cx, tokens, wh, b, seq_off, n_seq, h_out, t0, t0 + chunk, c_buf);
+    }
   }
   else
     lstm_kernel<MAXH, 1, FOLD><<<n_seq, 4 * MAXH, 0, s>>>(xw, tokx, posx, cx, tokens, wh, b,

@@ -1,20 +1,28 @@
 // Token permute + histogram, every MoE layer of a
-// batch in one pass, plus the bf16 row gather.
+// batch in one launch chain, plus the bf16 row gather.
 //
 // The reference never permutes: moe_apply gathers w1[ids] per token
 // (ref moe.py:253-256). The GPU path groups the (token, rank) rows of each
 // layer by expert with a stable counting sort whose output is bit-identical
-// to np.argsort(ids[l].reshape(-1), kind="stable") (oracle/permute.py):
+// to np.argsort(ids[l].reshape(-1), kind="stable") (oracle/permute.py).
+// Rows are cut into tiles of TILE rows (1024..8192, chosen so that L x tiles
+// covers >= 2 CTAs per SM); one CTA of 256 threads per (layer, tile):
 //
-//   hist_tiles : per (layer, tile of kTileRows rows) smem histogram
-//   scan       : per layer, exclusive scan over (expert-major, tile-minor)
-//                -> off[l] and each (expert, tile) base position
-//   scatter    : per tile, rows visited in order; the within-warp stable rank
-//                comes from __match_any_sync + popc (warp-shuffle prefix),
-//                the cross-warp prefix from a per-chunk smem count table.
+//   hist_tiles : 128-bit id loads into shared memory, warp-aggregated
+//                (__match_any_sync) shared histogram -> counts[l][tile][e]
+//   scan       : per layer, one thread per expert: totals over tiles
+//                (coalesced across experts), block exclusive scan -> off,
+//                then each (tile, expert) base position
+//   scatter    : the tile's ids staged again in shared memory; each warp
+//                walks its contiguous rows in order and takes the in-warp
+//                stable rank from __match_any_sync + popc, per-warp running
+//                counts give the cross-warp prefix; inv is written row-ordered
+//                (coalesced), then perm / alpha_perm are written from a
+//                shared-memory copy of the tile in sorted order, so every
+//                (tile, expert) run is a contiguous store.
 //
 // Since SiDA's hash table holds every layer's ids before inference starts
-// (ref pipeline.py:208-215), all L layers are permuted in one launch on the
+// (ref pipeline.py:208-215), all L layers are permuted in one chain on the
 // hash stream; only the x-row gather waits for each layer's input.
 #include <algorithm>
 
@@ -22,131 +30,207 @@
 
 namespace sida {
 
-constexpr int kTileRows = 4096;
 constexpr int kPermThreads = 256;
 constexpr int kPermWarps = kPermThreads / 32;
 constexpr int kMaxExperts = 1024;
 
+// Tile rows for (rows, layers): >= 2 CTAs per SM when the batch allows it.
+static inline int perm_tile(int n_rows, int n_layers) {
+  const long long want = (long long)n_rows * std::max(n_layers, 1) / (2 * kNumSMs);
+  int t = 1024;
+  while (t < 8192 && 2ll * t <= want) t *= 2;
+  return t;
+}
+
+static inline int perm_tiles(int n_rows, int tile) { return std::max(1, ceil_div(n_rows, tile)); }
+
+// Stage ids[r0, r1) of one layer into shared memory (128-bit loads when aligned).
+__device__ __forceinline__ void stage_ids(const int32_t* __restrict__ row_ids, int r0, int r1,
+                                          int32_t* __restrict__ s_ids) {
+  const int n = r1 - r0;
+  const int32_t* src = row_ids + r0;
+  if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+    const int n4 = n >> 2;
+    const int4* s4 = reinterpret_cast<const int4*>(src);
+    for (int i = threadIdx.x; i < n4; i += blockDim.x)
+      reinterpret_cast<int4*>(s_ids)[i] = __ldg(s4 + i);
+    for (int i = (n4 << 2) + threadIdx.x; i < n; i += blockDim.x) s_ids[i] = __ldg(src + i);
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s_ids[i] = __ldg(src + i);
+  }
+}
+
+template <int TILE>
 __global__ void __launch_bounds__(kPermThreads)
 hist_tiles_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
-                  int32_t* __restrict__ tile_counts, int32_t* __restrict__ err) {
-  extern __shared__ int32_t s_hist[];
+                  int32_t* __restrict__ counts, int32_t* __restrict__ err) {
+  __shared__ int32_t s_ids[TILE];
+  extern __shared__ int32_t s_hist[];  // [K]
   const int layer = blockIdx.y, tile = blockIdx.x;
+  const int lane = threadIdx.x & 31;
   for (int e = threadIdx.x; e < K; e += blockDim.x) s_hist[e] = 0;
+  const int r0 = tile * TILE, r1 = min(n_rows, r0 + TILE);
+  stage_ids(ids + (size_t)layer * n_rows, r0, r1, s_ids);
   __syncthreads();
-  const int32_t* row_ids = ids + (size_t)layer * n_rows;
-  const int r0 = tile * kTileRows, r1 = min(n_rows, r0 + kTileRows);
-  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    int e = row_ids[r];
-    if (e < 0 || e >= K) {
-      atomicExch(err, 1);
-      continue;
-    }
-    atomicAdd(&s_hist[e], 1);
+  const unsigned lt = (1u << lane) - 1u;
+  bool bad = false;
+  for (int i = threadIdx.x; i < TILE; i += blockDim.x) {  // uniform trip count: full warps
+    int e = i < r1 - r0 ? s_ids[i] : -1;
+    if (i < r1 - r0 && (e < 0 || e >= K)) { bad = true; e = -1; }
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    if (e >= 0 && (peers & lt) == 0) atomicAdd(&s_hist[e], __popc(peers));
   }
+  if (bad) atomicExch(err, 1);
   __syncthreads();
-  int32_t* tc = tile_counts + (size_t)layer * K * n_tiles;
-  for (int e = threadIdx.x; e < K; e += blockDim.x) tc[(size_t)e * n_tiles + tile] = s_hist[e];
+  int32_t* c = counts + ((size_t)layer * n_tiles + tile) * K;
+  for (int e = threadIdx.x; e < K; e += blockDim.x) c[e] = s_hist[e];
 }
 
-// One block per layer: exclusive scan of tile_counts in (expert, tile) order.
+// One CTA per layer, thread e = expert e: totals over tiles, exclusive scan
+// over experts (off, hist), then the base position of every (tile, expert).
 __global__ void __launch_bounds__(1024)
-scan_kernel(const int32_t* __restrict__ tile_counts, int K, int n_tiles,
-            int32_t* __restrict__ tile_base, int32_t* __restrict__ hist, int32_t* __restrict__ off) {
+scan_kernel(const int32_t* __restrict__ counts, int K, int n_tiles, int32_t* __restrict__ tile_base,
+            int32_t* __restrict__ hist, int32_t* __restrict__ off) {
   __shared__ int32_t s_warp[32];
-  __shared__ int32_t s_carry;
-  const int layer = blockIdx.x;
-  const size_t n = (size_t)K * n_tiles;
-  const int32_t* tc = tile_counts + (size_t)layer * n;
-  int32_t* tb = tile_base + (size_t)layer * n;
-  if (threadIdx.x == 0) s_carry = 0;
+  const int layer = blockIdx.x, e = threadIdx.x;
+  const int lane = e & 31, warp = e >> 5;
+  const int32_t* c = counts + (size_t)layer * n_tiles * K;
+  int tot = 0;
+  if (e < K)
+    for (int t = 0; t < n_tiles; ++t) tot += c[(size_t)t * K + e];
+  int incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (size_t base = 0; base < n; base += blockDim.x) {
-    size_t i = base + threadIdx.x;
-    int v = i < n ? tc[i] : 0;
-    int incl = v;
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    const int w = lane < nw ? s_warp[lane] : 0;
+    int wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int t = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += t;
+      const int v = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += v;
     }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      int w = lane < (int)(blockDim.x >> 5) ? s_warp[lane] : 0;
-      int wi = w;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, wi, o);
-        if (lane >= o) wi += t;
-      }
-      s_warp[lane] = wi - w;  // exclusive per-warp prefix
+    s_warp[lane] = wi - w;
+  }
+  __syncthreads();
+  const int excl = s_warp[warp] + incl - tot;
+  if (e < K) {
+    hist[(size_t)layer * K + e] = tot;
+    off[(size_t)layer * (K + 1) + e] = excl;
+    if (e == K - 1) off[(size_t)layer * (K + 1) + K] = excl + tot;
+    int run = excl;
+    int32_t* tb = tile_base + (size_t)layer * n_tiles * K;
+    for (int t = 0; t < n_tiles; ++t) {
+      tb[(size_t)t * K + e] = run;
+      run += c[(size_t)t * K + e];
     }
-    __syncthreads();
-    const int carry = s_carry;
-    if (i < n) tb[i] = carry + s_warp[warp] + incl - v;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) s_carry = carry + s_warp[warp] + incl;
-    __syncthreads();
   }
-  // hist / off from the per-expert sums
-  for (int e = threadIdx.x; e < K; e += blockDim.x) {
-    int s = 0;
-    for (int t = 0; t < n_tiles; ++t) s += tc[(size_t)e * n_tiles + t];
-    hist[(size_t)layer * K + e] = s;
-    off[(size_t)layer * (K + 1) + e] = tb[(size_t)e * n_tiles];
-  }
-  if (threadIdx.x == 0) off[(size_t)layer * (K + 1) + K] = s_carry;
 }
 
-__global__ void __launch_bounds__(kPermThreads)
+template <int TILE>
+__global__ void __launch_bounds__(kPermThreads, 2)
 scatter_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
                const int32_t* __restrict__ tile_base, const float* __restrict__ alpha_rows,
                int32_t* __restrict__ perm, int32_t* __restrict__ inv,
                float* __restrict__ alpha_perm) {
+  constexpr int R = TILE / kPermWarps;  // contiguous rows per warp
+  constexpr int NR = R / 32;            // rounds per warp
   extern __shared__ int32_t smem[];
-  int32_t* s_run = smem;                    // [K] running count of this tile
-  int32_t* s_warp = smem + K;               // [kPermWarps][K] counts of this chunk
+  int32_t* s_ids = smem;                        // [TILE] ids, then sorted rows
+  int32_t* s_ord = s_ids + TILE;                // [TILE] tile row of sorted position q
+  int32_t* s_cnt = s_ord + TILE;                // [warps][K] counts -> warp prefix
+  int32_t* s_tbase = s_cnt + kPermWarps * K;    // [K] global base of (tile, e)
+  int32_t* s_texc = s_tbase + K;                // [K + 1] tile-local exclusive prefix
   const int layer = blockIdx.y, tile = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int32_t* row_ids = ids + (size_t)layer * n_rows;
-  const int32_t* tb = tile_base + (size_t)layer * K * n_tiles;
-  int32_t* lperm = perm + (size_t)layer * n_rows;
-  int32_t* linv = inv + (size_t)layer * n_rows;
-  for (int e = threadIdx.x; e < K; e += blockDim.x) s_run[e] = tb[(size_t)e * n_tiles + tile];
-  for (int i = threadIdx.x; i < kPermWarps * K; i += blockDim.x) s_warp[i] = 0;
+  const int r0 = tile * TILE, r1 = min(n_rows, r0 + TILE), n = r1 - r0;
+  const int32_t* tb = tile_base + ((size_t)layer * n_tiles + tile) * K;
+  for (int i = threadIdx.x; i < kPermWarps * K; i += blockDim.x) s_cnt[i] = 0;
+  for (int e = threadIdx.x; e < K; e += blockDim.x) s_tbase[e] = tb[e];
+  stage_ids(ids + (size_t)layer * n_rows, r0, r1, s_ids);
   __syncthreads();
-  const unsigned lt_mask = (1u << lane) - 1u;
-  const int r0 = tile * kTileRows, r1 = min(n_rows, r0 + kTileRows);
-  for (int c0 = r0; c0 < r1; c0 += kPermThreads) {
-    const int r = c0 + threadIdx.x;
-    const bool valid = r < r1;
-    int e = valid ? row_ids[r] : -1;
-    if (valid && (e < 0 || e >= K)) e = -1;  // counted as error by hist pass
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    const int rank = __popc(peers & lt_mask);
-    const bool leader = (peers & lt_mask) == 0;
-    if (e >= 0 && leader) s_warp[warp * K + e] = __popc(peers);
-    __syncthreads();
-    if (e >= 0) {
-      int pos = s_run[e] + rank;
-      for (int w = 0; w < warp; ++w) pos += s_warp[w * K + e];
-      lperm[pos] = r;
-      linv[r] = pos;
-      if (alpha_perm) alpha_perm[(size_t)layer * n_rows + pos] = alpha_rows[(size_t)layer * n_rows + r];
-    }
-    __syncthreads();
-    for (int x = threadIdx.x; x < K; x += blockDim.x) {
-      int s = 0;
+
+  // pass 1: in-order stable local ranks, per warp over its R rows
+  const unsigned lt = (1u << lane) - 1u;
+  int32_t* my_cnt = s_cnt + warp * K;
+  int loc[NR];
 #pragma unroll
-      for (int w = 0; w < kPermWarps; ++w) {
-        s += s_warp[w * K + x];
-        s_warp[w * K + x] = 0;
-      }
-      s_run[x] += s;
+  for (int j = 0; j < NR; ++j) {
+    const int i = warp * R + j * 32 + lane;
+    int e = i < n ? s_ids[i] : -1;
+    if (e >= K) e = -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    int base = 0;
+    if (e >= 0) base = my_cnt[e];
+    __syncwarp();
+    if (e >= 0 && (peers & lt) == 0) my_cnt[e] = base + __popc(peers);
+    __syncwarp();
+    loc[j] = base + __popc(peers & lt);
+  }
+  __syncthreads();
+
+  // warp prefix per expert (in place) and the tile's per-expert totals
+  for (int e = threadIdx.x; e < K; e += blockDim.x) {
+    int run = 0;
+#pragma unroll
+    for (int w = 0; w < kPermWarps; ++w) {
+      const int c = s_cnt[w * K + e];
+      s_cnt[w * K + e] = run;
+      run += c;
     }
-    __syncthreads();
+    s_texc[e] = run;  // total; scanned below
+  }
+  __syncthreads();
+  // exclusive scan of the totals over experts (one warp, K <= 1024)
+  if (warp == 0) {
+    int carry = 0;
+    for (int b = 0; b < K; b += 32) {
+      const int e = b + lane;
+      const int v = e < K ? s_texc[e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (e < K) s_texc[e] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) s_texc[K] = carry;
+  }
+  __syncthreads();
+
+  // pass 2: positions; inv row-ordered, sorted order staged in shared memory
+  int32_t* linv = inv + (size_t)layer * n_rows;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const int i = warp * R + j * 32 + lane;
+    int e = i < n ? s_ids[i] : -1;
+    if (e >= K) e = -1;
+    if (e >= 0) {
+      const int within = s_cnt[warp * K + e] + loc[j];
+      linv[r0 + i] = s_tbase[e] + within;
+      s_ord[s_texc[e] + within] = i;
+    } else if (i < n) {
+      linv[r0 + i] = -1;
+    }
+  }
+  __syncthreads();
+  const int n_valid = s_texc[K];
+  int32_t* lperm = perm + (size_t)layer * n_rows;
+  const float* la = alpha_rows ? alpha_rows + (size_t)layer * n_rows + r0 : nullptr;
+  float* lap = alpha_perm ? alpha_perm + (size_t)layer * n_rows : nullptr;
+  for (int q = threadIdx.x; q < n_valid; q += blockDim.x) {
+    const int i = s_ord[q];
+    const int e = s_ids[i];
+    const int pos = s_tbase[e] + (q - s_texc[e]);
+    lperm[pos] = r0 + i;
+    if (lap) lap[pos] = la[i];
   }
 }
 
@@ -177,17 +261,46 @@ gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ perm
 
 using namespace sida;
 
-static inline int perm_tiles(int n_rows) { return std::max(1, ceil_div(n_rows, kTileRows)); }
-
 extern "C" size_t sida_permute_workspace_bytes(int n_layers, int n_rows, int num_experts) {
-  size_t n = (size_t)n_layers * num_experts * perm_tiles(n_rows);
-  return align_up(2 * n * sizeof(int32_t), 256) + 256;
+  const int tile = perm_tile(n_rows, n_layers);
+  size_t n = (size_t)n_layers * num_experts * perm_tiles(n_rows, tile);
+  return align_up(2 * n * sizeof(int32_t), 256);
+}
+
+template <int TILE>
+static int permute_launch(const int32_t* ids, int n_layers, int n_rows, int K, const float* alpha_rows,
+                          int32_t* hist, int32_t* off, int32_t* perm, int32_t* inv,
+                          float* alpha_perm, int32_t* counts, int32_t* tile_base, int32_t* err,
+                          cudaStream_t s) {
+  const int n_tiles = perm_tiles(n_rows, TILE);
+  dim3 grid(n_tiles, n_layers);
+  hist_tiles_kernel<TILE><<<grid, kPermThreads, K * sizeof(int32_t), s>>>(ids, n_rows, K, n_tiles,
+                                                                         counts, err);
+  SIDA_LAUNCH_CHECK();
+  const int scan_threads = std::max(32, ceil_div(K, 32) * 32);
+  scan_kernel<<<n_layers, scan_threads, 0, s>>>(counts, K, n_tiles, tile_base, hist, off);
+  SIDA_LAUNCH_CHECK();
+  if (n_rows > 0) {
+    const size_t smem = (2ull * TILE + (size_t)(kPermWarps + 2) * K + 1) * sizeof(int32_t);
+    static bool configured = false;
+    if (!configured) {
+      SIDA_CUDA(cudaFuncSetAttribute(scatter_kernel<TILE>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)((2ull * TILE + (kPermWarps + 2) * kMaxExperts + 1) *
+                                           sizeof(int32_t))));
+      configured = true;
+    }
+    scatter_kernel<TILE><<<grid, kPermThreads, smem, s>>>(ids, n_rows, K, n_tiles, tile_base,
+                                                          alpha_rows, perm, inv, alpha_perm);
+    SIDA_LAUNCH_CHECK();
+  }
+  return SIDA_OK;
 }
 
 extern "C" int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, int num_experts,
                                  const float* alpha_rows, int32_t* hist, int32_t* off,
-                                 int32_t* perm, int32_t* inv, float* alpha_perm, void* workspace,
-                                 size_t workspace_bytes, void* stream) {
+                                 int32_t* perm, int32_t* inv, float* alpha_perm, int32_t* err_flag,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
   SIDA_REQUIRE(n_layers >= 1 && n_rows >= 0 && num_experts >= 1, SIDA_ERR_CONTRACT,
                "bad permute dims L=%d rows=%d K=%d", n_layers, n_rows, num_experts);
   SIDA_REQUIRE(num_experts <= kMaxExperts, SIDA_ERR_UNSUPPORTED, "K=%d > %d", num_experts,
@@ -195,27 +308,23 @@ extern "C" int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, i
   SIDA_REQUIRE(workspace_bytes >= sida_permute_workspace_bytes(n_layers, n_rows, num_experts),
                SIDA_ERR_CONTRACT, "permute workspace too small");
   SIDA_REQUIRE(!alpha_perm || alpha_rows, SIDA_ERR_CONTRACT, "alpha_perm needs alpha_rows");
+  SIDA_REQUIRE(err_flag && hist && off && (n_rows == 0 || (ids && perm && inv)), SIDA_ERR_CONTRACT,
+               "null pointer passed to sida_permute_hist");
   cudaStream_t s = as_stream(stream);
-  const int n_tiles = perm_tiles(n_rows);
-  size_t n = (size_t)n_layers * num_experts * n_tiles;
-  int32_t* tile_counts = static_cast<int32_t*>(workspace);
-  int32_t* tile_base = tile_counts + n;
-  int32_t* err = reinterpret_cast<int32_t*>(static_cast<char*>(workspace) +
-                                            align_up(2 * n * sizeof(int32_t), 256));
-  SIDA_CUDA(cudaMemsetAsync(err, 0, sizeof(int32_t), s));
-  dim3 grid(n_tiles, n_layers);
-  hist_tiles_kernel<<<grid, kPermThreads, num_experts * sizeof(int32_t), s>>>(
-      ids, n_rows, num_experts, n_tiles, tile_counts, err);
-  SIDA_LAUNCH_CHECK();
-  scan_kernel<<<n_layers, 1024, 0, s>>>(tile_counts, num_experts, n_tiles, tile_base, hist, off);
-  SIDA_LAUNCH_CHECK();
-  if (n_rows > 0) {
-    size_t smem = (size_t)(1 + kPermWarps) * num_experts * sizeof(int32_t);
-    scatter_kernel<<<grid, kPermThreads, smem, s>>>(ids, n_rows, num_experts, n_tiles, tile_base,
-                                                    alpha_rows, perm, inv, alpha_perm);
-    SIDA_LAUNCH_CHECK();
+  const int tile = perm_tile(n_rows, n_layers);
+  const size_t n = (size_t)n_layers * num_experts * perm_tiles(n_rows, tile);
+  int32_t* counts = static_cast<int32_t*>(workspace);
+  int32_t* tile_base = counts + n;
+  switch (tile) {
+    case 1024: return permute_launch<1024>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
+                                           perm, inv, alpha_perm, counts, tile_base, err_flag, s);
+    case 2048: return permute_launch<2048>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
+                                           perm, inv, alpha_perm, counts, tile_base, err_flag, s);
+    case 4096: return permute_launch<4096>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
+                                           perm, inv, alpha_perm, counts, tile_base, err_flag, s);
+    default: return permute_launch<8192>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
+                                         perm, inv, alpha_perm, counts, tile_base, err_flag, s);
   }
-  return SIDA_OK;
 }
 
 // dst[p] = src[idx[p]] for bf16 rows (16-byte vectors): the expert-parallel

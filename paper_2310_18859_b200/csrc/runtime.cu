@@ -8,11 +8,16 @@
 #include <stdarg.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace sida {
 
 static thread_local char g_err[512] = {0};
+static std::atomic<unsigned long long> g_launches{0};
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -26,6 +31,10 @@ void set_error(const char* fmt, ...) {
 extern "C" int sida_abi_version(void) { return 1; }
 
 extern "C" const char* sida_last_error(void) { return sida::g_err; }
+
+extern "C" unsigned long long sida_launch_count(void) {
+  return sida::g_launches.load(std::memory_order_relaxed);
+}
 
 extern "C" int sida_device_check(int device) {
   cudaDeviceProp prop;

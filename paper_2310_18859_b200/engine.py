@@ -21,11 +21,15 @@ import torch
 from .errors import ContractError, UnservableError
 from .moe import BatchLayout, MoEModel
 from .offload import (
+    FFN_SLOT_MSG,
+    OUTPROJ_MSG,
+    PERMUTE_MSG,
     ExpertStore,
     MemoryBudget,
     ResidencyState,
     Wave,
     apply_group_inplace,
+    check_device_flags,
     plan_placement,
     plan_placement_spread,
     run_waves,
@@ -208,7 +212,7 @@ class SidaEngine:
         required, plan, waves = bp.required, bp.plan, bp.waves
         dt = table.on_device(model, stream=self.hash_stream)
         if tokens_dev is None:
-            tokens_dev = dt.tokens_for(model, batch)
+            tokens_dev = dt.tokens_for(model, batch, cs)
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         cs.wait_event(dt.ready)
@@ -296,6 +300,16 @@ class SidaEngine:
             "groups_issued_ahead": bp.early,
             "utilization": util,
         }
+
+    def check_errors(self, tables=()) -> None:
+        """Raise ContractError if a kernel flagged a contract violation since
+        the last check (synchronises; call where the host already waits)."""
+        flags = [(FFN_SLOT_MSG, self.store.err_flag), (OUTPROJ_MSG, self.model._err)]
+        for t in tables:
+            dt = getattr(t, "_dev", None)
+            if dt is not None:
+                flags.append((PERMUTE_MSG, dt.err))
+        check_device_flags(flags)
 
     # -- CUDA-graph replay ---------------------------------------------------------------
     def _graphable(self, bp: _BatchPlan, dt, lengths) -> bool:

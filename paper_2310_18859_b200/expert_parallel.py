@@ -255,6 +255,57 @@ class _LocalTable:
         return {(l, e) for l, s in enumerate(self._req) for e in s}
 
 
+class _GroupIssuer:
+    """Slot bookkeeping of one batch's plan, one group at a time, in plan
+    order (like SidaEngine._issue): group l is applied when layer l starts
+    (and group l+1 right after it when prefetchable, ref pipeline.py:246-253),
+    so an expert a later group evicts is still in its slot when its own layer
+    reads the slot row. Each load waits on its slot's last reader."""
+
+    def __init__(self, eng: "ExpertParallelEngine", plan, required):
+        self.eng, self.plan, self.required = eng, plan, required
+        self.issued = [False] * len(plan.groups)
+        self.done: list = [None] * len(plan.groups)
+
+    def _issue(self, idx: int) -> None:
+        eng = self.eng
+        g = self.plan.groups[idx]
+        eb = eng.model.expert_bytes_each()
+        apply_group_inplace(eng.state, g, eng.budget.fast_tier_bytes, eb)
+        eng.peak = max(eng.peak, eng.state.used_bytes)
+        loads = []
+        for op, key in g.steps:
+            if op == "evict":
+                eng.store.free_slot(key)
+            else:
+                loads.append((key, eng.store.take_slot(key)))
+        self.done[idx] = eng.store.enqueue_loads(loads)
+        self.issued[idx] = True
+
+    def issue_for(self, layer: int):
+        """Issue this layer's group (and the next one when prefetchable);
+        returns the done event of this layer's copies (or None)."""
+        if not self.issued[layer]:
+            self._issue(layer)
+        nxt = layer + 1
+        if nxt < len(self.plan.groups) and self.plan.groups[nxt].prefetchable and not self.issued[nxt]:
+            self._issue(nxt)
+        return self.done[layer]
+
+    def slot_row(self, layer: int) -> np.ndarray:
+        """Local expert -> slot of ``layer``, taken right before its FFN;
+        every expert the layer routes rows to must be resident."""
+        eng = self.eng
+        lo = eng.rank * eng.kl
+        row = np.full(eng.kl, -1, dtype=np.int32)
+        for e in self.required[layer]:
+            slot = eng.store.slot_of.get((layer, e))
+            if slot is None:
+                raise ContractError(f"plan/state mismatch: expert {(layer, e)} not resident")
+            row[e - lo] = slot
+        return row
+
+
 class ExpertParallelEngine:
     """SiDA serving with experts sharded over the ranks of ``group``.
 
@@ -289,7 +340,7 @@ class ExpertParallelEngine:
         cs = self.base.compute_stream
         dt = table.on_device(model, stream=self.base.hash_stream)
         if tokens_dev is None:
-            tokens_dev = dt.tokens_for(model, batch)
+            tokens_dev = dt.tokens_for(model, batch, cs)
         torch.cuda.current_stream(model.device).wait_event(dt.ready)
         counts = self.transport.all_gather(dt.hist).cpu().numpy().astype(np.int64)  # (G, L, K)
         local = _LocalTable(counts, self.rank, self.kl)
@@ -298,19 +349,10 @@ class ExpertParallelEngine:
             if any(k[0] == g.layer and k[1] in local.required_by_layer()[g.layer]
                    for k in g.evictions):
                 raise UnservableError("a layer's local expert working set exceeds the budget")
-        loads_by_layer = []
-        for g in plan.groups:
-            ls = []
-            for op, key in g.steps:
-                if op == "evict":
-                    store.free_slot(key)
-                else:
-                    ls.append((key, store.take_slot(key)))
-            loads_by_layer.append(ls)
+        issuer = _GroupIssuer(self, plan, local.required_by_layer())
         if getattr(self.transport, "peer", False):
-            return self._forward_peer(table, dt, counts, plan, loads_by_layer, lengths, tokens_dev)
+            return self._forward_peer(table, dt, counts, issuer, lengths, tokens_dev)
         # per-layer regroup maps and local offsets, uploaded once per batch
-        lo_e = self.rank * self.kl
         maps = [ep_regroup(counts, l, self.rank, self.world) for l in range(c.num_layers)]
         splits = [ep_splits(counts, l, self.rank, self.world) for l in range(c.num_layers)]
         k = dt.k
@@ -322,9 +364,7 @@ class ExpertParallelEngine:
             xb = None
             n_rows = x.shape[0] * k
             for layer in range(c.num_layers):
-                apply_group_inplace(self.state, plan.groups[layer], budget.fast_tier_bytes, eb)
-                self.peak = max(self.peak, self.state.used_bytes)
-                done = store.enqueue_loads(loads_by_layer[layer])
+                done = issuer.issue_for(layer)
                 x = model.attention_mix(layer, x, lay, xb=xb)
                 off_t, perm, alpha_perm = dt.layer(layer)
                 x_perm = torch.empty((n_rows, c.d_model), dtype=torch.bfloat16, device=x.device)
@@ -341,11 +381,7 @@ class ExpertParallelEngine:
                     x_loc = torch.empty((n_recv, c.d_model), dtype=torch.bfloat16, device=x.device)
                     _lib.check(h.sida_gather_bf16_rows(recv.data_ptr(), src_t.data_ptr(), n_recv,
                                                        c.d_model, x_loc.data_ptr(), cs.cuda_stream))
-                    row = np.full(self.kl, -1, dtype=np.int32)
-                    for e in range(self.kl):
-                        key = (layer, lo_e + e)
-                        if key in store.slot_of:
-                            row[e] = store.slot_of[key]
+                    row = issuer.slot_row(layer)
                     row_t = torch.from_numpy(row).pin_memory().to(x.device, non_blocking=True)
                     hidden = torch.empty((n_recv, c.expert_hidden), dtype=torch.bfloat16,
                                          device=x.device)
@@ -371,7 +407,7 @@ class ExpertParallelEngine:
         return logits
 
     # ------------------------------------------------------------------ peer memory
-    def _forward_peer(self, table, dt, counts, plan, loads_by_layer, lengths, tokens_dev):
+    def _forward_peer(self, table, dt, counts, issuer, lengths, tokens_dev):
         """The EP layer with both exchanges fused into the producing epilogues
         (PeerTransport): out-projection → owners' receive buffers (by layer
         parity) → flags → local grouped FFN whose GEMM2 epilogue writes into
@@ -386,7 +422,6 @@ class ExpertParallelEngine:
         rows_max = int(counts.sum(axis=2).max())  # largest (token, rank) count of any source
         if not tp.ready or rows_max > tp.cap_y:
             tp.setup(model, max(rows_max, getattr(tp, "cap_y", 0)) * 2)
-        lo_e = self.rank * self.kl
         dev = model.device
 
         def h2d(a):
@@ -399,9 +434,7 @@ class ExpertParallelEngine:
             x = model.embed_layout(lay)
             xb = None
             for layer in range(c.num_layers):
-                apply_group_inplace(self.state, plan.groups[layer], budget.fast_tier_bytes, eb)
-                self.peak = max(self.peak, self.state.used_bytes)
-                done = store.enqueue_loads(loads_by_layer[layer])
+                done = issuer.issue_for(layer)
                 d_start, d_val, r_start, r_val, off_l, n_recv = ep_peer_maps(
                     counts, layer, self.rank, self.world, tp.cap_x, tp.cap_y)
                 d_start_t, d_val_t = h2d(d_start), h2d(d_val)
@@ -420,11 +453,7 @@ class ExpertParallelEngine:
                     _lib.check(h.sida_segment_map(r_start_t.data_ptr(), r_val_t.data_ptr(),
                                                   self.kl * self.world, None, n_recv,
                                                   rmap.data_ptr(), cs.cuda_stream))
-                    row = np.full(self.kl, -1, dtype=np.int32)
-                    for e in range(self.kl):
-                        key = (layer, lo_e + e)
-                        if key in store.slot_of:
-                            row[e] = store.slot_of[key]
+                    row = issuer.slot_row(layer)
                     row_t, off_t = h2d(row), h2d(off_l)
                     hidden = torch.empty((n_recv, c.expert_hidden), dtype=torch.bfloat16,
                                          device=dev)

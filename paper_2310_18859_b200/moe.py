@@ -139,6 +139,65 @@ class Rng:
         return self._gen.permutation(x)
 
 
+def router_scores(x, w_r) -> np.ndarray:
+    """Softmax over the router's per-expert linear scores for one embedding
+    (ref moe.py:108-115), fp64 on the GPU (`sida_router_scores_f64`)."""
+    from .numkit import check_finite
+
+    x = check_finite(x, "router input")
+    w_r = np.asarray(w_r, dtype=np.float64)
+    if x.shape[0] != w_r.shape[0]:
+        raise ContractError(
+            f"dimension mismatch: x has {x.shape[0]}, router expects {w_r.shape[0]}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    xd = torch.from_numpy(np.ascontiguousarray(x.reshape(1, -1))).to(dev)
+    wd = torch.from_numpy(np.ascontiguousarray(w_r)).to(dev)
+    probs = torch.empty((1, w_r.shape[1]), dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().sida_router_scores_f64(xd.data_ptr(), 1, x.shape[0], wd.data_ptr(),
+                                                 w_r.shape[1], probs.data_ptr(),
+                                                 torch.cuda.current_stream().cuda_stream))
+    return probs.cpu().numpy()[0]
+
+
+def moe_layer_forward(x, selected, alphas, experts, eval_counts: np.ndarray | None = None
+                      ) -> np.ndarray:
+    """Weighted sum of the selected experts' MLP outputs for one embedding
+    (ref moe.py:118-146, Eq. 1), with the reference's contract checks: a
+    non-empty selection, ids in range, non-negative alphas. Only the selected
+    experts are uploaded and evaluated (`sida_moe_token_f64`, fp64);
+    ``eval_counts`` records each evaluation. No residual (the layer adds it)."""
+    w1, b1, w2, b2 = (np.asarray(a, dtype=np.float64) for a in experts)
+    num_experts = w1.shape[0]
+    selected = np.asarray(selected, dtype=np.int64)
+    alphas = np.asarray(alphas, dtype=np.float64)
+    if selected.size == 0:
+        raise ContractError("selected expert set is empty")
+    if np.any(selected < 0) or np.any(selected >= num_experts):
+        raise ContractError("expert index out of range")
+    if np.any(alphas < 0):
+        raise ContractError("scaling factors must be non-negative")
+    x = np.asarray(x, dtype=np.float64)
+    d, h = w1.shape[1], w1.shape[2]
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    sel = selected.reshape(-1)
+    xd, ad = up(x.reshape(-1)), up(alphas.reshape(-1))
+    w1d, b1d, w2d, b2d = up(w1[sel]), up(b1[sel]), up(w2[sel]), up(b2[sel])
+    hid = torch.empty((sel.size, h), dtype=torch.float64, device=dev)
+    out = torch.empty(w2.shape[2], dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().sida_moe_token_f64(
+        xd.data_ptr(), int(sel.size), ad.data_ptr(), w1d.data_ptr(), b1d.data_ptr(),
+        w2d.data_ptr(), b2d.data_ptr(), d, h, hid.data_ptr(), out.data_ptr(),
+        torch.cuda.current_stream().cuda_stream))
+    if eval_counts is not None:
+        for idx in sel:
+            eval_counts[idx] += 1
+    return out.cpu().numpy()
+
+
 def to_bf16(a: np.ndarray, device=None) -> torch.Tensor:
     """float64 -> float32 (RNE) -> bfloat16 (RNE): the one rounding recipe the
     GPU model and the parity oracle share (tests/test_oracle_golden.py)."""
@@ -589,6 +648,7 @@ def model_forward(model: MoEModel, batch: SequenceBatch, mode: str = "router", t
         t0 = time.perf_counter()
         logits, ids, al, pr = router_forward(model, lay, model.config.routing_k, store)
         out = logits.cpu().numpy().astype(np.float64)
+        _check_flags(model, store)
         if timings is not None:
             timings["forward"] = timings.get("forward", 0.0) + time.perf_counter() - t0
         trace = ActivationTrace(lengths=batch.lengths, selected=ids.cpu().numpy().astype(np.int64),
@@ -608,6 +668,14 @@ def model_forward(model: MoEModel, batch: SequenceBatch, mode: str = "router", t
         x = model.attention_mix(layer, x, lay)
         x = store.run_layer(model, layer, x, dev_table)
     logits = model.pool_classify(x, lay).cpu().numpy().astype(np.float64)
+    _check_flags(model, store, dev_table)
     trace = ActivationTrace(lengths=batch.lengths, selected=table.ids, alphas=table.alphas,
                             probs=None)
     return logits, trace
+
+
+def _check_flags(model: MoEModel, store, dev_table=None) -> None:
+    from .offload import FFN_SLOT_MSG, OUTPROJ_MSG, PERMUTE_MSG, check_device_flags
+
+    check_device_flags([(FFN_SLOT_MSG, store.err_flag), (OUTPROJ_MSG, model._err),
+                        (PERMUTE_MSG, dev_table.err if dev_table is not None else None)])

@@ -332,6 +332,29 @@ def memory_reduction(table, model) -> float:
 
 
 # ------------------------------------------------------------------------------------
+def check_device_flags(named_flags) -> None:
+    """Read the kernels' device-side contract flags at a point that already
+    synchronises and raise ContractError for any that is set (then clear
+    them). ``named_flags``: [(what went wrong, int32 device tensor or None)].
+    The flags are the grouped FFN's "routed expert without an HBM slot"
+    (the tile is skipped, its rows are garbage), the permute's "expert id out
+    of range" and the output projection's scatter flag."""
+    flags = [(n, f) for n, f in named_flags if f is not None]
+    if not flags:
+        return
+    vals = torch.cat([f.view(-1)[:1] for _, f in flags]).cpu().tolist()
+    bad = [n for (n, _), v in zip(flags, vals) if v]
+    if bad:
+        for _, f in flags:
+            f.zero_()
+        raise ContractError("device contract check failed: " + "; ".join(sorted(set(bad))))
+
+
+FFN_SLOT_MSG = "grouped FFN: a routed expert had no HBM slot (plan/slot mismatch)"
+PERMUTE_MSG = "permute: expert id out of range"
+OUTPROJ_MSG = "output projection: scatter contract violated"
+
+
 @dataclass
 class Wave:
     """Experts of one layer computed together: loads to enqueue first, then
@@ -378,7 +401,6 @@ class ExpertStore:
     stream) for the event recorded after the last FFN that read the slot.
     """
 
-    _full_cache: dict = {}
 
     def __init__(self, model, n_slots: int, copy_stream=None):
         if n_slots < 1:
@@ -401,13 +423,28 @@ class ExpertStore:
 
     @classmethod
     def full(cls, model) -> "ExpertStore":
-        """One store per model holding every expert (model_forward's default)."""
-        key = id(model)
-        st = cls._full_cache.get(key)
-        if st is None or st.model is not model:
+        """One store per model holding every expert (model_forward's default).
+        It lives on the model (released with it); ``release_full(model)``
+        frees its HBM arena earlier."""
+        st = getattr(model, "_full_store", None)
+        if st is None:
             c = model.config
             st = cls(model, c.num_layers * c.num_experts)
-            cls._full_cache[key] = st
+            model._full_store = st
+        return st
+
+    @staticmethod
+    def release_full(model) -> None:
+        model._full_store = None
+
+    @classmethod
+    def layer_cycling(cls, model) -> "ExpertStore":
+        """A store of one layer's worth of slots (num_experts) for passes that
+        visit the layers in order (the hit-rate router pass of serve_sida):
+        run_layer evicts the other layers' experts before loading, so the
+        arena stays at 1/L of the full one (base-128: 1.2 GB, not 14.5 GB)."""
+        st = cls(model, model.config.num_experts)
+        st.cycle_layers = True
         return st
 
     @classmethod
@@ -472,6 +509,9 @@ class ExpertStore:
         dev_table.ready.synchronize()
         st.wait_event(dev_table.ready)
         need = [int(e) for e in np.nonzero(table_hist[tl].cpu().numpy())[0]]
+        if getattr(self, "cycle_layers", False):
+            for key in [k for k in self.slot_of if k[0] != layer]:
+                self.free_slot(key)  # reuse waits on the slot's reader event
         loads = [((layer, e), self.take_slot((layer, e))) for e in need
                  if (layer, e) not in self.slot_of]
         done = self.enqueue_loads(loads)

@@ -147,6 +147,7 @@ class DeviceTable:
         self.k = k
         self.tokens = tokens        # int32 device tokens when built by the GPU hasher
         self.hist = self.off = self.perm = self.inv = self.alpha_perm = None
+        self.err = None             # int32 (1,): set by the permute on an out-of-range id
         self.ready = torch.cuda.Event()
 
     def permute(self, num_experts: int, stream) -> None:
@@ -160,10 +161,13 @@ class DeviceTable:
         self.alpha_perm = torch.empty((L, rows), dtype=torch.float32, device=dev)
         ws_bytes = h.sida_permute_workspace_bytes(L, rows, num_experts)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        with torch.cuda.stream(stream):
+            self.err = torch.zeros(1, dtype=torch.int32, device=dev)
         _lib.check(h.sida_permute_hist(
             self.ids.data_ptr(), L, rows, num_experts, self.alpha_f32.data_ptr(),
             self.hist.data_ptr(), self.off.data_ptr(), self.perm.data_ptr(), self.inv.data_ptr(),
-            self.alpha_perm.data_ptr(), ws.data_ptr(), ws_bytes, stream.cuda_stream))
+            self.alpha_perm.data_ptr(), self.err.data_ptr(), ws.data_ptr(), ws_bytes,
+            stream.cuda_stream))
         ws.record_stream(stream)
         self.ready.record(stream)
 
@@ -171,17 +175,23 @@ class DeviceTable:
         """Mark the table's buffers as in use on ``stream`` (caching-allocator
         safety when the table was built on another stream)."""
         for t in (self.ids, self.alpha, self.alpha_f32, self.hist, self.off, self.perm, self.inv,
-                  self.alpha_perm, self.tokens):
+                  self.alpha_perm, self.tokens, self.err):
             if t is not None:
                 t.record_stream(stream)
 
     def layer(self, layer: int):
         return self.off[layer], self.perm[layer], self.alpha_perm[layer]
 
-    def tokens_for(self, model: MoEModel, batch: SequenceBatch) -> torch.Tensor:
+    def tokens_for(self, model: MoEModel, batch: SequenceBatch, stream=None) -> torch.Tensor:
+        """The batch's int32 tokens on the device. A table built on the host
+        has none: they are copied on ``stream`` (the stream that will read
+        them; default the current one), so no other stream can race the copy."""
         if self.tokens is None:
             toks = model.validate_tokens(batch)
-            self.tokens = torch.from_numpy(toks).pin_memory().to(model.device, non_blocking=True)
+            st = stream or torch.cuda.current_stream(model.device)
+            with torch.cuda.stream(st):
+                self.tokens = torch.from_numpy(toks).pin_memory().to(model.device,
+                                                                     non_blocking=True)
         return self.tokens
 
 

@@ -100,6 +100,45 @@ def test_permute_max_size_properties(cuda_device):
     assert bool((dt.hist.long() == ref_hist).all())
 
 
+@pytest.mark.parametrize("L,N,K,skew", [(12, 262144, 256, 0.0), (12, 262144, 1024, 1.2),
+                                         (3, 100003, 128, 2.5)])
+def test_permute_c4_scale_bit_exact(cuda_device, L, N, K, skew):
+    """C4 sizes (SURVEY §8: up to 262,144 tokens x 12 layers, K up to 256;
+    K = 1024 is the kernel's limit) bit-exact against the stable argsort,
+    including heavily skewed routing (one expert owning most rows) and a row
+    count that is not a multiple of the tile or of 4 (unaligned layers)."""
+    g = np.random.default_rng(N + K)
+    if skew > 0:
+        p = 1.0 / np.arange(1, K + 1) ** skew
+        ids = g.choice(K, size=(L, N, 1), p=p / p.sum())
+    else:
+        ids = g.integers(0, K, size=(L, N, 1))
+    dt = _permute_gpu(ids, K)
+    flat = ids.reshape(L, N)
+    perm = np.argsort(flat, axis=1, kind="stable")
+    np.testing.assert_array_equal(dt.perm.cpu().numpy(), perm)
+    inv = np.empty_like(perm)
+    np.put_along_axis(inv, perm, np.arange(N)[None].repeat(L, 0), axis=1)
+    np.testing.assert_array_equal(dt.inv.cpu().numpy(), inv)
+    hist = np.stack([np.bincount(flat[l], minlength=K) for l in range(L)])
+    np.testing.assert_array_equal(dt.hist.cpu().numpy(), hist)
+    assert int(dt.err.item()) == 0
+
+
+def test_permute_flags_out_of_range_ids(cuda_device):
+    """An expert id outside [0, K) sets the permute's device flag; the next
+    synchronising check raises ContractError (ref moe.py:250-251 contract)."""
+    from paper_2310_18859_b200 import ContractError
+    from paper_2310_18859_b200.offload import PERMUTE_MSG, check_device_flags
+
+    ids = np.zeros((2, 100, 1), dtype=np.int64)
+    ids[1, 37, 0] = 9
+    dt = _permute_gpu(ids, 8)
+    with pytest.raises(ContractError, match="out of range"):
+        check_device_flags([(PERMUTE_MSG, dt.err)])
+    check_device_flags([(PERMUTE_MSG, dt.err)])  # cleared after raising
+
+
 def test_gather_rows(cuda_device):
     _l, h = _lib()
     N, k, d = 3000, 2, 768
