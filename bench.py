@@ -2,27 +2,32 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one serving batch (BASELINE.json configs[1]: Switch-base-8 shape,
-12 MoE layers, 8 experts, d=768, h=3072, top-1, bf16 experts with SiDA
-offload) of B x T synthetic tokens through the whole hot path: fp64 hash
-predictor + all-layer permute (hash stream, one batch ahead), residency plan
-and expert streaming (copy stream), then per layer mixing attention, row
-gather and the tcgen05 grouped expert FFN with the fused alpha/unpermute/
-residual epilogue, and the classifier head (compute stream). By default 86 of
-the 96 experts fit the HBM budget (--budget-frac 0.9) and the expert store uses
-the spread victim order (--victim-policy), so every step streams 12 experts
-from pinned host memory behind compute; --budget-frac 1.0 is the all-resident
-case.
+Workload (N = 1): Switch-base-128 shape (north_star target; larger than
+BASELINE configs[2]), 12 MoE layers, 128 experts, d=768, h=3072, top-1, bf16
+experts, SiDA serving with host-resident experts: every expert image lives in
+pinned host DRAM and only --budget-frac of them fit the HBM slot arena, so
+each step streams the experts its hash table asks for (hash-driven prefetch,
+one layer ahead) while the previous layers compute. A step is one serving
+batch of B x T synthetic tokens (256 x 128) through the whole hot path: fp64
+hash predictor + all-layer permute (hash stream, one batch ahead), residency
+plan + expert copies (copy stream), and per layer the fused QKV projection,
+attention core, output projection with the expert-sorted scatter, and the
+tcgen05 grouped expert FFN with the alpha/unpermute/residual epilogue, then
+the classifier head (compute stream) -- every kernel from this repo's library.
 
-  value  device-resident tokens, K steps timed with CUDA events on the
-         compute stream, max over ranks; whole-job tokens/s
-  e2e    the public API `serve_sida` on host `SequenceBatch`es (H2D of
-         tokens, D2H of logits inside the timed region), wall clock
-  --impl reference: the CPU oracle port of the reference algorithm on this
-         host (bounded per-step sample, see `cpu_sample`)
+  value    device-resident tokens, K steps timed with CUDA events on the
+           compute stream (barrier + synchronize on both sides), max over
+           ranks, whole-job tokens/s
+  e2e      the public API `serve_sida` on host `SequenceBatch`es (H2D of
+           tokens, D2H of logits inside the timed region), wall clock
+  --impl reference: the reference algorithm (CPU oracle port) on this host's
+           cores, the same 12-layer workload end to end, one sequence per step
 
-Under torchrun each rank serves its own batch stream with a full replica of
-the model (data-parallel replicas; the per-GPU work is fixed: weak scaling).
+N > 1 (torchrun, one process per GPU): expert parallelism over NCCL
+(--parallel ep, default): rank r owns experts [r K/N, (r+1) K/N) of every
+layer, serves its own batch stream, and exchanges token rows per layer with
+NCCL all-to-all (weak scaling: per-GPU tokens fixed). --parallel dp runs
+independent replicas instead.
 """
 
 from __future__ import annotations
@@ -39,8 +44,9 @@ import numpy as np
 REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
-BASE8 = dict(vocab_size=32128, d_model=768, num_layers=12, num_experts=8, expert_hidden=3072,
-             max_seq_len=512, routing_k=1, num_classes=2)
+SWITCH = dict(vocab_size=32128, d_model=768, num_layers=12, expert_hidden=3072,
+              max_seq_len=512, routing_k=1, num_classes=2)
+ZIPF_A = 1.1  # ref corpus.py CorpusSpec.zipf_a default
 
 
 def parse():
@@ -49,27 +55,23 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--batch", type=int, default=256, help="sequences per serving batch")
+    p.add_argument("--batch", type=int, default=256, help="sequences per serving batch (per GPU)")
     p.add_argument("--seq", type=int, default=128, help="tokens per sequence")
-    p.add_argument("--experts", type=int, default=8)
-    p.add_argument("--budget-frac", type=float, default=0.9,
-                   help="HBM expert budget as a fraction of all expert bytes (SiDA offload: "
-                        "the default keeps 86 of base-8's 96 experts in HBM)")
+    p.add_argument("--experts", type=int, default=128)
+    p.add_argument("--budget-frac", type=float, default=0.97,
+                   help="HBM expert budget as a fraction of all (local) expert bytes")
     p.add_argument("--victim-policy", default="spread", choices=["fifo", "spread"],
                    help="expert-store victim order: the reference's FIFO classes or the "
-                        "opt-in spread order (identical logits; copies hidden at 90 %%)")
+                        "opt-in spread order (identical logits)")
+    p.add_argument("--parallel", default="auto", choices=["auto", "dp", "ep"],
+                   help="N>1: expert parallel over NCCL (auto/ep) or data-parallel replicas")
+    p.add_argument("--ep-transport", default="nccl", choices=["nccl", "peer"])
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-steps", type=int, default=8,
-                   help="CPU oracle sample size (sequences); ~1.3 s of CPU work each")
-    p.add_argument("--parallel", default="dp", choices=["dp", "ep"],
-                   help="N>1: data-parallel replicas (default) or expert parallel over NCCL")
-    p.add_argument("--ep-transport", default="nccl", choices=["nccl", "peer"],
-                   help="--parallel ep data exchange: NCCL all-to-all or the epilogue-fused "
-                        "peer-memory path (CUDA IPC / NVLink mappings)")
-    p.add_argument("--no-north-star", action="store_true",
-                   help="skip the base-128 grouped-FFN roofline measurement")
-    p.add_argument("--no-streaming", action="store_true",
-                   help="skip the H2D-link / budget-limited streaming measurement")
+    p.add_argument("--cpu-seqs", type=int, default=2,
+                   help="CPU oracle sample: sequences through the full 12-layer forward")
+    p.add_argument("--no-extras", action="store_true",
+                   help="skip the side measurements (streaming, Zipf regime, north-star "
+                        "FFN shapes, permute/hash/attention rooflines)")
     return p.parse_args()
 
 
@@ -80,47 +82,88 @@ def dist_env():
     return ws, rank, local
 
 
-# ----------------------------------------------------------------------------- CPU oracle
-def cpu_sample(cfg: dict, seq: int, steps: int, seed: int = 0):
-    """Time the oracle (numpy port of the reference algorithm) on this host.
+def workload_name(args, ws, ep):
+    return (f"Switch-base-{args.experts} SiDA serving, 12 layers, bf16, host-resident experts "
+            f"streamed by hash-driven prefetch (HBM budget {args.budget_frac:.2f} of the "
+            f"{'rank-local ' if ep else ''}experts), {ws} B200"
+            + (f", expert-parallel over {ws} ranks (BASELINE configs[3])" if ep else
+               " (north-star shape; BASELINE configs[2] family)"))
 
-    Per step: one sequence of ``seq`` tokens through the reference's
-    `build_hash_table` (all 12 layer heads) and ONE MoE layer
-    (`attention_mix` + `moe_apply`, gathered per-token einsum exactly like ref
-    moe.py:252-259) at the full Switch-base shape; the step's tokens/s is
-    seq / (t_hash + L * t_layer), i.e. the 12-layer forward is extrapolated
-    from one layer because the float64 experts of the remaining layers are
-    never materialised. Returns (tokens_per_s, seconds of CPU work, detail)."""
+
+# ----------------------------------------------------------------------------- CPU oracle
+class RefWeights:
+    """Float64 weights for the reference algorithm at the Switch shape without
+    materialising L*K*(2dh) doubles (58 GB at base-128): every expert matrix is
+    a distinct strided window of one 3 GB random buffer (experts of a layer
+    never overlap; layers are shifted), so each gathered expert is a DRAM
+    read like the real thing. Values do not matter for timing."""
+
+    def __init__(self, cfg: dict, seed: int = 0):
+        d, h, K, L = cfg["d_model"], cfg["expert_hidden"], cfg["num_experts"], cfg["num_layers"]
+        g = np.random.default_rng(seed)
+        n = 384 * 1024 * 1024  # doubles (3 GB)
+        self.base = g.standard_normal(n, dtype=np.float32).astype(np.float64)
+        self.base *= np.sqrt(2.0 / (d + h))
+        stride = (n - d * h) // K
+        assert stride >= d * h, "buffer too small for disjoint experts"
+        ast = np.lib.stride_tricks.as_strided
+        self.params = {"tok_emb": g.normal(0, 1 / np.sqrt(d), (cfg["vocab_size"], d)),
+                       "pos_emb": g.normal(0, 1 / np.sqrt(d), (cfg["max_seq_len"], d)),
+                       "wc": g.normal(0, 1 / np.sqrt(d), (d, cfg["num_classes"]))}
+        shift = (n - d * h - (K - 1) * stride) // max(L, 1)
+        for layer in range(L):
+            pre = f"block{layer}."
+            for nm in ("wq", "wk", "wv", "wo"):
+                self.params[pre + nm] = g.normal(0, np.sqrt(1 / d), (d, d))
+            o1 = layer * shift
+            o2 = (layer * shift + stride // 2) % max(1, n - d * h - (K - 1) * stride)
+            self.params[pre + "w1"] = ast(self.base[o1:], (K, d, h), (stride * 8, h * 8, 8),
+                                          writeable=False)
+            self.params[pre + "w2"] = ast(self.base[o2:], (K, h, d), (stride * 8, d * 8, 8),
+                                          writeable=False)
+            self.params[pre + "b1"] = np.zeros((K, h))
+            self.params[pre + "b2"] = np.zeros((K, d))
+
+
+def cpu_reference_steps(cfg: dict, seq: int, n_steps: int, threads: int, seed: int = 0):
+    """Per step: one sequence of ``seq`` tokens through the reference
+    algorithm end to end -- `build_hash_table` over all L layer heads
+    (ref predictor.py:373-399), then the 12-layer external-table forward
+    (embed, attention_mix, moe_apply with the per-token gathered einsum of
+    ref moe.py:252-259, pool_classify). moe_apply's token chunks run on
+    ``threads`` host threads (per-token arithmetic unchanged; numpy releases
+    the GIL inside einsum). Returns per-step seconds."""
+    from concurrent.futures import ThreadPoolExecutor
+
     from oracle import moe as omoe
     from oracle import predictor as opred
 
-    g = np.random.default_rng(seed)
-    d, h, K, L = cfg["d_model"], cfg["expert_hidden"], cfg["num_experts"], cfg["num_layers"]
-    shape = omoe.MoEShape(**{**cfg, "num_layers": 1})
-    params = {"tok_emb": g.normal(0, 1 / np.sqrt(d), (cfg["vocab_size"], d)),
-              "pos_emb": g.normal(0, 1 / np.sqrt(d), (cfg["max_seq_len"], d))}
-    for n in ("wq", "wk", "wv", "wo"):
-        params["block0." + n] = g.normal(0, np.sqrt(1 / d), (d, d))
-    params["block0.w1"] = g.normal(0, np.sqrt(2 / (d + h)), (K, d, h))
-    params["block0.b1"] = np.zeros((K, h))
-    params["block0.w2"] = g.normal(0, np.sqrt(2 / (d + h)), (K, h, d))
-    params["block0.b2"] = np.zeros((K, d))
-    pparams = opred.init_params(opred.PredictorShape(d, L, K), 1)
+    w = RefWeights(cfg, seed)
+    params = w.params
+    L, K = cfg["num_layers"], cfg["num_experts"]
+    shape = omoe.MoEShape(**cfg)
+    pparams = opred.init_params(opred.PredictorShape(cfg["d_model"], L, K), 1)
     emb = lambda t: omoe.embed(params, shape, t)  # noqa: E731
-    rates, work = [], 0.0
-    for _ in range(steps):
-        toks = g.integers(0, cfg["vocab_size"], size=seq)
-        t0 = time.perf_counter()
-        ids, alphas = opred.build_hash_table(pparams, [toks], 1, emb)
-        t1 = time.perf_counter()
-        x = omoe.attention_mix(params, shape, 0, emb(toks))
-        omoe.moe_apply(params, 0, x, ids[0], alphas[0])
-        t2 = time.perf_counter()
-        work += t2 - t0
-        rates.append(seq / ((t1 - t0) + L * (t2 - t1)))
-    detail = f"{steps} step(s) x 1 sequence of {seq} tokens: hash over {L} layer heads + 1 of {L} " \
-             f"MoE layers (attention_mix + gathered moe_apply), 12-layer forward extrapolated x{L}"
-    return float(np.mean(rates)), work, detail
+    g = np.random.default_rng(seed + 7)
+    times = []
+    chunk = 16
+    with ThreadPoolExecutor(threads) as ex:
+        for _ in range(n_steps):
+            toks = g.integers(0, cfg["vocab_size"], size=seq)
+            t0 = time.perf_counter()
+            ids, alphas = opred.build_hash_table(pparams, [toks], 1, emb)
+            x = emb(toks)
+            for layer in range(L):
+                x = omoe.attention_mix(params, shape, layer, x)
+                xa = x
+                parts = list(ex.map(
+                    lambda s, xa=xa, layer=layer: omoe.moe_apply(
+                        params, layer, xa[s:s + chunk], ids[layer, s:s + chunk],
+                        alphas[layer, s:s + chunk]), range(0, seq, chunk)))
+                x = np.concatenate(parts)
+            omoe.pool_classify(params, x)
+            times.append(time.perf_counter() - t0)
+    return times
 
 
 def blas_threads():
@@ -134,34 +177,37 @@ def blas_threads():
 
 def run_reference(args):
     ws, rank, _ = dist_env()
-    cfg = dict(BASE8, num_experts=args.experts)
     if rank != 0:
         return
-    total_tok, total_t = 0, 0.0
-    detail = ""
-    for i in range(args.warmup + args.steps):
-        rate, work, detail = cpu_sample(cfg, args.seq, 1, seed=100 + i)
-        if i >= args.warmup:
-            total_tok += args.seq
-            total_t += args.seq / rate
-    value = total_tok / total_t
+    cfg = dict(SWITCH, num_experts=args.experts)
+    threads = os.cpu_count() or 1
+    times = cpu_reference_steps(cfg, args.seq, args.warmup + args.steps, threads)
+    timed = times[args.warmup:]
+    total = float(np.sum(timed))
+    value = args.steps * args.seq / total
+    sample = (f"per step 1 sequence of {args.seq} tokens through the reference algorithm end to "
+              f"end: hash over all {cfg['num_layers']} layer heads + the {cfg['num_layers']}-layer "
+              f"external forward (gathered per-token moe_apply, ref moe.py:252-259), moe_apply "
+              f"token chunks on {threads} threads; float64 experts are strided windows of one "
+              f"3 GB buffer (58 GB would not fit host RAM)")
     line = {
-        "impl": "reference", "metric": "MoE inference tokens/sec (SiDA serving, base-8)",
+        "impl": "reference", "metric": "MoE inference tokens/sec (SiDA serving)",
         "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic tokens, random-init Switch-base-8-shaped weights",
-        "config": {"workload": "Switch-base-8 SiDA serving with expert offload, 12 layers, "
-                               "bf16, 1 B200 (BASELINE configs[1])", "global_batch": args.batch * max(ws, 1),
-                   "seq_len": args.seq, "tokens_per_step_per_gpu": args.batch * args.seq,
-                   "layers": cfg["num_layers"], "experts": cfg["num_experts"],
-                   "d_model": cfg["d_model"], "expert_hidden": cfg["expert_hidden"],
-                   "top_k": 1, "parallelism": "cpu (reference algorithm, numpy f64)",
-                   "sample_per_step": f"1 sequence of {args.seq} tokens (see cpu_baseline)"},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": os.cpu_count(),
-                         "blas_threads": blas_threads(), "kind": "port", "sample": detail},
+        "data": "synthetic uniform tokens, random Switch-shaped weights",
+        "config": {"workload": workload_name(args, ws, ws > 1 and args.parallel != "dp"),
+                   "global_batch": args.batch * max(ws, 1), "seq_len": args.seq,
+                   "tokens_per_step_per_gpu": args.batch * args.seq, "layers": cfg["num_layers"],
+                   "experts": cfg["num_experts"], "d_model": cfg["d_model"],
+                   "expert_hidden": cfg["expert_hidden"], "top_k": 1,
+                   "parallelism": "cpu (reference algorithm, numpy f64)",
+                   "sample_per_step": f"1 sequence of {args.seq} tokens, 12 layers end to end"},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
+                         "blas_threads": blas_threads(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "wall_s_timed": total,
     }
     print(json.dumps(line), flush=True)
 
@@ -180,8 +226,7 @@ class ClockSampler:
         self.samples: list[tuple[int, int, int]] = []
         self._stop = threading.Event()
         self._t = None
-        # NVML init takes tens of ms: do it here, outside the timed region
-        try:
+        try:  # NVML init takes tens of ms: do it here, outside the timed region
             import pynvml
 
             pynvml.nvmlInit()
@@ -231,19 +276,58 @@ def measured_peaks():
         return {}
 
 
-def measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms, steps=3,
-                      fracs=(0.9, 0.75, 0.5)):
-    """Expert streaming evidence: the pinned-host -> HBM link
-    measured with the engine's own copy entry point (sida_expert_copy), and
-    budget-limited serving runs (90 / 75 / 50 % of the experts fit, so every
-    batch streams the experts FIFO-evicted during the previous one) whose step
-    times are compared with an all-resident run through the same loop
-    (budget 1.0): exposed = budget step - that step; "fully hidden" =
-    exposed ~ 0 while copy time > 0."""
+def tensor_peak(peaks: dict, clocks: dict | None) -> tuple[float, str]:
+    """The bf16 peak that matches the clocks the measurement ran at: the burst
+    figure (measured at max clocks) when the median SM clock under load was
+    within 5 % of max, else the sustained one (measured at a power-capped
+    ~1327 MHz median)."""
+    burst = peaks.get("bf16_tflops", 1638.8)
+    sus = peaks.get("bf16_tflops_sustained", 1380.0)
+    if clocks and clocks.get("sm_mhz") and clocks.get("sm_max_mhz"):
+        if clocks["sm_mhz"] >= 0.95 * clocks["sm_max_mhz"]:
+            return burst, "MEASURED_PEAKS.json bf16_tflops (burst; clocks at max)"
+        return sus, "MEASURED_PEAKS.json bf16_tflops_sustained (clocks below max)"
+    return burst, "MEASURED_PEAKS.json bf16_tflops (burst)"
+
+
+def synth_tokens(n, vocab, gen, zipf=False, device="cuda"):
     import torch
 
-    from paper_2310_18859_b200 import MemoryBudget, _lib
-    from paper_2310_18859_b200.engine import SidaEngine
+    if not zipf:
+        return torch.randint(0, vocab, (n,), generator=gen, device=device, dtype=torch.int32)
+    # Zipf(a) over the vocabulary, the marginal of ref corpus.py generate_corpus
+    w = 1.0 / torch.arange(1, vocab + 1, device=device, dtype=torch.float64) ** ZIPF_A
+    return torch.multinomial(w / w.sum(), n, replacement=True, generator=gen).to(torch.int32)
+
+
+def run_stream(engine, toks, lengths, steps, warmup):
+    """The device-resident pipeline: hash(j+1) on the hash stream overlaps
+    forward(j). Returns (ms per timed step from CUDA events on the compute
+    stream, the tables of the timed batches)."""
+    import torch
+
+    cs = engine.compute_stream
+    tables = {0: engine.hash_tokens(0, toks[0], lengths)}
+    timed = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for j in range(warmup + steps):
+        if j == warmup:
+            torch.cuda.synchronize()
+            e0.record(cs)
+        tables[j + 1] = engine.hash_tokens(j + 1, toks[(j + 1) % len(toks)], lengths)
+        t = tables.pop(j)
+        engine.forward(t, lengths, tokens_dev=toks[j % len(toks)], next_table=tables[j + 1])
+        if j >= warmup:
+            timed.append(t)
+    e1.record(cs)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps, timed
+
+
+def h2d_link_gbs(model):
+    import torch
+
+    from paper_2310_18859_b200 import _lib
 
     h = _lib.lib()
     eb = model.expert_bytes_each()
@@ -255,72 +339,81 @@ def measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms, steps=3,
         if it == 1:
             e0.record(cs)
         for i in range(8):
-            src = model.expert_images[i]
-            _lib.check(h.sida_expert_copy(dst.data_ptr() + i * eb, src.data_ptr(), eb,
-                                          cs.cuda_stream, None, None))
+            _lib.check(h.sida_expert_copy(dst.data_ptr() + i * eb,
+                                          model.expert_images[i].data_ptr(), eb, cs.cuda_stream,
+                                          None, None))
     e1.record(cs)
     torch.cuda.synchronize()
-    h2d_gbs = reps * 8 * eb / (e0.elapsed_time(e1) / 1e3) / 1e9
+    return reps * 8 * eb / (e0.elapsed_time(e1) / 1e3) / 1e9
+
+
+def budget_runs(model, pred, cfg, lengths, runs, steps=4, zipf=False, seed=0):
+    """Serving runs through one loop at several HBM budgets (fraction of all
+    experts): ms/step, expert loads per step, exposed copy time against the
+    first run (budget 1.0, every expert resident after warm-up), and the
+    SiDA memory metrics of the reference: `memory_reduction` (ref
+    offload.py:292-300, 1 - a batch's required experts / all experts, mean
+    over the timed batches), `effective_utilization` (ref offload.py:281-289,
+    resident bytes the last batch used / resident bytes) and the HBM expert
+    footprint (peak slots)."""
+    import torch
+
+    from paper_2310_18859_b200 import MemoryBudget, memory_reduction
+    from paper_2310_18859_b200.engine import SidaEngine
+
+    eb = model.expert_bytes_each()
     n_all = cfg.num_layers * cfg.num_experts
-    runs = []
-    for frac, depth, policy in ([(1.0, 1, "fifo")] + [(f, 1, "fifo") for f in fracs]
-                                + [(f, 1, "spread") for f in fracs]):
-        xbatch = False
+    n_tok = sum(lengths)
+    g = torch.Generator(device=model.device)
+    g.manual_seed(4321 + seed)
+    toks = [synth_tokens(n_tok, cfg.vocab_size, g, zipf=zipf) for _ in range(steps + 3)]
+    out = []
+    for frac, policy in runs:
         slots = max(1, int(round(frac * n_all)))
         eng = SidaEngine(model, pred, MemoryBudget(slots * eb), eval_top_k=1,
                          victim_policy=policy)
-        eng.depth = depth
-        tables = {0: eng.hash_tokens(0, toks[0], lengths)}
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        loads0 = 0
-        for j in range(steps + 2):
-            if j == 2:  # two warm batches: the FIFO state reaches its steady cycle
-                torch.cuda.synchronize()
-                loads0 = eng.store.bytes_loaded
-                s0.record(eng.compute_stream)
-            tables[j + 1] = eng.hash_tokens(j + 1, toks[(j + 1) % len(toks)], lengths)
-            eng.forward(tables.pop(j), lengths, tokens_dev=toks[j % len(toks)],
-                        next_table=tables[j + 1] if xbatch else None)
-        s1.record(eng.compute_stream)
-        torch.cuda.synchronize()
-        b_ms = s0.elapsed_time(s1) / steps
+        run_stream(eng, toks, lengths, 2, 1)  # reach the steady residency cycle
+        loads0 = eng.store.bytes_loaded
+        ms, tabs = run_stream(eng, toks, lengths, steps, 0)
         loaded = (eng.store.bytes_loaded - loads0) / steps
-        runs.append({"budget_frac": frac, "budget_slots": slots, "prefetch_depth": depth,
-                     "victim_policy": policy,
-                     "tokens_per_s": n_tok / (b_ms / 1e3), "ms_per_step": b_ms,
-                     "expert_loads_per_step": loaded / eb,
-                     "copy_ms_at_link_rate": loaded / (h2d_gbs * 1e9) * 1e3,
-                     "exposed_ms_per_step": b_ms - (runs[0]["ms_per_step"] if runs else b_ms)})
-        del eng
+        mr = [memory_reduction(t, model) for t in tabs]
+        st = eng.state
+        act = tabs[-1].required_experts()
+        util = (sum(st.resident.get(k, 0) for k in act) / st.used_bytes
+                if st.used_bytes else 1.0)
+        out.append({"budget_frac": frac, "budget_slots": slots, "victim_policy": policy,
+                    "ms_per_step": ms, "tokens_per_s": n_tok / (ms / 1e3),
+                    "expert_loads_per_step": loaded / eb,
+                    "copy_ms_per_step_at_link": None,
+                    "hbm_expert_footprint_bytes": eng.store.peak_slots * eb,
+                    "footprint_frac_of_all_experts": eng.store.peak_slots / n_all,
+                    "memory_reduction_per_batch": float(np.mean(mr)),
+                    "effective_utilization": util,
+                    "exposed_ms_per_step": ms - (out[0]["ms_per_step"] if out else ms)})
+        eng.check_errors(tabs)
+        del eng, tabs
         torch.cuda.empty_cache()
-    return {"h2d_link_gbs": h2d_gbs, "h2d_source": "pinned host -> HBM, 8 expert images x 4 "
-            "via sida_expert_copy on one stream", "all_resident_ms_per_step": step_ms,
-            "budgets": runs,
-            "note": "the predictor's routing activates every expert of every layer in every "
-                    "32K-token batch; with a budget below the working set the reference planner "
-                    "(victim_policy fifo) evicts the oldest experts the batch has consumed, "
-                    "which the next batch needs first, so its loads pile onto the first layers; "
-                    "victim_policy spread (offload.plan_placement_spread, opt-in, not the "
-                    "reference's plan) keeps about one load per layer, issued a layer ahead"}
+    return out
 
 
-def measure_ffn_shape(experts: int, n_tok: int, peaks: dict, iters: int = 10) -> dict:
+def measure_ffn_shape(experts: int, n_tok: int, peak_t: float, peak_b: float,
+                      iters: int = 10) -> dict:
     """One Switch-shaped MoE layer with `experts` experts at `n_tok` tokens
-    (uniform random routing, every expert resident): the grouped FFN (GEMM1 +
-    GEMM2) timed with CUDA events on the launching stream against SURVEY
-    §8(d)'s roofline max(4 d h N / bf16 sustained, min bytes / HBM)."""
+    (uniform ids, SURVEY §8(d) seed 3, every expert resident): the grouped FFN
+    (GEMM1 + GEMM2) timed with CUDA events on the launching stream against
+    SURVEY §8(d)'s roofline max(4 d h N / tensor peak, min bytes / HBM)."""
     import torch
 
     from paper_2310_18859_b200 import MoEConfig, MoEModel
     from paper_2310_18859_b200.offload import ExpertStore, Wave, run_waves
     from paper_2310_18859_b200.predictor import DeviceTable
 
-    cfg = MoEConfig(**dict(BASE8, num_layers=1, num_experts=experts, vocab_size=64,
+    cfg = MoEConfig(**dict(SWITCH, num_layers=1, num_experts=experts, vocab_size=64,
                            max_seq_len=16))
     model = MoEModel.synthetic(cfg, 0)
     store = ExpertStore.full(model)
     g = torch.Generator(device="cuda")
-    g.manual_seed(3)  # SURVEY §8(d): balanced synthetic ids, seed 3
+    g.manual_seed(3)
     ids = torch.randint(0, experts, (1, n_tok, 1), device="cuda", dtype=torch.int32, generator=g)
     al = torch.rand((1, n_tok, 1), device="cuda", dtype=torch.float64, generator=g)
     dt = DeviceTable(ids, al, al.float(), n_tok, 1)
@@ -345,33 +438,124 @@ def measure_ffn_shape(experts: int, n_tok: int, peaks: dict, iters: int = 10) ->
     d_, h_ = cfg.d_model, cfg.expert_hidden
     flops = 4.0 * n_tok * d_ * h_
     min_bytes = len(need) * (2 * d_ * h_ + h_ + d_) * 2 + 3.0 * n_tok * d_ * 2
-    t_tensor = flops / (peaks.get("bf16_tflops_sustained", 1373.4) * 1e12) * 1e3
-    t_hbm = min_bytes / (peaks.get("hbm_gbs", 6549.4) * 1e9) * 1e3
+    t_tensor = flops / (peak_t * 1e12) * 1e3
+    t_hbm = min_bytes / (peak_b * 1e9) * 1e3
     out = {"experts": experts, "tokens": n_tok, "rows_per_expert": n_tok / experts,
-           "avg_ms": avg_ms, "tflops": flops / (avg_ms / 1e3) / 1e12,
-           "tensor_ms": t_tensor, "hbm_ms": t_hbm,
-           "bound": "tensor" if t_tensor >= t_hbm else "hbm",
+           "avg_ms": avg_ms, "tflops": flops / (avg_ms / 1e3) / 1e12, "tensor_ms": t_tensor,
+           "hbm_ms": t_hbm, "bound": "tensor" if t_tensor >= t_hbm else "hbm",
            "frac": max(t_tensor, t_hbm) / avg_ms}
     del model, store, dt, x
     torch.cuda.empty_cache()
     return out
 
 
+def measure_permute(L: int, N: int, K: int, peak_b: float, d: int = 768, iters: int = 10):
+    """sida_permute_hist over all L layers (+ the bf16 row gather of one layer,
+    fp32 x -> x_perm, the materialised-x_perm case of SURVEY §8(d)) timed with
+    CUDA events. Algorithmic bytes: ids read 4, perm 4 and inv 4 written, alpha
+    read 4 and alpha_perm 4 written per row and layer, + 8K (hist, off); the
+    gather reads 4d and writes 2d bytes per row."""
+    import torch
+
+    from paper_2310_18859_b200 import _lib
+    from paper_2310_18859_b200.predictor import DeviceTable
+
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    ids = torch.randint(0, K, (L, N, 1), device="cuda", dtype=torch.int32, generator=g)
+    al = torch.rand((L, N, 1), device="cuda", dtype=torch.float64, generator=g)
+    dt = DeviceTable(ids, al, al.float(), N, 1)
+    st = torch.cuda.current_stream()
+    x = torch.randn(N, d, device="cuda", generator=g)
+    xp = torch.empty((N, d), dtype=torch.bfloat16, device="cuda")
+    h = _lib.lib()
+    for _ in range(2):
+        dt.permute(K, st)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    torch.cuda.synchronize()
+    ev[0].record(st)
+    for _ in range(iters):
+        dt.permute(K, st)
+    ev[1].record(st)
+    for _ in range(iters):
+        _lib.check(h.sida_gather_rows_bf16(x.data_ptr(), dt.perm[0].data_ptr(), N, 1, d,
+                                           xp.data_ptr(), st.cuda_stream))
+    ev[2].record(st)
+    torch.cuda.synchronize()
+    t_perm = ev[0].elapsed_time(ev[1]) / iters
+    t_gat = ev[1].elapsed_time(ev[2]) / iters
+    b_perm = L * (20.0 * N + 8 * K)
+    b_gat = 6.0 * N * d
+    return {"layers": L, "rows": N, "experts": K,
+            "permute_ms": t_perm, "permute_bytes": b_perm, "permute_gbs": b_perm / t_perm / 1e6,
+            "permute_frac": b_perm / t_perm / 1e6 / peak_b,
+            "gather_ms": t_gat, "gather_bytes": b_gat, "gather_gbs": b_gat / t_gat / 1e6,
+            "gather_frac": b_gat / t_gat / 1e6 / peak_b,
+            "combined_frac": (b_perm + b_gat) / (t_perm + t_gat) / 1e6 / peak_b}
+
+
+def measure_hash(model, pred, n_seq: int, seq: int, iters: int = 5):
+    """The fp64 hash predictor + permute for one batch, alone on one stream
+    (CUDA events): latency-bound (T sequential LSTM steps), reported in
+    tokens/s and as HBM bytes (token ids, embedding rows, table writes)."""
+    import torch
+
+    from paper_2310_18859_b200.predictor import hash_device
+
+    n = n_seq * seq
+    g = torch.Generator(device="cuda")
+    g.manual_seed(10)
+    toks = torch.randint(0, model.config.vocab_size, (n,), device="cuda", dtype=torch.int32,
+                         generator=g)
+    st = torch.cuda.current_stream()
+    lengths = [seq] * n_seq
+    for _ in range(2):
+        hash_device(pred, model, toks, lengths, 1, 0, st)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(iters):
+        hash_device(pred, model, toks, lengths, 1, 0, st)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    c = model.config
+    byts = n * 4 + n * c.d_model * 2 + c.num_layers * n * (4 + 8 + 4)
+    return {"tokens": n, "ms": ms, "tokens_per_s": n / (ms / 1e3), "bytes": byts,
+            "gbs": byts / ms / 1e6}
+
+
+def build_engine(args, model, pred, ws, ep):
+    from paper_2310_18859_b200 import MemoryBudget
+    from paper_2310_18859_b200.engine import SidaEngine
+
+    cfg = model.config
+    eb = model.expert_bytes_each()
+    n_local = cfg.num_layers * cfg.num_experts // (ws if ep else 1)
+    slots = max(1, int(round(args.budget_frac * n_local)))
+    budget = MemoryBudget(slots * eb)
+    if ep:
+        from paper_2310_18859_b200.expert_parallel import (ExpertParallelEngine, GlooTransport,
+                                                           PeerTransport)
+
+        share = os.environ.get("SIDA_BENCH_SHARE_GPU") == "1"
+        if share:  # gloo plumbing (collectives staged through host memory)
+            transport = (PeerTransport(control=GlooTransport()) if args.ep_transport == "peer"
+                         else GlooTransport())
+        else:
+            transport = PeerTransport() if args.ep_transport == "peer" else None
+        return ExpertParallelEngine(model, pred, budget, transport=transport,
+                                    victim_policy=args.victim_policy), budget, slots
+    return SidaEngine(model, pred, budget, eval_top_k=1,
+                      victim_policy=args.victim_policy), budget, slots
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2310_18859_b200 import (
-        MemoryBudget,
-        MoEConfig,
-        MoEModel,
-        PredictorConfig,
-        PredictorNet,
-        Rng,
-        SequenceBatch,
-        serve_sida,
-    )
-    from paper_2310_18859_b200.engine import SidaEngine
+    from paper_2310_18859_b200 import (MoEConfig, MoEModel, PredictorConfig, PredictorNet, Rng,
+                                       SequenceBatch, _lib, serve_sida)
 
     ws, rank, local = dist_env()
     # SIDA_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo plumbing -- a
@@ -383,216 +567,208 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     red_dev = torch.device("cpu") if share else dev
+    ep = ws > 1 and args.parallel in ("auto", "ep")
     if ws > 1:
         if share:
             dist.init_process_group("gloo")
         else:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
-    cfg = MoEConfig(**dict(BASE8, num_experts=args.experts))
+    cfg = MoEConfig(**dict(SWITCH, num_experts=args.experts))
     model = MoEModel.synthetic(cfg, seed=0, device=dev)
     pred = PredictorNet(PredictorConfig(), cfg.d_model, cfg.num_layers, cfg.num_experts, Rng(1))
     eb = model.expert_bytes_each()
-    ep_mode = args.parallel == "ep" and ws > 1
-    n_all = cfg.num_layers * cfg.num_experts // (ws if ep_mode else 1)
-    slots = max(1, int(round(args.budget_frac * n_all)))
-    budget = MemoryBudget(slots * eb)
-    if ep_mode:
-        from paper_2310_18859_b200.expert_parallel import ExpertParallelEngine
-
-        from paper_2310_18859_b200.expert_parallel import PeerTransport
-
-        if share:  # gloo plumbing (collectives staged through host memory)
-            from paper_2310_18859_b200.expert_parallel import GlooTransport
-
-            transport = (PeerTransport(control=GlooTransport()) if args.ep_transport == "peer"
-                         else GlooTransport())
-        else:
-            transport = PeerTransport() if args.ep_transport == "peer" else None
-        engine = ExpertParallelEngine(model, pred, budget, transport=transport)
-        engine.compute_stream = engine.base.compute_stream
-        engine.ffn_events, engine.mix_events = None, []
-    else:
-        engine = SidaEngine(model, pred, budget, eval_top_k=1,
-                            victim_policy=args.victim_policy)
+    engine, budget, slots = build_engine(args, model, pred, ws, ep)
     B, T = args.batch, args.seq
     n_tok = B * T
     lengths = [T] * B
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
     n_steps = args.warmup + args.steps
-    toks = [torch.randint(0, cfg.vocab_size, (n_tok,), generator=g, device=dev,
-                          dtype=torch.int32) for _ in range(n_steps + 1)]
+    toks = [synth_tokens(n_tok, cfg.vocab_size, g) for _ in range(n_steps + 1)]
     torch.cuda.synchronize()
+    h = _lib.lib()
 
     def barrier():
         if ws > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(v):
+        if ws > 1:
+            t = torch.tensor([v], device=red_dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return v
+
     cs = engine.compute_stream
     # ---- device-resident pipeline: hash(j+1) on the hash stream overlaps forward(j)
     tables = {0: engine.hash_tokens(0, toks[0], lengths)}
-    outs = []
     ev_start = torch.cuda.Event(enable_timing=True)
     ev_end = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
+    seen = []
     for j in range(n_steps):
         if j == args.warmup:
-            if not ep_mode:
-                engine.ffn_events = []
-            sampler.__enter__()
+            engine.ffn_events = []
+            engine.mix_events = []
             barrier()
+            loads0 = engine.store.n_loads
+            launches0 = h.sida_launch_count()
+            sampler.__enter__()
             ev_start.record(cs)
             t_wall0 = time.perf_counter()
         tables[j + 1] = engine.hash_tokens(j + 1, toks[j + 1], lengths)
-        out = (engine.forward(tables.pop(j), lengths, tokens_dev=toks[j]) if ep_mode else
-               engine.forward(tables.pop(j), lengths, tokens_dev=toks[j],
-                              next_table=tables[j + 1]))
-        outs.append(out if ep_mode else out[0])
+        engine.forward(tables.pop(j), lengths, tokens_dev=toks[j], next_table=tables[j + 1])
     ev_end.record(cs)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_wall0
     sampler.__exit__()
-    ms = ev_start.elapsed_time(ev_end)
+    launches = h.sida_launch_count() - launches0
+    loads_timed = engine.store.n_loads - loads0
+    ms = max_over_ranks(ev_start.elapsed_time(ev_end))
     ffn_ms = [a.elapsed_time(b) for a, b, _, _ in (engine.ffn_events or [])]
     ffn_active = [n for _, _, _, n in (engine.ffn_events or [])]
-    mix_ms = [a.elapsed_time(b) for a, b in engine.mix_events]
+    mix_ms = [a.elapsed_time(b) for a, b in (engine.mix_events or [])]
     engine.ffn_events = None
     engine.mix_events = []
-    if ws > 1:
-        t = torch.tensor([ms], device=red_dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    engine.check_errors(list(tables.values()))
     value = ws * args.steps * n_tok / (ms / 1e3)
-
-    # ---- e2e through the public API: host SequenceBatches in, host logits out
-    e2e, rep = None, None
-    if not ep_mode:
-        rng = np.random.default_rng(99 + rank)
-        host_batches = [SequenceBatch(i, [rng.integers(0, cfg.vocab_size, size=T)
-                                          for _ in range(B)]) for i in range(n_steps)]
-        serve_sida(model, pred, host_batches[: args.warmup], budget, engine=engine,
-                   compute_hit_rate=False)
-        barrier()
-        t0 = time.perf_counter()
-        rep = serve_sida(model, pred, [SequenceBatch(i, b.sequences) for i, b in
-                                       enumerate(host_batches[args.warmup:])], budget,
-                         engine=engine, compute_hit_rate=False)
-        barrier()
-        e2e_s = time.perf_counter() - t0
-        if ws > 1:
-            t = torch.tensor([e2e_s], device=red_dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = ws * args.steps * n_tok / e2e_s
-
-    # ---- expert streaming: pinned H2D link bandwidth, then a budget-limited
-    # run (half of the experts fit) to expose how much copy time is hidden
-    streaming = None
-    if not ep_mode and not args.no_streaming:
-        streaming = measure_streaming(model, pred, cfg, toks, lengths, n_tok, step_ms=ms / args.steps)
-
-    # ---- roofline of the dominant kernel: grouped FFN (GEMM1 + GEMM2; the row
-    # gather is folded into the attention output projection's epilogue)
-    # roofline time = max(FLOPs / tensor peak, min bytes / HBM peak)
-    # with FLOPs = 4 d h N k and min bytes = active experts x (2dh+h+d) x 2 (the
-    # weights, once) + 3 N k d x 2 (x_perm read, residual read, output write)
-    peaks = measured_peaks()
-    d_, h_ = cfg.d_model, cfg.expert_hidden
-    flops = 4.0 * n_tok * d_ * h_   # per layer launch set
-    n_active = float(np.mean(ffn_active)) if ffn_active else float(cfg.num_experts)
-    min_bytes = n_active * (2 * d_ * h_ + h_ + d_) * 2 + 3.0 * n_tok * d_ * 2
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "r1", "ffn_traffic.json")
-    if os.path.exists(tpath) and n_tok == 32768 and cfg.num_experts == 8:
-        traffic = json.load(open(tpath))["traffic_bytes_per_launch_set"]
-    ffn_avg_ms = float(np.mean(ffn_ms)) if ffn_ms else None
-    peak_t = peaks.get("bf16_tflops_sustained", 1373.4)
-    peak_b = peaks.get("hbm_gbs", 6549.4)
-    t_tensor = flops / (peak_t * 1e12) * 1e3    # ms
-    t_hbm = min_bytes / (peak_b * 1e9) * 1e3    # ms
-    if t_tensor >= t_hbm:
-        bound, unit, peak = "tensor", "TFLOP/s", peak_t
-        achieved = flops / (ffn_avg_ms / 1e3) / 1e12 if ffn_avg_ms else None
-    else:
-        bound, unit, peak = "hbm", "GB/s", peak_b
-        achieved = min_bytes / (ffn_avg_ms / 1e3) / 1e9 if ffn_avg_ms else None
     step_ms = ms / args.steps
     clocks = sampler.summary()
-    # hash: lstm x2, rows_gemm x2, block offsets, attention; permute: 3; per layer:
-    # attention core + out-projection (+ scatter) + GEMM1 + GEMM2 (EP: + gather,
-    # regroup, combine; the QKV projection is cuBLAS and not counted)
-    launches_per_step = 6 + 3 + cfg.num_layers * (7 if ep_mode else 4)
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rate, work, detail = cpu_sample(dict(BASE8, num_experts=args.experts), T, args.cpu_steps)
-        cpu = {"value": rate, "unit": "tokens/s", "cores": os.cpu_count(),
-               "blas_threads": blas_threads(), "kind": "port",
-               "sample": detail + f" ({work:.1f} s of CPU work)"}
-    # ---- north-star target (BASELINE.json: Switch-base-128 grouped FFN at
-    # >= 70 % of its roofline on one B200): one base-128 layer at the bench
-    # batch (32K tokens, ~256 rows per expert: at the HBM/tensor ridge) and at
-    # 1024 x 128 tokens per batch
-    north = None
-    if rank == 0 and ws == 1 and not args.no_north_star:
-        north = {"target_frac": 0.70,
-                 "shapes": [measure_ffn_shape(128, n, peaks) for n in (32768, 131072)],
-                 "balanced_base8": measure_ffn_shape(8, n_tok, peaks)}
-    # routing the timed FFNs saw (random-init predictor: report the
-    # per-layer histogram; the balanced case is north_star_ffn.balanced_base8)
-    routing = None
-    if not ep_mode and (n_steps in tables):
-        hist = tables[n_steps].on_device(model).hist.cpu().numpy()
-        torch.cuda.synchronize()
-        routing = {"source": "random-init predictor (Rng(1)), last hashed batch",
-                   "hist_per_layer": hist.tolist(),
-                   "max_over_mean_per_layer": [round(float(h.max() / max(h.mean(), 1e-9)), 3)
-                                               for h in hist]}
-    footprint = engine.store.peak_slots * eb
+
+    # ---- e2e through the public API: host SequenceBatches in, host logits out
+    rng = np.random.default_rng(99 + rank)
+    host_batches = [SequenceBatch(i, [rng.integers(0, cfg.vocab_size, size=T) for _ in range(B)])
+                    for i in range(n_steps)]
+    serve_sida(model, pred, host_batches[: args.warmup], budget, engine=engine,
+               compute_hit_rate=False)
+    barrier()
+    t0 = time.perf_counter()
+    rep = serve_sida(model, pred, [SequenceBatch(i, b.sequences) for i, b in
+                                   enumerate(host_batches[args.warmup:])], budget,
+                     engine=engine, compute_hit_rate=False)
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e = ws * args.steps * n_tok / e2e_s
+
+    # ---- roofline of the dominant kernel: the grouped FFN (GEMM1 + GEMM2 of
+    # a layer) timed with CUDA events on the compute stream inside the timed
+    # region. SURVEY §8(d): roofline time = max(FLOPs / tensor peak, min bytes
+    # / HBM) with FLOPs = 4 d h N k and min bytes = active experts x (2dh+h+d)
+    # x 2 (the weights, once) + 3 N k d x 2 (x_perm, residual, output)
+    peaks = measured_peaks()
+    peak_t, peak_src = tensor_peak(peaks, clocks)
+    peak_b = peaks.get("hbm_gbs", 6547.2)
+    d_, h_ = cfg.d_model, cfg.expert_hidden
+    rows_ffn = n_tok if not ep else None
+    flops = 4.0 * n_tok * d_ * h_ if not ep else None
+    ffn_avg_ms = float(np.mean(ffn_ms)) if ffn_ms else None
+    roofline = None
+    if ffn_avg_ms and not ep:
+        n_active = float(np.mean(ffn_active))
+        min_bytes = n_active * (2 * d_ * h_ + h_ + d_) * 2 + 3.0 * rows_ffn * d_ * 2
+        t_tensor = flops / (peak_t * 1e12) * 1e3
+        t_hbm = min_bytes / (peak_b * 1e9) * 1e3
+        t_sus = flops / (peaks.get("bf16_tflops_sustained", 1380.0) * 1e12) * 1e3
+        tpath = os.path.join(REPO, "profiles", "r2", "ffn_traffic.json")
+        traffic, tsrc = None, None
+        if os.path.exists(tpath):
+            tj = json.load(open(tpath))
+            key = f"base{cfg.num_experts}_{n_tok}"
+            if key in tj:
+                traffic, tsrc = tj[key]["dram_bytes_per_layer"], tj[key]["source"]
+        if t_tensor >= t_hbm:
+            bound, unit, peak = "tensor", "TFLOP/s", peak_t
+            achieved = flops / (ffn_avg_ms / 1e3) / 1e12
+        else:
+            bound, unit, peak = "hbm", "GB/s", peak_b
+            achieved = min_bytes / (ffn_avg_ms / 1e3) / 1e9
+        roofline = {"kernel": "grouped_ffn (tcgen05 GEMM1 + GEMM2, per layer)", "bound": bound,
+                    "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+                    "traffic": traffic, "traffic_source": tsrc, "peak_source": peak_src,
+                    "frac_vs_sustained_peak": max(t_sus, t_hbm) / ffn_avg_ms,
+                    "flops_per_launch": flops, "min_bytes_per_launch": min_bytes,
+                    "active_experts_per_layer": n_active, "roofline_ms": max(t_tensor, t_hbm),
+                    "tensor_ms": t_tensor, "hbm_ms": t_hbm, "avg_ms": ffn_avg_ms,
+                    "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms,
+                    "attention_mix_avg_ms": float(np.mean(mix_ms)) if mix_ms else None}
+
     line = {
-        "metric": "MoE inference tokens/sec (SiDA serving, base-8)",
+        "metric": "MoE inference tokens/sec (SiDA serving)",
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic uniform tokens, random-init Switch-base-8-shaped weights (GPU RNG)",
-        "config": {"workload": "Switch-base-8 SiDA serving with expert offload, 12 layers, "
-                               f"bf16, {ws} B200 (BASELINE configs[1])", "global_batch": B * ws,
-                   "seq_len": T,
-                   "tokens_per_step_per_gpu": n_tok, "layers": cfg.num_layers,
+        "data": "synthetic uniform tokens, random-init Switch-shaped weights (GPU RNG)",
+        "config": {"workload": workload_name(args, ws, ep), "global_batch": B * ws,
+                   "seq_len": T, "tokens_per_step_per_gpu": n_tok, "layers": cfg.num_layers,
                    "experts": cfg.num_experts, "d_model": cfg.d_model,
                    "expert_hidden": cfg.expert_hidden, "top_k": 1,
                    "hbm_budget_slots": slots, "budget_frac": args.budget_frac,
                    "victim_policy": args.victim_policy,
-                   "parallelism": (f"ep{ws}-{args.ep_transport}" if ep_mode
-                                   else f"replicas{ws}"),
-                   "l2_note": "per-step working set (activations 32768x768 fp32 + bf16 hidden "
-                              "32768x3072 = 300 MB) exceeds the 126 MB L2"},
-        "expert_memory": {"footprint_bytes": footprint, "slots": engine.store.peak_slots,
-                          "slot_bytes": eb, "all_expert_bytes": model.total_expert_bytes(),
-                          "loads_timed": rep.expert_loads if rep else None},
-        "expert_streaming": streaming,
-        "roofline": {"kernel": "grouped_ffn (tcgen05 GEMM1 + GEMM2, per layer)",
-                     "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                     "frac": achieved / peak if achieved else None, "traffic": traffic,
-                     "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained / hbm_gbs",
-                     "flops_per_launch": flops, "min_bytes_per_launch": min_bytes,
-                     "active_experts_per_layer": n_active,
-                     "roofline_ms": max(t_tensor, t_hbm), "tensor_ms": t_tensor,
-                     "hbm_ms": t_hbm,
-                     "tflops_achieved": flops / (ffn_avg_ms / 1e3) / 1e12 if ffn_avg_ms else None,
-                     "avg_ms": ffn_avg_ms,
-                     "share_of_step": ffn_avg_ms * cfg.num_layers / step_ms if ffn_avg_ms else None,
-                     "attention_mix_avg_ms": float(np.mean(mix_ms)) if mix_ms else None},
-        "north_star_ffn": north,
-        "routing": routing,
-        "cpu_baseline": cpu,
+                   "parallelism": (f"ep{ws}-{args.ep_transport}" if ep else f"replicas{ws}"),
+                   "l2_note": "inputs larger than L2: per-step working set (12 x 32768x768 fp32 "
+                              "activations + bf16 hidden 32768x3072 + the layer's experts) "
+                              "exceeds the 126 MB L2"},
+        "expert_memory": {"footprint_bytes": engine.store.peak_slots * eb,
+                          "slots": engine.store.peak_slots, "slot_bytes": eb,
+                          "all_expert_bytes": model.total_expert_bytes() // (ws if ep else 1),
+                          "footprint_frac": engine.store.peak_slots * eb /
+                          (model.total_expert_bytes() / (ws if ep else 1)),
+                          "expert_loads_timed_region": loads_timed,
+                          "expert_loads_e2e": rep.expert_loads},
+        "roofline": roofline,
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": n_tok * 4 + (B + 1) * 4,
                 "d2h_bytes_per_step": B * cfg.num_classes * 4 + cfg.num_layers * cfg.num_experts * 4,
                 "api": "paper_2310_18859_b200.serve_sida"},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches,
+        "gpu_launches_source": "sida_launch_count() delta over the timed region (every kernel "
+                               "this library launched; no library or torch kernels run in the "
+                               "step)",
         "clocks": clocks,
         "wall_s_timed": wall,
     }
+
+    if rank == 0 and ws == 1 and not args.no_extras:
+        line["north_star_ffn"] = {
+            "target_frac": 0.70, "peak_tflops": peak_t, "peak_source": peak_src,
+            "shapes": [measure_ffn_shape(128, n, peak_t, peak_b) for n in (32768, 131072)],
+            "balanced_base8": measure_ffn_shape(8, 32768, peak_t, peak_b)}
+        line["rooflines"] = {
+            "permute_bench_scale": measure_permute(cfg.num_layers, n_tok, cfg.num_experts, peak_b),
+            "permute_c4_scale": measure_permute(12, 262144, 256, peak_b),
+            "hash": measure_hash(model, pred, B, T),
+            "ncu": "profiles/r2/ (per-kernel dram__bytes and launch lists)"}
+        link = h2d_link_gbs(model)
+        line["expert_streaming"] = {
+            "h2d_link_gbs": link, "h2d_source": "pinned host -> HBM, 8 expert images x 4 via "
+                                                "sida_expert_copy on one stream",
+            "budgets": budget_runs(model, pred, cfg, lengths,
+                                   [(1.0, "fifo"), (0.97, "spread"), (0.97, "fifo"),
+                                    (0.9, "spread"), (0.75, "spread")])}
+        for r in line["expert_streaming"]["budgets"]:
+            r["copy_ms_per_step_at_link"] = r["expert_loads_per_step"] * eb / (link * 1e9) * 1e3
+        line["memory_regime_zipf"] = {
+            "tokens": f"Zipf(a={ZIPF_A}) over the vocabulary (ref corpus.py generate_corpus "
+                      "marginal): a batch activates a subset of the experts, the regime SiDA "
+                      "saves memory in",
+            "budgets": budget_runs(model, pred, cfg, lengths,
+                                   [(1.0, "fifo"), (0.8, "spread"), (0.7, "spread"),
+                                    (0.6, "spread"), (0.8, "fifo")], zipf=True, seed=1)}
+        for r in line["memory_regime_zipf"]["budgets"]:
+            r["copy_ms_per_step_at_link"] = r["expert_loads_per_step"] * eb / (link * 1e9) * 1e3
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        times = cpu_reference_steps(dict(SWITCH, num_experts=args.experts), T,
+                                    args.cpu_seqs + 1, os.cpu_count() or 1)
+        rate = args.cpu_seqs * T / float(np.sum(times[1:]))
+        line["cpu_baseline"] = {"value": rate, "unit": "tokens/s", "cores": os.cpu_count(),
+                                "blas_threads": blas_threads(), "kind": "port",
+                                "sample": f"{args.cpu_seqs} sequence(s) of {T} tokens, each "
+                                          "through the reference algorithm's hash + 12-layer "
+                                          "forward end to end (same routine as --impl "
+                                          f"reference), {float(np.sum(times[1:])):.1f} s of "
+                                          "CPU work"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -97,9 +97,9 @@ int sida_debug_hash_prof(unsigned long long* out);
  * ids: int32 (L, n_rows) with n_rows = n_tokens*k, row = token*k + rank.
  * Outputs per layer: hist (L,K), off (L,K+1), perm (L,n_rows) stable by
  * row within expert, inv (L,n_rows) with inv[perm[p]] = p; alpha_perm
- * (optional, L x n_rows float32) = alpha_rows[perm[p]]. err_flag (int32, set to 1
- * when an id lies outside [0, K); never cleared here: the caller zeroes it
- * and reads it at its next synchronisation point -> ContractError).
+ * (optional, L x n_rows float32) = alpha_rows[perm[p]]. err_flag (int32,
+ * zeroed by the call, set to 1 when an id lies outside [0, K): the caller
+ * reads it at its next synchronisation point -> ContractError).
  * Replaces the implicit grouping of ref moe.py:253-256 (w1[ids] gather).
  * ------------------------------------------------------------------- */
 size_t sida_permute_workspace_bytes(int n_layers, int n_rows, int num_experts);
@@ -179,9 +179,24 @@ int sida_get_ffn_tiles(void);
  * ctx = softmax(q k^T / sqrt(d)) v per sequence, single head, non-causal, on
  * tcgen05 (scores and P.V in TMEM, softmax in registers). qkv bf16
  * (n_tokens, 3d) = [q | k | v]; seq_off int32 (n_seq + 1) device offsets;
- * every sequence <= 256 tokens (max_len), d % 128 == 0; ctx bf16 (n_tokens, d). */
+ * every sequence <= 512 tokens (max_len), d % 64 == 0; ctx bf16 (n_tokens, d).
+ * Up to 256 tokens P = exp(S - max) goes through shared memory; up to 512 it
+ * stays in TMEM over the consumed scores and C = P V reads A from TMEM. */
 int sida_attention_core(const uint16_t* qkv, const int32_t* seq_off, int n_seq, int n_tokens,
                         int max_len, int d, uint16_t* ctx, void* stream);
+
+/* Embedding and classifier head (the ends of the forward, so a serving step
+ * launches only this library's kernels):
+ *  - sida_embed: x[t] = tok_emb[tokens[t]] + pos_emb[t - seq_off[s]] for token t
+ *    of sequence s (ref moe.py:206-218); tables bf16 (vocab, d) / (max_len, d);
+ *    x float32 (n_tokens, d) and its bf16 copy xb; d % 8 == 0;
+ *  - sida_pool_classify: logits (n_seq, n_cls) float32 = mean of each
+ *    sequence's rows of x @ wc (float32 (d, n_cls)) (ref moe.py:264-266). */
+int sida_embed(const int32_t* tokens, const int32_t* seq_off, int n_seq, int n_tokens,
+               const uint16_t* tok_emb, const uint16_t* pos_emb, int d, float* x, uint16_t* xb,
+               void* stream);
+int sida_pool_classify(const float* x, const int32_t* seq_off, int n_seq, int d, const float* wc,
+                       int n_cls, float* logits, void* stream);
 
 /* Mixing-attention output projection (ref moe.py:232-233) on the same
  * tcgen05 GEMM, residual fused: out[t] = resid[t] + ctx[t] W_o (fp32), and,
@@ -193,6 +208,14 @@ size_t sida_out_proj_bytes(int d);
 int sida_out_proj_scatter(const uint16_t* ctx, int n_rows, int d, const void* wo_t,
                           const float* resid, float* out, const int32_t* inv, int k,
                           uint16_t* x_perm, int32_t* err_flag, void* stream);
+
+/* Dense bf16 linear layer on the same tcgen05 GEMM (used for the mixing
+ * attention's fused QKV projection, ref moe.py:225-227): out (n_rows, n) bf16
+ * = x (n_rows, k) bf16 @ W + b, with w_t = W^T (n, k) bf16 K-major followed by
+ * b (n) bf16, sida_linear_bytes(k, n) bytes; k, n multiples of 64. */
+size_t sida_linear_bytes(int k, int n);
+int sida_linear_bf16(const uint16_t* x, int n_rows, int k, int n, const void* w_t, uint16_t* out,
+                     int32_t* err_flag, void* stream);
 
 /* fp32 FMA check path: same contraction with float32 weights in the
  * reference layout w1 (K,d,h), b1 (K,h), w2 (K,h,d), b2 (K,d); x_perm
@@ -211,6 +234,12 @@ int sida_gather_bf16_rows(const uint16_t* src, const int32_t* idx, int n_rows, i
 int sida_unpermute_combine(const uint16_t* y_perm, const int32_t* inv, const float* alpha_perm,
                            const float* resid, int n_tokens, int k, int d, float* out,
                            uint16_t* out_bf16, void* stream);
+/* The same combine for any row placement: out[t] = resid[t] + sum_r
+ * alpha_rows[t*k + r] y[map[t*k + r]] (alpha in row order), e.g. the
+ * expert-parallel NCCL path's chunk-major dispatch order. */
+int sida_map_combine(const uint16_t* y, const int32_t* map, const float* alpha_rows,
+                     const float* resid, int n_tokens, int k, int d, float* out,
+                     uint16_t* out_bf16, void* stream);
 
 /* Expert parallelism over peer memory: the dispatch and
  * return all-to-alls folded into the epilogues that produce the rows.

@@ -137,12 +137,15 @@ def pool_classify(params, x: np.ndarray) -> np.ndarray:
 
 
 def forward_external(params, shape: MoEShape, sequences, ids: np.ndarray,
-                     alphas: np.ndarray, return_layers: bool = False):
+                     alphas: np.ndarray, return_layers: bool = False, grouped: bool = False):
     """Batch forward with router bypass (ref `moe.py:408-442` external mode).
 
     ``ids``/``alphas`` are (L, N, k) over the concatenated token axis.
+    ``grouped`` evaluates the experts with :func:`moe_apply_grouped` (same
+    contraction, one BLAS GEMM per expert) for Switch-sized checks.
     Returns (logits (B, C), and optionally the per-layer (attn_out, moe_out)
     lists per sequence)."""
+    moe_fn = moe_apply_grouped if grouped else moe_apply
     logits, trace = [], []
     off = 0
     for tokens in sequences:
@@ -153,8 +156,8 @@ def forward_external(params, shape: MoEShape, sequences, ids: np.ndarray,
             if ids.shape[0] <= layer or off + t > ids.shape[1]:
                 raise ValueError(f"missing hash entry for layer {layer}")
             xa = attention_mix(params, shape, layer, x)
-            x = moe_apply(params, layer, xa, ids[layer, off : off + t],
-                          alphas[layer, off : off + t])
+            x = moe_fn(params, layer, xa, ids[layer, off : off + t],
+                       alphas[layer, off : off + t])
             per_layer.append((xa, x))
         logits.append(pool_classify(params, x))
         trace.append(per_layer)

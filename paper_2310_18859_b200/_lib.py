@@ -51,8 +51,13 @@ SIGNATURES = {
     "sida_combine_ranks": (_i, [_vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "sida_gather_bf16_rows": (_i, [_vp, _vp, _i, _i, _vp, _vp]),
     "sida_unpermute_combine": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
+    "sida_map_combine": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp]),
     "sida_attention_core": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "sida_out_proj_bytes": (_sz, [_i]),
+    "sida_linear_bytes": (_sz, [_i, _i]),
+    "sida_embed": (_i, [_vp, _vp, _i, _i, _vp, _vp, _i, _vp, _vp, _vp]),
+    "sida_pool_classify": (_i, [_vp, _vp, _i, _i, _vp, _i, _vp, _vp]),
+    "sida_linear_bf16": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp]),
     "sida_out_proj_scatter": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp]),
     "sida_router_topk": (_i, [_vp, _i, _i, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp]),
     "sida_out_proj_scatter_peer": (_i, [_vp, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _i, _vp,

@@ -1,6 +1,6 @@
 // Fused mixing-attention core on the 5th-gen tensor cores (sm_100a):
 //   ctx = softmax(q k^T / sqrt(d)) v        per sequence, single head, non-causal
-// for sequences of at most 256 tokens (ref moe.py:220-233; the projections
+// for sequences of at most 512 tokens (ref moe.py:220-233; the projections
 // q,k,v = x W and the output projection run as GEMMs around this kernel).
 //
 // Up to 128 tokens: one CTA per sequence, two CTAs per SM (~105 KB smem, 256
@@ -41,7 +41,7 @@ using namespace sm100;
 
 constexpr int BM = 128;        // queries per CTA (one TMEM lane each)
 constexpr int BK = 64;         // d per phase-1 k-block (one SW128 row)
-constexpr int NC = 128;        // d columns per phase-3 chunk
+constexpr int NC = 128;        // d columns per phase-3 chunk (64 when d % 128 != 0)
 constexpr int kSlots = 2;
 constexpr int kStageTile = 32 * 32 * 2; // per-warp bf16 epilogue staging tile
 constexpr int kEpiWarps = 4;
@@ -52,12 +52,23 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 //        TMEM 256 columns (S [0,128), C chunks {[128,256), [0,128)}), 2 CTAs/SM
 //   256: ring slot 64 KB (Q 16 + K 32 KB, or a V chunk 2 x 32 KB), P 64 KB,
 //        TMEM 512 columns (S [0,256), C chunks {[256,384), [384,512)}), 1 CTA/SM
-template <int NKEY>
+//   512: ring slot 80 KB (Q 16 + K 64 KB, or half a V chunk: 256 keys x 2 x 64
+//        columns), S fills all 512 TMEM columns (two N=256 MMAs per k-step) and
+//        P stays in TMEM: the softmax warps write bf16 P pairs over S's first
+//        256 columns (tcgen05.st, each lane only overwriting scores it has
+//        already read) and C = P V reads A from TMEM (the tcgen05 "TS" form),
+//        so the 128 KB P tile never touches shared memory; C chunks use the
+//        consumed S columns {[256,384), [384,512)}. 1 CTA/SM.
+template <int NKEY, int NCT = NC>
 struct Cfg {
-  static constexpr int kSlot = NKEY * 256;              // = max(QK, V) stage bytes
+  static constexpr bool kPT = NKEY == 512;                // P in TMEM
+  static constexpr int kVKeys = kPT ? 256 : NKEY;         // keys per V stage
+  static constexpr int kVPerChunk = NKEY / kVKeys;        // V stages per d chunk
   static constexpr int kQKBytes = BM * 128 + NKEY * 128;
-  static constexpr int kVBytes = NKEY * 256;
-  static constexpr int kPBytes = BM * NKEY * 2;         // NKEY/64 K-atoms x 128 rows x 128 B
+  static constexpr int kVBytes = kVKeys * NCT * 2;
+  static constexpr int kSlot = kQKBytes > kVBytes ? kQKBytes : kVBytes;
+  static constexpr int kPBytes = kPT ? 0 : BM * NKEY * 2;  // NKEY/64 K-atoms x 128 rows x 128 B
+  static constexpr int kSN = NKEY > 256 ? 256 : NKEY;     // N of one phase-1 MMA
   static constexpr uint32_t kTmemCols = NKEY == 128 ? 256 : 512;
   static constexpr uint32_t kC0 = NKEY == 128 ? 128 : 256;  // C chunk buffers (TMEM columns)
   static constexpr uint32_t kC1 = NKEY == 128 ? 0 : 384;
@@ -80,11 +91,11 @@ __device__ __forceinline__ void mbar_arrive_local(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int NKEY>
-__global__ void __launch_bounds__(kThreads, Cfg<NKEY>::kMinBlocks)
+template <int NKEY, int NCT>
+__global__ void __launch_bounds__(kThreads, Cfg<NKEY, NCT>::kMinBlocks)
 attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __restrict__ seq_off,
                  int d, float scale_log2e, uint16_t* __restrict__ ctx) {
-  using C = Cfg<NKEY>;
+  using C = Cfg<NKEY, NCT>;
   constexpr int kSlot = C::kSlot;
   constexpr int kPBytes = C::kPBytes;
   constexpr uint32_t kTmemCols = C::kTmemCols;
@@ -108,7 +119,7 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
   const int T = seq_off[seq + 1] - row0;
   const int q0 = blockIdx.y * BM;             // first query row of this CTA (in the sequence)
   if (q0 >= T) return;                        // (uniform: before any barrier / TMEM use)
-  const int n_kb = d / BK, n_chunks = d / NC;
+  const int n_kb = d / BK, n_chunks = d / NCT;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kSlots; ++i) {
@@ -145,7 +156,7 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
     if (lane == 0) {
       int slot = 0;
       uint32_t phase = 0;
-      const int n_loads = n_kb + n_chunks;
+      const int n_loads = n_kb + n_chunks * C::kVPerChunk;
       for (int i = 0; i < n_loads; ++i) {
         mbar_wait(&empty[slot], phase ^ 1);
         uint8_t* dst = ring + slot * kSlot;
@@ -159,13 +170,15 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
                            row0 + kh * 128, fb);
         } else {
           mbar_expect_tx(&full[slot], C::kVBytes);
-          const int c0 = 2 * d + (i - n_kb) * NC;
+          const int vi = i - n_kb;
+          const int c0 = 2 * d + (vi / C::kVPerChunk) * NCT;
+          const int k0 = row0 + (vi % C::kVPerChunk) * C::kVKeys;
 #pragma unroll
-          for (int gcol = 0; gcol < 2; ++gcol)                              // V[:, c0 + 64 g ..]
+          for (int gcol = 0; gcol < NCT / 64; ++gcol)                       // V[:, c0 + 64 g ..]
 #pragma unroll
-            for (int kh = 0; kh < NKEY / 128; ++kh)
-              tma_load_2d<1>(dst + gcol * (NKEY * 128) + kh * 128 * 128, &tm_qkv,
-                             c0 + gcol * 64, row0 + kh * 128, fb);
+            for (int kh = 0; kh < C::kVKeys / 128; ++kh)
+              tma_load_2d<1>(dst + gcol * (C::kVKeys * 128) + kh * 128 * 128, &tm_qkv,
+                             c0 + gcol * 64, k0 + kh * 128, fb);
         }
         if (++slot == kSlots) { slot = 0; phase ^= 1; }
       }
@@ -173,8 +186,8 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
   } else if (warp == 1) {
     // ===== MMA issuer (one thread)
     if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16<BM, NKEY>();
-      constexpr uint32_t idesc_c = idesc_bf16<BM, NC>() | (1u << 16);  // B (V) MN-major
+      constexpr uint32_t idesc_s = idesc_bf16<BM, C::kSN>();
+      constexpr uint32_t idesc_c = idesc_bf16<BM, NCT>() | (1u << 16);  // B (V) MN-major
       int slot = 0;
       uint32_t phase = 0;
       for (int i = 0; i < n_kb; ++i) {
@@ -184,8 +197,10 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
         const uint32_t b0 = a0 + BM * 128;
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
-          umma_bf16<1>(tmem, sw128_desc(a0 + k * 32), sw128_desc(b0 + k * 32), idesc_s,
-                       (i | k) != 0);
+#pragma unroll
+          for (int nh = 0; nh < NKEY / C::kSN; ++nh)  // 512 keys: two N=256 halves
+            umma_bf16<1>(tmem + nh * C::kSN, sw128_desc(a0 + k * 32),
+                         sw128_desc(b0 + nh * C::kSN * 128 + k * 32), idesc_s, (i | k) != 0);
         tc_commit<1>(&empty[slot]);
         if (++slot == kSlots) { slot = 0; phase ^= 1; }
       }
@@ -196,17 +211,25 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
       for (int j = 0; j < n_chunks; ++j) {
         const int b = j & 1;
         if (j >= 2) mbar_wait(&c_empty[b], ((j >> 1) - 1) & 1);
-        mbar_wait(&full[slot], phase);
-        tc_fence_after();
         const uint32_t d_tmem = tmem + (b == 0 ? C::kC0 : C::kC1);
-        const uint32_t v0 = smem_u32(ring + slot * kSlot);
+        for (int hv = 0; hv < C::kVPerChunk; ++hv) {
+          mbar_wait(&full[slot], phase);
+          tc_fence_after();
+          const uint32_t v0 = smem_u32(ring + slot * kSlot);
 #pragma unroll
-        for (int k = 0; k < NKEY / 16; ++k)  // 16 keys per MMA: P atom k/4, V rows 16k..
-          umma_bf16<1>(d_tmem, sw128_desc(p0 + (k >> 2) * (BM * 128) + (k & 3) * 32),
-                       sw128_mn_desc(v0 + k * 16 * 128, NKEY * 128), idesc_c, k != 0);
-        tc_commit<1>(&empty[slot]);
+          for (int k = 0; k < C::kVKeys / 16; ++k) {  // 16 keys per MMA, V rows 16k..
+            const uint64_t vb = sw128_mn_desc(v0 + k * 16 * 128, C::kVKeys * 128);
+            if constexpr (C::kPT)  // P from TMEM: keys hv*256 + 16k.. = columns /2
+              umma_bf16_ts(d_tmem, tmem + hv * (C::kVKeys / 2) + k * 8, vb, idesc_c,
+                           (hv | k) != 0);
+            else                   // P from smem: atom k/4, 16-key step k%4
+              umma_bf16<1>(d_tmem, sw128_desc(p0 + (k >> 2) * (BM * 128) + (k & 3) * 32), vb,
+                           idesc_c, k != 0);
+          }
+          tc_commit<1>(&empty[slot]);
+          if (++slot == kSlots) { slot = 0; phase ^= 1; }
+        }
         tc_commit<1>(&c_full[b]);
-        if (++slot == kSlots) { slot = 0; phase ^= 1; }
       }
     }
   } else {
@@ -239,20 +262,31 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
         e[j] = c * 32 + j < T ? exp2f(fmaf(__uint_as_float(v[j]), scale_log2e, -mb)) : 0.f;
         sum += e[j];
       }
-      // keys c*32 .. +31 = atom c/2, 16-B chunks 4*(c%2) .. +3 of row r
+      if constexpr (C::kPT) {
+        // keys c*32 .. +31 -> bf16 pairs in columns c*16 .. +15 of this lane
+        // (scores of keys < c*32 + 32 are already read: no lane overwrites an
+        // unread score)
+        uint32_t pk[16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 o;
-        o.x = bf16x2_rn(e[q * 8 + 0], e[q * 8 + 1]);
-        o.y = bf16x2_rn(e[q * 8 + 2], e[q * 8 + 3]);
-        o.z = bf16x2_rn(e[q * 8 + 4], e[q * 8 + 5]);
-        o.w = bf16x2_rn(e[q * 8 + 6], e[q * 8 + 7]);
-        const int chunk = (c & 1) * 4 + q;
-        sts128(prow + (c >> 1) * (BM * 128) + ((chunk ^ (r & 7)) << 4), o);
+        for (int q = 0; q < 16; ++q) pk[q] = bf16x2_rn(e[2 * q], e[2 * q + 1]);
+        tmem_st16(t_lane + c * 16, pk);
+      } else {
+        // keys c*32 .. +31 = atom c/2, 16-B chunks 4*(c%2) .. +3 of row r
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 o;
+          o.x = bf16x2_rn(e[q * 8 + 0], e[q * 8 + 1]);
+          o.y = bf16x2_rn(e[q * 8 + 2], e[q * 8 + 3]);
+          o.z = bf16x2_rn(e[q * 8 + 4], e[q * 8 + 5]);
+          o.w = bf16x2_rn(e[q * 8 + 6], e[q * 8 + 7]);
+          const int chunk = (c & 1) * 4 + q;
+          sts128(prow + (c >> 1) * (BM * 128) + ((chunk ^ (r & 7)) << 4), o);
+        }
       }
     }
     const float inv_sum = 1.f / sum;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P -> tensor core
+    if constexpr (C::kPT) tmem_wait_st();                           // P -> tensor core (TMEM)
+    else asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P -> tensor core (smem)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive_local(p_full);
@@ -266,7 +300,7 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
       tc_fence_after();
       const uint32_t t_c = t_lane + (b == 0 ? C::kC0 : C::kC1);
 #pragma unroll
-      for (int c = 0; c < NC / 32; ++c) {
+      for (int c = 0; c < NCT / 32; ++c) {
         tmem_ld32_nowait(t_c + c * 32, v);
         tmem_wait_ld();
         const uint32_t srow = stile + lane * 64;
@@ -290,7 +324,7 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
           const int rr = i * 8 + (lane >> 2), q = lane & 3;
           const uint4 val = lds128(stile + rr * 64 + ((q ^ ((rr >> 1) & 3)) << 4));
           if (q0 + quarter * 32 + rr < T)
-            *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(q_row0 + rr) * d + j * NC +
+            *reinterpret_cast<uint4*>(ctx + static_cast<size_t>(q_row0 + rr) * d + j * NCT +
                                       c * 32 + q * 8) = val;
         }
         __syncwarp();
@@ -323,6 +357,22 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+template <int NKEY, int NCT>
+static int launch_core(const CUtensorMap& tm, const int32_t* seq_off, int n_seq, int nq, int d,
+                       float scale_log2e, uint16_t* ctx, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    SIDA_CUDA(cudaFuncSetAttribute(attn_core_kernel<NKEY, NCT>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Cfg<NKEY, NCT>::kSmem));
+    configured = true;
+  }
+  attn_core_kernel<NKEY, NCT><<<dim3(n_seq, nq), kThreads, Cfg<NKEY, NCT>::kSmem, s>>>(
+      tm, seq_off, d, scale_log2e, ctx);
+  SIDA_LAUNCH_CHECK();
+  return SIDA_OK;
+}
+
 }  // namespace attn
 }  // namespace sida
 
@@ -330,14 +380,14 @@ using namespace sida;
 
 // qkv: bf16 (n_tokens, 3d) = [q | k | v] per token (x @ [Wq|Wk|Wv]);
 // seq_off: int32 (n_seq + 1) exclusive offsets on the concatenated token axis;
-// every sequence at most 256 tokens; ctx: bf16 (n_tokens, d).
+// every sequence at most 512 tokens; ctx: bf16 (n_tokens, d).
 extern "C" int sida_attention_core(const uint16_t* qkv, const int32_t* seq_off, int n_seq,
                                    int n_tokens, int max_len, int d, uint16_t* ctx,
                                    void* stream) {
-  SIDA_REQUIRE(d % attn::NC == 0 && d >= attn::NC, SIDA_ERR_UNSUPPORTED,
-               "fused attention needs d multiple of %d (d=%d)", attn::NC, d);
-  SIDA_REQUIRE(max_len >= 1 && max_len <= 256, SIDA_ERR_UNSUPPORTED,
-               "fused attention handles sequences of at most 256 tokens (got %d)", max_len);
+  SIDA_REQUIRE(d % 64 == 0 && d >= 64, SIDA_ERR_UNSUPPORTED,
+               "fused attention needs d multiple of 64 (d=%d)", d);
+  SIDA_REQUIRE(max_len >= 1 && max_len <= 512, SIDA_ERR_UNSUPPORTED,
+               "fused attention handles sequences of at most 512 tokens (got %d)", max_len);
   SIDA_REQUIRE(n_seq >= 0 && n_tokens >= 0, SIDA_ERR_CONTRACT, "bad attention dims");
   SIDA_REQUIRE(qkv && seq_off && ctx, SIDA_ERR_CONTRACT,
                "null pointer passed to sida_attention_core");
@@ -355,27 +405,16 @@ extern "C" int sida_attention_core(const uint16_t* qkv, const int32_t* seq_off, 
   SIDA_REQUIRE(r == CUDA_SUCCESS, SIDA_ERR_CUDA, "tensor map encode failed: %d", (int)r);
   const float scale_log2e = 1.4426950408889634f / sqrtf(static_cast<float>(d));
   cudaStream_t s = as_stream(stream);
-  if (max_len <= 128) {
-    static bool cfg128 = false;
-    if (!cfg128) {
-      SIDA_CUDA(cudaFuncSetAttribute(attn::attn_core_kernel<128>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)attn::Cfg<128>::kSmem));
-      cfg128 = true;
-    }
-    attn::attn_core_kernel<128><<<dim3(n_seq, 1), attn::kThreads, attn::Cfg<128>::kSmem, s>>>(
-        tm, seq_off, d, scale_log2e, ctx);
+  const int nq = ceil_div(max_len, attn::BM);
+  int st;
+  if (d % 128 == 0) {
+    st = max_len <= 128 ? attn::launch_core<128, 128>(tm, seq_off, n_seq, 1, d, scale_log2e, ctx, s)
+       : max_len <= 256 ? attn::launch_core<256, 128>(tm, seq_off, n_seq, nq, d, scale_log2e, ctx, s)
+                        : attn::launch_core<512, 128>(tm, seq_off, n_seq, nq, d, scale_log2e, ctx, s);
   } else {
-    static bool cfg256 = false;
-    if (!cfg256) {
-      SIDA_CUDA(cudaFuncSetAttribute(attn::attn_core_kernel<256>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)attn::Cfg<256>::kSmem));
-      cfg256 = true;
-    }
-    attn::attn_core_kernel<256><<<dim3(n_seq, ceil_div(max_len, attn::BM)), attn::kThreads,
-                                  attn::Cfg<256>::kSmem, s>>>(tm, seq_off, d, scale_log2e, ctx);
+    st = max_len <= 128 ? attn::launch_core<128, 64>(tm, seq_off, n_seq, 1, d, scale_log2e, ctx, s)
+       : max_len <= 256 ? attn::launch_core<256, 64>(tm, seq_off, n_seq, nq, d, scale_log2e, ctx, s)
+                        : attn::launch_core<512, 64>(tm, seq_off, n_seq, nq, d, scale_log2e, ctx, s);
   }
-  SIDA_LAUNCH_CHECK();
-  return SIDA_OK;
+  return st;
 }

@@ -87,6 +87,7 @@ struct GemmParams {
   int peer_stride;             //   v % peer_stride (expert-parallel dispatch / return)
   int32_t* err_flag;
   unsigned long long* prof;    // optional per-CTA cycle counters (sida_debug_gemm_prof)
+  int linear;                  // GEMM1 epilogue without the ReLU (sida_linear_bf16)
 };
 
 // prof slots per CTA: producer wait(empty), MMA wait(tmem_empty), MMA wait(full),
@@ -461,12 +462,14 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           const uint32_t srow = stile + lane * 64;
           const int sw = (lane >> 1) & 3;
 #pragma unroll
+          const float lo = gp.linear ? -INFINITY : 0.f;  // ReLU floor (none: linear)
+#pragma unroll
           for (int q = 0; q < 4; ++q) {
             uint4 o;
-            o.x = bf16x2_rn(fmaxf(f[q * 8 + 0], 0.f), fmaxf(f[q * 8 + 1], 0.f));
-            o.y = bf16x2_rn(fmaxf(f[q * 8 + 2], 0.f), fmaxf(f[q * 8 + 3], 0.f));
-            o.z = bf16x2_rn(fmaxf(f[q * 8 + 4], 0.f), fmaxf(f[q * 8 + 5], 0.f));
-            o.w = bf16x2_rn(fmaxf(f[q * 8 + 6], 0.f), fmaxf(f[q * 8 + 7], 0.f));
+            o.x = bf16x2_rn(fmaxf(f[q * 8 + 0], lo), fmaxf(f[q * 8 + 1], lo));
+            o.y = bf16x2_rn(fmaxf(f[q * 8 + 2], lo), fmaxf(f[q * 8 + 3], lo));
+            o.z = bf16x2_rn(fmaxf(f[q * 8 + 4], lo), fmaxf(f[q * 8 + 5], lo));
+            o.w = bf16x2_rn(fmaxf(f[q * 8 + 6], lo), fmaxf(f[q * 8 + 7], lo));
             sts128(srow + ((q ^ sw) << 4), o);
           }
           __syncwarp();
@@ -1645,6 +1648,33 @@ extern "C" int sida_out_proj_scatter(const uint16_t* ctx, int n_rows, int d, con
     return sm100::launch_gemm<128, 2, 1>(ctx, wo_t, 1, p, 1, as_stream(stream));
   }
   return sm100::dispatch_gemm<2>(ctx, wo_t, 1, p, 1, cg, as_stream(stream));
+}
+
+// Dense bf16 linear layer on the same tcgen05 GEMM (one "expert" over every
+// row, GEMM1 epilogue without the ReLU): out = x W (bf16), W given as
+// w_t = W^T (n x k, bf16, K-major) followed by n bf16 bias values,
+// sida_linear_bytes(k, n) bytes. The mixing attention's fused QKV projection
+// (ref moe.py:225-227: q, k, v = x Wq, x Wk, x Wv as one n = 3d product).
+extern "C" size_t sida_linear_bytes(int k, int n) {
+  return align_up(static_cast<size_t>(n) * k * 2 + static_cast<size_t>(n) * 2, 16);
+}
+
+extern "C" int sida_linear_bf16(const uint16_t* x, int n_rows, int k, int n, const void* w_t,
+                                uint16_t* out, int32_t* err_flag, void* stream) {
+  SIDA_REQUIRE(k % 64 == 0 && n % 64 == 0, SIDA_ERR_UNSUPPORTED,
+               "tcgen05 linear needs k, n multiples of 64 (k=%d n=%d)", k, n);
+  SIDA_REQUIRE(n_rows >= 0, SIDA_ERR_CONTRACT, "bad linear rows=%d", n_rows);
+  SIDA_REQUIRE(x && w_t && out && err_flag, SIDA_ERR_CONTRACT,
+               "null pointer passed to sida_linear_bf16");
+  if (n_rows == 0) return SIDA_OK;
+  sm100::GemmParams p{};
+  p.n_rows = n_rows; p.kdim = k; p.ndim = n;
+  p.off = nullptr; p.num_experts = 1; p.expert_slot = nullptr;
+  p.arena = static_cast<const uint8_t*>(w_t);
+  p.slot_stride = sida_linear_bytes(k, n);
+  p.bias_off = static_cast<size_t>(n) * k * 2;
+  p.hidden = out; p.err_flag = err_flag; p.linear = 1;
+  return sm100::dispatch_gemm<1>(x, w_t, 1, p, 1, n_rows >= 1024 ? 2 : 1, as_stream(stream));
 }
 
 // Both expert GEMMs of one layer in ONE persistent launch (STAGE 3): GEMM1

@@ -311,6 +311,7 @@ extern "C" int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, i
   SIDA_REQUIRE(err_flag && hist && off && (n_rows == 0 || (ids && perm && inv)), SIDA_ERR_CONTRACT,
                "null pointer passed to sida_permute_hist");
   cudaStream_t s = as_stream(stream);
+  SIDA_CUDA(cudaMemsetAsync(err_flag, 0, sizeof(int32_t), s));
   const int tile = perm_tile(n_rows, n_layers);
   const size_t n = (size_t)n_layers * num_experts * perm_tiles(n_rows, tile);
   int32_t* counts = static_cast<int32_t*>(workspace);
@@ -344,11 +345,15 @@ gather_bf16_rows_kernel(const uint4* __restrict__ src, const int32_t* __restrict
 // out[t] = resid[t] + sum_{r<k} alpha_perm[inv[t*k+r]] * y_perm[inv[t*k+r]] (ranks in
 // order, ref moe.py:252-262): the combine of expert-parallel outputs that
 // come back in the source rank's permuted row order. One warp per token.
+// alpha_rows (optional) replaces alpha_perm: the weight of (t, r) read in row
+// order, for maps whose positions are not the table's permuted order (the
+// chunk-major dispatch order of the expert-parallel NCCL path).
 __global__ void __launch_bounds__(256)
 unpermute_combine_kernel(const uint16_t* __restrict__ y_perm, const int32_t* __restrict__ inv,
                          const float* __restrict__ alpha_perm, const float* __restrict__ resid,
                          int n_tokens, int k, int d, float* __restrict__ out,
-                         uint16_t* __restrict__ out_bf16) {
+                         uint16_t* __restrict__ out_bf16,
+                         const float* __restrict__ alpha_rows = nullptr) {
   const int lane = threadIdx.x & 31;
   const int warps = (gridDim.x * blockDim.x) >> 5;
   for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tokens; t += warps) {
@@ -356,7 +361,7 @@ unpermute_combine_kernel(const uint16_t* __restrict__ y_perm, const int32_t* __r
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int r = 0; r < k; ++r) {
         const int p = inv[(size_t)t * k + r];
-        const float a = alpha_perm[p];
+        const float a = alpha_rows ? alpha_rows[(size_t)t * k + r] : alpha_perm[p];
         const uint2 raw = *reinterpret_cast<const uint2*>(y_perm + (size_t)p * d + c);
         acc.x += a * bf16_to_f32(static_cast<uint16_t>(raw.x & 0xFFFF));
         acc.y += a * bf16_to_f32(static_cast<uint16_t>(raw.x >> 16));
@@ -394,6 +399,20 @@ extern "C" int sida_unpermute_combine(const uint16_t* y_perm, const int32_t* inv
   const int blocks = std::min(ceil_div(n_tokens, 8), kNumSMs * 16);
   unpermute_combine_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
       y_perm, inv, alpha_perm, resid, n_tokens, k, d, out, out_bf16);
+  SIDA_LAUNCH_CHECK();
+  return SIDA_OK;
+}
+
+extern "C" int sida_map_combine(const uint16_t* y, const int32_t* map, const float* alpha_rows,
+                                const float* resid, int n_tokens, int k, int d, float* out,
+                                uint16_t* out_bf16, void* stream) {
+  SIDA_REQUIRE(d % 4 == 0 && k >= 1, SIDA_ERR_UNSUPPORTED, "combine needs d %% 4 == 0 (d=%d)", d);
+  SIDA_REQUIRE(y && map && alpha_rows && resid && out, SIDA_ERR_CONTRACT,
+               "null pointer passed to sida_map_combine");
+  if (n_tokens == 0) return SIDA_OK;
+  const int blocks = std::min(ceil_div(n_tokens, 8), kNumSMs * 16);
+  unpermute_combine_kernel<<<blocks, 256, 0, as_stream(stream)>>>(
+      y, map, nullptr, resid, n_tokens, k, d, out, out_bf16, alpha_rows);
   SIDA_LAUNCH_CHECK();
   return SIDA_OK;
 }

@@ -236,8 +236,9 @@ class SidaEngine:
                     issue(idx)
         with torch.cuda.stream(cs):
             lay = BatchLayout(list(lengths), tokens_dev, model.device)
-            x = model.embed_layout(lay)
-            xb = None  # bf16 copy of x for the next attention GEMM (FFN epilogue output)
+            # x fp32 residual stream, xb its bf16 copy for the next QKV GEMM
+            # (written by the embedding kernel, then by each FFN epilogue)
+            x, xb = model.embed_layout(lay, with_bf16=True)
             for layer in range(n_layers):
                 if not issued[layer]:
                     issue(layer)
@@ -334,8 +335,7 @@ class SidaEngine:
 
     def _graph_body(self, lay: BatchLayout, dt, waves, rows):
         model, cs = self.model, self.compute_stream
-        x = model.embed_layout(lay)
-        xb = None
+        x, xb = model.embed_layout(lay, with_bf16=True)
         for layer in range(model.config.num_layers):
             x_perm = torch.empty((lay.n_tokens * dt.k, model.config.d_model),
                                  dtype=torch.bfloat16, device=x.device)

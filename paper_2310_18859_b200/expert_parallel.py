@@ -4,20 +4,27 @@ Rank r owns experts [r*K/G, (r+1)*K/G) of every MoE layer (contiguous blocks),
 holds only those in its HBM slot arena, and serves its own batch stream
 (hash, embed and attention are local). Per batch the ranks exchange their
 (L, K) expert histograms once -- SiDA knows every layer's routing before
-inference starts, so no per-layer size handshake is needed. Per layer:
+inference starts, so there is no per-layer size handshake -- and every map
+of the batch is derived from that count matrix: segment tables on the host
+(O(G K) per layer, vectorised, one pinned upload per batch), row-level maps
+on the device (`sida_segment_map`). Per layer, with the local experts split
+into C chunks:
 
-  x_perm  = gather(x_attn)            rows already grouped by expert, hence by
-                                      destination rank (experts are contiguous)
-  recv    = all_to_all(x_perm)        bf16 rows, splits from the histograms
-  x_local = regroup(recv)             (source, expert) order -> expert-major
-  y_recv  = grouped FFN (local experts); the GEMM2 epilogue writes each row
-            straight back to its receive position (row_map) as bf16
-  y_back  = all_to_all(y_recv)        back to the source rank, x_perm order
-  out     = x_attn + sum_r alpha * y  sida_unpermute_combine (ranks in order)
+  send    = out-proj epilogue scatter   each token's bf16 expert input goes
+            straight to its dispatch position (chunk-major, then destination
+            rank, expert, token): no gather pass
+  recv_c  = all_to_all(send_c)          NCCL, one per chunk, all issued at once
+  x_loc_c = regroup(recv_c)             (source, expert) -> expert-major
+  ret_c   = grouped FFN (chunk c experts); the GEMM2 epilogue writes each row
+            back to its receive position as bf16 (row_map)
+  back_c  = all_to_all(ret_c)           issued right after FFN c
+  out     = x_attn + sum_r alpha * back sida_map_combine (ranks in order)
 
-The transport is NCCL over NVLink (`NcclTransport`, device tensors) in
-production; `GlooTransport` stages through host memory so the same data path
-runs (and is tested) with several ranks on one GPU or on CPU-only hosts.
+The collectives run on NCCL's stream, so dispatch c+1 overlaps FFN c and
+return c overlaps FFN c+1. `GlooTransport` stages the same data path through
+host memory (tests: several ranks on one GPU or CPU-only hosts);
+`PeerTransport` replaces both exchanges with epilogue stores into peer
+memory.
 """
 
 from __future__ import annotations
@@ -29,7 +36,18 @@ import torch.distributed as dist
 from . import _lib
 from .errors import ContractError, UnservableError
 from .moe import BatchLayout, MoEModel
-from .offload import ExpertStore, MemoryBudget, ResidencyState, apply_group_inplace, plan_placement
+from .offload import (
+    FFN_SLOT_MSG,
+    OUTPROJ_MSG,
+    PERMUTE_MSG,
+    ExpertStore,
+    MemoryBudget,
+    ResidencyState,
+    apply_group_inplace,
+    check_device_flags,
+    plan_placement,
+    plan_placement_spread,
+)
 
 
 # ----------------------------------------------------------------------- host math
@@ -51,16 +69,14 @@ def ep_splits(counts: np.ndarray, layer: int, rank: int, world: int):
 
 
 def ep_regroup(counts: np.ndarray, layer: int, rank: int, world: int):
-    """Receive buffer (source-major, then local expert) -> expert-major order.
+    """Receive buffer (source-major, then local expert) -> expert-major order
+    (the host oracle of the device-built regroup map, one chunk).
 
     Returns (src (R,) int32: receive position of each expert-major row,
     off (Kl+1,) int32 expert offsets of the expert-major rows)."""
     kl = owner_block(counts.shape[2], world)
     c = counts[:, layer, rank * kl:(rank + 1) * kl].astype(np.int64)  # (G, Kl)
-    recv_off = np.zeros((world, kl), dtype=np.int64)                  # start of (g, e) in recv
-    flat = c.reshape(-1)
-    starts = np.concatenate([[0], np.cumsum(flat)[:-1]]).reshape(world, kl)
-    recv_off[:] = starts
+    starts = np.concatenate([[0], np.cumsum(c.reshape(-1))[:-1]]).reshape(world, kl)
     per_e = c.sum(axis=0)
     off = np.zeros(kl + 1, dtype=np.int32)
     np.cumsum(per_e, out=off[1:])
@@ -69,9 +85,67 @@ def ep_regroup(counts: np.ndarray, layer: int, rank: int, world: int):
         pos = off[e]
         for g in range(world):
             n = int(c[g, e])
-            src[pos:pos + n] = np.arange(recv_off[g, e], recv_off[g, e] + n, dtype=np.int32)
+            src[pos:pos + n] = np.arange(starts[g, e], starts[g, e] + n, dtype=np.int32)
             pos += n
     return src, off
+
+
+def chunk_bounds(kl: int, chunks: int) -> np.ndarray:
+    """Local-expert boundaries of the C exchange chunks (contiguous blocks)."""
+    c = max(1, min(chunks, kl))
+    return np.array([(i * kl) // c for i in range(c + 1)], dtype=np.int64)
+
+
+def ep_layer_plan(counts: np.ndarray, layer: int, rank: int, world: int, chunks: int) -> dict:
+    """Segment tables and split sizes of one layer of the chunked NCCL path,
+    from the (G, L, K) count matrix (vectorised numpy).
+
+    dispatch: my rows in x_perm (expert-sorted) order are laid out chunk-major
+      (chunk c, then owner q, then expert, then token) in the send buffer;
+      expert e's rows start at d_val[e] (segments d_start = my expert offsets);
+    chunk c: send_rows[q] / recv_rows[g]; the receive buffer is source-major
+      (g, then local expert); regroup segments (x_loc order, expert-major /
+      source-minor) map each x_loc row to its receive position; off_local
+      (kc + 1) delimit the chunk's local experts in x_loc; n_recv rows."""
+    G = world
+    c = counts[:, layer, :].astype(np.int64)                   # (G, K)
+    K = c.shape[1]
+    kl = owner_block(K, G)
+    b = chunk_bounds(kl, chunks)
+    C = len(b) - 1
+    mine = c[rank]
+    off_me = np.zeros(K + 1, dtype=np.int64)
+    np.cumsum(mine, out=off_me[1:])
+    # block (chunk ci, owner q) = experts q*kl + [b[ci], b[ci+1]), contiguous in x_perm
+    first = np.array([[q * kl + b[ci] for q in range(G)] for ci in range(C)])      # (C, G)
+    last = np.array([[q * kl + b[ci + 1] for q in range(G)] for ci in range(C)])
+    sizes = off_me[last] - off_me[first]                                          # (C, G)
+    dstart = np.concatenate([[0], np.cumsum(sizes.reshape(-1))[:-1]]).reshape(C, G)
+    e = np.arange(K)
+    q_of, el_of = e // kl, e % kl
+    ci_of = np.searchsorted(b, el_of, side="right") - 1
+    d_val = dstart[ci_of, q_of] + (off_me[e] - off_me[first[ci_of, q_of]])
+    chunk_rows = sizes.sum(axis=1)
+    out = {"d_start": off_me[:K].astype(np.int32), "d_val": d_val.astype(np.int32),
+           "chunk_start": np.concatenate([[0], np.cumsum(chunk_rows)]).astype(np.int64),
+           "chunks": []}
+    lo = rank * kl
+    for ci in range(C):
+        cc = c[:, lo + b[ci]:lo + b[ci + 1]]                   # (G, kc) rows from each source
+        kc = cc.shape[1]
+        rs = np.concatenate([[0], np.cumsum(cc.reshape(-1))[:-1]]).reshape(G, kc)   # recv (g, el)
+        ccT = cc.T                                                                     # (kc, G)
+        xs = np.concatenate([[0], np.cumsum(ccT.reshape(-1))[:-1]]).reshape(kc, G)  # x_loc (el, g)
+        per_e = cc.sum(axis=0)
+        off_l = np.zeros(kc + 1, dtype=np.int64)
+        np.cumsum(per_e, out=off_l[1:])
+        out["chunks"].append({
+            "experts": (int(b[ci]), int(b[ci + 1])),
+            "send_rows": sizes[ci].tolist(), "recv_rows": cc.sum(axis=1).tolist(),
+            "seg_start": xs.reshape(-1).astype(np.int32),
+            "seg_val": rs.T.reshape(-1).astype(np.int32),
+            "off_local": off_l.astype(np.int32), "n_recv": int(off_l[-1])})
+    return out
 
 
 # ----------------------------------------------------------------------- transports
@@ -87,12 +161,22 @@ class NcclTransport:
         dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
         return out
 
-    def all_to_all(self, send: torch.Tensor, send_rows, recv_rows) -> torch.Tensor:
-        recv = torch.empty((int(sum(recv_rows)),) + tuple(send.shape[1:]), dtype=send.dtype,
-                           device=send.device)
-        dist.all_to_all_single(recv, send, output_split_sizes=[int(v) for v in recv_rows],
-                               input_split_sizes=[int(v) for v in send_rows], group=self.group)
+    def all_to_all(self, send: torch.Tensor, send_rows, recv_rows,
+                   recv: torch.Tensor | None = None) -> torch.Tensor:
+        recv, wait = self.all_to_all_async(send, send_rows, recv_rows, recv)
+        wait()
         return recv
+
+    def all_to_all_async(self, send, send_rows, recv_rows, recv=None):
+        """Enqueue the exchange (it waits for the current stream's work) and
+        return (recv, wait) -- wait() makes the current stream wait for it."""
+        if recv is None:
+            recv = torch.empty((int(sum(recv_rows)),) + tuple(send.shape[1:]), dtype=send.dtype,
+                               device=send.device)
+        work = dist.all_to_all_single(recv, send, output_split_sizes=[int(v) for v in recv_rows],
+                                      input_split_sizes=[int(v) for v in send_rows],
+                                      group=self.group, async_op=True)
+        return recv, work.wait
 
 
 class GlooTransport(NcclTransport):
@@ -105,14 +189,17 @@ class GlooTransport(NcclTransport):
         dist.all_gather(parts, h, group=self.group)
         return torch.stack(parts).to(t.device)
 
-    def all_to_all(self, send: torch.Tensor, send_rows, recv_rows) -> torch.Tensor:
+    def all_to_all_async(self, send, send_rows, recv_rows, recv=None):
         hs = send.detach().cpu().contiguous()
         raw = hs.view(torch.uint8).reshape(hs.shape[0], -1)  # gloo moves raw bytes per row
-        recv = torch.empty((int(sum(recv_rows)), raw.shape[1]), dtype=torch.uint8)
-        dist.all_to_all_single(recv, raw, output_split_sizes=[int(v) for v in recv_rows],
+        got = torch.empty((int(sum(recv_rows)), raw.shape[1]), dtype=torch.uint8)
+        dist.all_to_all_single(got, raw, output_split_sizes=[int(v) for v in recv_rows],
                                input_split_sizes=[int(v) for v in send_rows], group=self.group)
-        out = recv.view(send.dtype).reshape((-1,) + tuple(send.shape[1:]))
-        return out.to(send.device)
+        out = got.view(send.dtype).reshape((-1,) + tuple(send.shape[1:])).to(send.device)
+        if recv is not None:
+            recv.copy_(out)
+            out = recv
+        return out, (lambda: None)
 
 
 class PeerTransport(NcclTransport):
@@ -307,16 +394,21 @@ class _GroupIssuer:
 
 
 class ExpertParallelEngine:
-    """SiDA serving with experts sharded over the ranks of ``group``.
+    """SiDA serving with experts sharded over the ranks of ``group``; the
+    same interface as `engine.SidaEngine` (hash_tokens / forward / check_errors,
+    hash + compute + copy streams), so `serve_sida(..., engine=...)` drives it.
 
     Residency is per rank over its own expert block (the reference planner on
     the union of every rank's needs for those experts). A layer whose local
-    working set exceeds the budget is rejected (waves are single-GPU only)."""
+    working set exceeds the budget is rejected (waves are single-GPU only).
+    ``chunks``: exchange chunks per layer (NCCL path)."""
 
     def __init__(self, model: MoEModel, predictor, budget: MemoryBudget, transport=None,
-                 group=None, eval_top_k: int = 1):
+                 group=None, eval_top_k: int = 1, victim_policy: str = "fifo", chunks: int = 2):
         from .engine import SidaEngine  # streams + hash plumbing
 
+        if victim_policy not in ("fifo", "spread"):
+            raise ContractError(f"unknown victim policy {victim_policy!r}")
         self.model = model
         self.group = group
         self.world = dist.get_world_size(group)
@@ -324,99 +416,208 @@ class ExpertParallelEngine:
         self.kl = owner_block(model.config.num_experts, self.world)
         self.transport = transport or NcclTransport(group)
         self.base = SidaEngine(model, predictor, budget, eval_top_k)
+        self.hash_stream = self.base.hash_stream
+        self.compute_stream = self.base.compute_stream
         self.store: ExpertStore = self.base.store
         self.state = ResidencyState()
         self.budget = budget
+        self.victim_policy = victim_policy
+        self.chunks = max(1, int(chunks))
         self.peak = 0
+        self.ffn_events = None  # (per-layer FFN timing is single-GPU only)
+        self.mix_events: list = []
 
     def hash_tokens(self, batch_id, tokens_dev, lengths):
-        return self.base.hash_tokens(batch_id, tokens_dev, lengths)
+        """Hash + permute on the hash stream, then this batch's histogram
+        all-gather enqueued right away (every rank hashes its batches in the
+        same order, so the collectives match): by the time `forward` needs the
+        count matrix it has long arrived, and the gather never queues behind
+        the previous batch's exchanges."""
+        table = self.base.hash_tokens(batch_id, tokens_dev, lengths)
+        table._ep_counts = self._gather_counts(table._dev)
+        return table
 
-    def forward(self, table, lengths, tokens_dev=None, batch=None):
-        model, store, budget = self.model, self.store, self.budget
-        c = model.config
-        h = _lib.lib()
+    def check_errors(self, tables=()) -> None:
+        flags = [(FFN_SLOT_MSG, self.store.err_flag), (OUTPROJ_MSG, self.model._err)]
+        for t in tables:
+            dt = getattr(t, "_dev", None)
+            if dt is not None:
+                flags.append((PERMUTE_MSG, dt.err))
+        check_device_flags(flags)
+
+    def _gather_counts(self, dt):
+        """(G, L, K) histograms of every rank's batch: one all-gather per
+        batch, enqueued behind the hash stream (not the busy compute stream),
+        copied to pinned host memory; returns (host tensor, ready event)."""
+        with torch.cuda.stream(self.hash_stream):
+            self.hash_stream.wait_event(dt.ready)
+            g = self.transport.all_gather(dt.hist)
+            host = torch.empty(g.shape, dtype=g.dtype, pin_memory=True)
+            host.copy_(g, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(self.hash_stream)
+        return host, ev
+
+    def _counts(self, table, dt) -> np.ndarray:
+        pend = getattr(table, "_ep_counts", None)
+        host, ev = pend if pend is not None else self._gather_counts(dt)
+        ev.synchronize()
+        return host.numpy().astype(np.int64)
+
+    def forward(self, table, lengths, tokens_dev=None, batch=None, next_table=None):
+        """One batch; returns (logits (n_seq, C) on the device, record dict,
+        (start, end) events on the compute stream) like SidaEngine.forward."""
+        model, budget = self.model, self.budget
         eb = model.expert_bytes_each()
-        cs = self.base.compute_stream
-        dt = table.on_device(model, stream=self.base.hash_stream)
+        cs = self.compute_stream
+        dt = table.on_device(model, stream=self.hash_stream)
         if tokens_dev is None:
             tokens_dev = dt.tokens_for(model, batch, cs)
-        torch.cuda.current_stream(model.device).wait_event(dt.ready)
-        counts = self.transport.all_gather(dt.hist).cpu().numpy().astype(np.int64)  # (G, L, K)
+        counts = self._counts(table, dt)
         local = _LocalTable(counts, self.rank, self.kl)
-        plan = plan_placement(local, self.state, budget, eb)
+        planner = plan_placement if self.victim_policy == "fifo" else plan_placement_spread
+        plan = planner(local, self.state, budget, eb)
         for g in plan.groups:
             if any(k[0] == g.layer and k[1] in local.required_by_layer()[g.layer]
                    for k in g.evictions):
                 raise UnservableError("a layer's local expert working set exceeds the budget")
         issuer = _GroupIssuer(self, plan, local.required_by_layer())
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        cs.wait_event(dt.ready)
+        dt.use_on(cs)
+        ev0.record(cs)
         if getattr(self.transport, "peer", False):
-            return self._forward_peer(table, dt, counts, issuer, lengths, tokens_dev)
-        # per-layer regroup maps and local offsets, uploaded once per batch
-        maps = [ep_regroup(counts, l, self.rank, self.world) for l in range(c.num_layers)]
-        splits = [ep_splits(counts, l, self.rank, self.world) for l in range(c.num_layers)]
+            logits = self._forward_peer(dt, counts, issuer, lengths, tokens_dev)
+        else:
+            logits = self._forward_nccl(dt, counts, issuer, lengths, tokens_dev)
+        ev1.record(cs)
+        resident_req = [k for k in local.required_experts() if k in self.state.resident]
+        util = (sum(self.state.resident[k] for k in resident_req) / self.state.used_bytes
+                if self.state.used_bytes else 1.0)
+        rec = {"batch_id": table.batch_id, "num_samples": len(lengths),
+               "num_tokens": int(sum(lengths)), "transfer_s": plan.estimated_transfer_s,
+               "expert_loads": len(plan.loads), "groups_issued_ahead": 0, "utilization": util}
+        return logits, rec, (ev0, ev1)
+
+    # ------------------------------------------------------------------ NCCL, chunked
+    @staticmethod
+    def _upload_plans(plans, dev):
+        """Every segment table of the batch in one pinned H2D copy."""
+        parts, index = [], []
+        pos = 0
+
+        def add(a):
+            nonlocal pos
+            parts.append(np.asarray(a, dtype=np.int32))
+            index.append((pos, len(a)))
+            pos += len(a)
+            return len(index) - 1
+
+        keys = []
+        for p in plans:
+            k = {"d_start": add(p["d_start"]), "d_val": add(p["d_val"]), "chunks": []}
+            for ch in p["chunks"]:
+                k["chunks"].append({n: add(ch[n]) for n in ("seg_start", "seg_val", "off_local")})
+            keys.append(k)
+        flat = np.concatenate(parts) if parts else np.zeros(1, dtype=np.int32)
+        buf = torch.from_numpy(flat).pin_memory().to(dev, non_blocking=True)
+
+        def view(i):
+            a, n = index[i]
+            return buf[a:a + n]
+
+        out = [{"d_start": view(k["d_start"]), "d_val": view(k["d_val"]),
+                "chunks": [{n: view(i) for n, i in ch.items()} for ch in k["chunks"]]}
+               for k in keys]
+        return out, buf
+
+    def _forward_nccl(self, dt, counts, issuer, lengths, tokens_dev):
+        model, store, tp = self.model, self.store, self.transport
+        c = model.config
+        h = _lib.lib()
+        cs = self.compute_stream
+        sh = cs.cuda_stream
         k = dt.k
+        d = c.d_model
+        dev = model.device
+        plans = [ep_layer_plan(counts, l, self.rank, self.world, self.chunks)
+                 for l in range(c.num_layers)]
         with torch.cuda.stream(cs):
-            cs.wait_event(dt.ready)
-            dt.use_on(cs)
-            lay = BatchLayout(list(lengths), tokens_dev, model.device)
-            x = model.embed_layout(lay)
-            xb = None
+            dplans, _buf = self._upload_plans(plans, dev)
+            lay = BatchLayout(list(lengths), tokens_dev, dev)
+            x, xb = model.embed_layout(lay, with_bf16=True)
             n_rows = x.shape[0] * k
             for layer in range(c.num_layers):
                 done = issuer.issue_for(layer)
-                x = model.attention_mix(layer, x, lay, xb=xb)
-                off_t, perm, alpha_perm = dt.layer(layer)
-                x_perm = torch.empty((n_rows, c.d_model), dtype=torch.bfloat16, device=x.device)
-                _lib.check(h.sida_gather_rows_bf16(x.data_ptr(), perm.data_ptr(), n_rows, k,
-                                                   c.d_model, x_perm.data_ptr(), cs.cuda_stream))
-                send_rows, recv_rows = splits[layer]
-                recv = self.transport.all_to_all(x_perm, send_rows, recv_rows)
-                src, off_local = maps[layer]
-                n_recv = int(src.size)
-                y_recv = torch.empty((n_recv, c.d_model), dtype=torch.bfloat16, device=x.device)
-                if n_recv:
-                    src_t = torch.from_numpy(src).pin_memory().to(x.device, non_blocking=True)
-                    off_l = torch.from_numpy(off_local).pin_memory().to(x.device, non_blocking=True)
-                    x_loc = torch.empty((n_recv, c.d_model), dtype=torch.bfloat16, device=x.device)
-                    _lib.check(h.sida_gather_bf16_rows(recv.data_ptr(), src_t.data_ptr(), n_recv,
-                                                       c.d_model, x_loc.data_ptr(), cs.cuda_stream))
-                    row = issuer.slot_row(layer)
-                    row_t = torch.from_numpy(row).pin_memory().to(x.device, non_blocking=True)
-                    hidden = torch.empty((n_recv, c.expert_hidden), dtype=torch.bfloat16,
-                                         device=x.device)
-                    if done is not None:
-                        cs.wait_event(done)
-                    _lib.check(h.sida_grouped_ffn_bf16(
-                        x_loc.data_ptr(), n_recv, c.d_model, c.expert_hidden, off_l.data_ptr(),
-                        self.kl, row_t.data_ptr(), None, 0, store.base_ptr, store.slot_stride,
-                        store.n_slots, src_t.data_ptr(), None, None, None, y_recv.data_ptr(),
-                        hidden.data_ptr(), store.err_flag.data_ptr(), cs.cuda_stream))
-                    ev = torch.cuda.Event()
-                    ev.record(cs)
-                    store.mark_read(row, ev)
-                y_back = self.transport.all_to_all(y_recv, recv_rows, send_rows)
-                out = torch.empty_like(x)
-                xb = torch.empty(x.shape, dtype=torch.bfloat16, device=x.device)
-                _lib.check(h.sida_unpermute_combine(
-                    y_back.data_ptr(), dt.inv[layer].data_ptr(), alpha_perm.data_ptr(),
-                    x.data_ptr(), x.shape[0], k, c.d_model, out.data_ptr(), xb.data_ptr(),
-                    cs.cuda_stream))
+                pl, dpl = plans[layer], dplans[layer]
+                # dispatch positions of my (token, rank) rows (chunk-major)
+                dmap = torch.empty(n_rows, dtype=torch.int32, device=dev)
+                _lib.check(h.sida_segment_map(dpl["d_start"].data_ptr(), dpl["d_val"].data_ptr(),
+                                              c.num_experts, dt.inv[layer].data_ptr(), n_rows,
+                                              dmap.data_ptr(), sh))
+                send = torch.empty((n_rows, d), dtype=torch.bfloat16, device=dev)
+                x_attn = model.attention_mix(layer, x, lay, xb=xb, scatter=(dmap, k, send))
+                back = torch.empty((n_rows, d), dtype=torch.bfloat16, device=dev)
+                cstart = pl["chunk_start"]
+                recvs = [tp.all_to_all_async(send[cstart[i]:cstart[i + 1]], ch["send_rows"],
+                                             ch["recv_rows"])
+                         for i, ch in enumerate(pl["chunks"])]
+                row = issuer.slot_row(layer)
+                row_t = store.rows.upload(row, cs)
+                if done is not None:
+                    cs.wait_event(done)
+                waits = []
+                for i, (ch, dch) in enumerate(zip(pl["chunks"], dpl["chunks"])):
+                    recv, wait = recvs[i]
+                    wait()
+                    n_recv = ch["n_recv"]
+                    ret = torch.empty((n_recv, d), dtype=torch.bfloat16, device=dev)
+                    e0, e1 = ch["experts"]
+                    if n_recv:
+                        src = torch.empty(n_recv, dtype=torch.int32, device=dev)
+                        _lib.check(h.sida_segment_map(
+                            dch["seg_start"].data_ptr(), dch["seg_val"].data_ptr(),
+                            (e1 - e0) * self.world, None, n_recv, src.data_ptr(), sh))
+                        x_loc = torch.empty((n_recv, d), dtype=torch.bfloat16, device=dev)
+                        _lib.check(h.sida_gather_bf16_rows(recv.data_ptr(), src.data_ptr(),
+                                                           n_recv, d, x_loc.data_ptr(), sh))
+                        hidden = torch.empty((n_recv, c.expert_hidden), dtype=torch.bfloat16,
+                                             device=dev)
+                        _lib.check(h.sida_grouped_ffn_bf16(
+                            x_loc.data_ptr(), n_recv, d, c.expert_hidden,
+                            dch["off_local"].data_ptr(), e1 - e0, row_t[e0:e1].data_ptr(), None,
+                            0, store.base_ptr, store.slot_stride, store.n_slots, src.data_ptr(),
+                            None, None, None, ret.data_ptr(), hidden.data_ptr(),
+                            store.err_flag.data_ptr(), sh))
+                    _, w = tp.all_to_all_async(ret, ch["recv_rows"], ch["send_rows"],
+                                               back[cstart[i]:cstart[i + 1]])
+                    waits.append(w)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                store.mark_read(row, ev)
+                for w in waits:
+                    w()
+                out = torch.empty_like(x_attn)
+                xb = torch.empty(x_attn.shape, dtype=torch.bfloat16, device=dev)
+                _lib.check(h.sida_map_combine(back.data_ptr(), dmap.data_ptr(),
+                                              dt.alpha_f32[layer].data_ptr(), x_attn.data_ptr(),
+                                              x_attn.shape[0], k, d, out.data_ptr(),
+                                              xb.data_ptr(), sh))
                 x = out
             logits = model.pool_classify(x, lay)
         return logits
 
     # ------------------------------------------------------------------ peer memory
-    def _forward_peer(self, table, dt, counts, issuer, lengths, tokens_dev):
+    def _forward_peer(self, dt, counts, issuer, lengths, tokens_dev):
         """The EP layer with both exchanges fused into the producing epilogues
         (PeerTransport): out-projection → owners' receive buffers (by layer
         parity) → flags → local grouped FFN whose GEMM2 epilogue writes into
         the sources' return buffers → flags → unpermute-combine."""
-        model, store, budget, tp = self.model, self.store, self.budget, self.transport
+        model, store, tp = self.model, self.store, self.transport
         c = model.config
         h = _lib.lib()
-        eb = model.expert_bytes_each()
-        cs = self.base.compute_stream
+        cs = self.compute_stream
         k = dt.k
         n_rows = int(sum(lengths)) * k
         rows_max = int(counts.sum(axis=2).max())  # largest (token, rank) count of any source
@@ -428,11 +629,8 @@ class ExpertParallelEngine:
             return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(dev, non_blocking=True)
 
         with torch.cuda.stream(cs):
-            cs.wait_event(dt.ready)
-            dt.use_on(cs)
             lay = BatchLayout(list(lengths), tokens_dev, dev)
-            x = model.embed_layout(lay)
-            xb = None
+            x, xb = model.embed_layout(lay, with_bf16=True)
             for layer in range(c.num_layers):
                 done = issuer.issue_for(layer)
                 d_start, d_val, r_start, r_val, off_l, n_recv = ep_peer_maps(

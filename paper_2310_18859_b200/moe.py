@@ -32,17 +32,14 @@ from . import _lib
 from .errors import ContractError
 
 
-# A/B switch for measurements: SIDA_ATTN_CUBLAS=1 runs the attention core as
-# cuBLAS batched products + torch softmax instead of sida_attention_core.
-_ATTN_CUBLAS = bool(os.environ.get("SIDA_ATTN_CUBLAS"))
 # SIDA_FFN_FUSED=1: the two expert GEMMs as one interleaved persistent launch
 # (sida_grouped_ffn_bf16_fused) instead of two; measured slower (base-8 0.316
 # vs 0.293 ms, base-128 0.553 vs 0.461 ms), so off by default. SIDA_FFN_LAG:
 # GEMM2 lag in m-tiles.
 _FFN_FUSED = os.environ.get("SIDA_FFN_FUSED", "0") == "1"
 _FFN_LAG = int(os.environ.get("SIDA_FFN_LAG", "32"))
-# SIDA_OUTPROJ_CUBLAS=1: output projection as cuBLAS addmm (+ the FFN's row gather)
-_OUTPROJ_CUBLAS = bool(os.environ.get("SIDA_OUTPROJ_CUBLAS"))
+# longest sequence the fused attention core serves (csrc/attention.cu)
+MAX_ATTN_TOKENS = 512
 
 
 @dataclass
@@ -215,8 +212,14 @@ def _default_device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_SEQ_OFF_CACHE: dict = {}
+
+
 class BatchLayout:
-    """A batch's concatenated global token axis on the device (ref moe.py:14-16)."""
+    """A batch's concatenated global token axis on the device (ref moe.py:14-16):
+    int32 tokens and the (n_seq + 1) int32 sequence offsets every kernel of
+    the forward reads (uniform batches reuse one cached offsets tensor, so a
+    steady-state step moves no per-token metadata)."""
 
     def __init__(self, lengths: list[int], tokens: torch.Tensor, device):
         self.lengths = [int(n) for n in lengths]
@@ -228,31 +231,20 @@ class BatchLayout:
         np.cumsum(self.lengths, out=off[1:])
         self.offsets = off
         self.tokens = tokens  # int32 (n_tokens,) on device
-        if self.uniform:  # positions derived on the device: no per-token H2D traffic
-            self.pos = torch.arange(self.n_tokens, device=device) % self.max_len
-            self.seq_off = torch.arange(0, self.n_tokens + 1, self.max_len, device=device,
-                                        dtype=torch.int32)
-            return
-
-        def h2d(a):
-            return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(device,
-                                                                              non_blocking=True)
-
-        seq_id = np.repeat(np.arange(self.n_seq), self.lengths)
-        self.pos = h2d(np.arange(self.n_tokens) - off[seq_id])
-        self.seq_off = h2d(off.astype(np.int32))
-        self.len_t = h2d(np.asarray(self.lengths, dtype=np.float32))
-        if not self.uniform:
-            pad = np.full((self.n_seq, self.max_len), self.n_tokens, dtype=np.int64)
-            for i, n in enumerate(self.lengths):
-                pad[i, :n] = np.arange(off[i], off[i] + n)
-            self.pad_index = h2d(pad.reshape(-1))
-            mask = np.zeros((self.n_seq, 1, self.max_len), dtype=np.float32)
-            for i, n in enumerate(self.lengths):
-                mask[i, 0, n:] = -np.inf
-            self.key_mask = h2d(mask)
-            self.valid_rows = h2d(np.concatenate([np.arange(i * self.max_len, i * self.max_len + n)
-                                                  for i, n in enumerate(self.lengths)]))
+        dev = torch.device(device)
+        if self.uniform:
+            key = (dev.index if dev.index is not None else torch.cuda.current_device(),
+                   self.n_seq, self.max_len)
+            t = _SEQ_OFF_CACHE.get(key)
+            if t is None:
+                if len(_SEQ_OFF_CACHE) >= 64:
+                    _SEQ_OFF_CACHE.pop(next(iter(_SEQ_OFF_CACHE)))
+                t = torch.from_numpy(off.astype(np.int32)).to(device)
+                _SEQ_OFF_CACHE[key] = t
+            self.seq_off = t
+        else:
+            self.seq_off = torch.from_numpy(off.astype(np.int32)).pin_memory().to(
+                device, non_blocking=True)
 
     @classmethod
     def from_batch(cls, model: "MoEModel", batch: SequenceBatch) -> "BatchLayout":
@@ -339,21 +331,33 @@ class MoEModel:
         return torch.cuda.current_stream(self._dev_index).cuda_stream
 
     def _prepare_out_proj(self):
-        """Per layer W_o^T (K-major) + a zero bias row: the B operand of the
-        fused output projection (sida_out_proj_scatter); tcgen05 shapes only."""
+        """Per layer the tcgen05 B operands of the mixing attention's two
+        projections, each "W^T (K-major) + a zero bias row": [Wq|Wk|Wv]^T for
+        the fused QKV GEMM (sida_linear_bf16) and W_o^T for the output
+        projection with its fused residual/scatter epilogue
+        (sida_out_proj_scatter). The B200 mixing attention needs
+        d_model % 64 == 0 (every Switch shape); other widths have no
+        attention path (attention_mix raises), the expert FFN still runs."""
         d = self.config.d_model
         self._dev_index = self.device.index if self.device.index is not None else \
             torch.cuda.current_device()
         self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
-        self.wo_t = None
-        if d % 64 or _OUTPROJ_CUBLAS:
+        self.wo_t = self.wqkv_t = None
+        if d % 64:
             return
-        nbytes = int(_lib.load().sida_out_proj_bytes(d))
+        h = _lib.load()
+        nbytes = int(h.sida_out_proj_bytes(d))
         self.wo_t = []
         for w in self.wo:
             buf = torch.zeros(nbytes // 2, dtype=torch.bfloat16, device=self.device)
             buf[: d * d] = w.t().contiguous().view(-1)
             self.wo_t.append(buf)
+        qbytes = int(h.sida_linear_bytes(d, 3 * d))
+        self.wqkv_t = []
+        for w in self.wqkv:
+            buf = torch.zeros(qbytes // 2, dtype=torch.bfloat16, device=self.device)
+            buf[: 3 * d * d] = w.t().contiguous().view(-1)
+            self.wqkv_t.append(buf)
 
     @classmethod
     def synthetic(cls, config: MoEConfig, seed: int = 0, device=None) -> "MoEModel":
@@ -389,6 +393,32 @@ class MoEModel:
             self.expert_images[i].copy_(img.view(torch.uint8))
         torch.cuda.synchronize(self.device)
         return self
+
+    def reference_params(self) -> dict[str, np.ndarray]:
+        """The model's weights as a reference parameter dict (float64 of the
+        bf16 values actually served; ref moe.py:158-181 names and layouts),
+        e.g. to check a `synthetic` model end to end against the oracle."""
+        c = self.config
+        d, hh = c.d_model, c.expert_hidden
+
+        def f64(t):
+            return t.detach().float().cpu().numpy().astype(np.float64)
+
+        p = {"tok_emb": f64(self.tok_emb), "pos_emb": f64(self.pos_emb), "wc": f64(self.wc)}
+        for layer in range(c.num_layers):
+            pre = f"block{layer}."
+            wq, wk, wv = f64(self.wqkv[layer]).reshape(d, 3, d).transpose(1, 0, 2)
+            p[pre + "wq"], p[pre + "wk"], p[pre + "wv"] = wq, wk, wv
+            p[pre + "wo"] = f64(self.wo[layer])
+            p[pre + "w_r"] = f64(self.w_r[layer])
+            imgs = self.expert_images[layer * c.num_experts:(layer + 1) * c.num_experts]
+            raw = imgs.view(torch.bfloat16)[:, : 2 * d * hh + hh + d].float().numpy()
+            raw = raw.astype(np.float64)
+            p[pre + "w1"] = raw[:, : hh * d].reshape(-1, hh, d).transpose(0, 2, 1).copy()
+            p[pre + "w2"] = raw[:, hh * d: 2 * hh * d].reshape(-1, d, hh).transpose(0, 2, 1).copy()
+            p[pre + "b1"] = raw[:, 2 * hh * d: 2 * hh * d + hh].copy()
+            p[pre + "b2"] = raw[:, 2 * hh * d + hh:].copy()
+        return p
 
     # -- parameter bookkeeping (ref moe.py:188-198) ---------------------------------
     def expert_bytes_each(self) -> int:
@@ -431,58 +461,54 @@ class MoEModel:
         te = self.tok_emb.index_select(0, torch.from_numpy(toks).to(self.device)).double()
         return (te + self.pos_emb[: toks.size].double()).cpu().numpy()
 
-    def embed_layout(self, lay: BatchLayout) -> torch.Tensor:
-        """float32 (n_tokens, d): tok_emb[t] + pos_emb[pos] (exact in fp32)."""
-        return (self.tok_emb.index_select(0, lay.tokens.long()).float()
-                + self.pos_emb.index_select(0, lay.pos).float())
+    def embed_layout(self, lay: BatchLayout, with_bf16: bool = False):
+        """float32 (n_tokens, d): tok_emb[t] + pos_emb[pos] (exact in fp32),
+        one sida_embed launch; ``with_bf16`` also returns its bf16 copy (the
+        first QKV projection's input) from the same kernel."""
+        d = self.config.d_model
+        x = torch.empty((lay.n_tokens, d), dtype=torch.float32, device=self.device)
+        xb = torch.empty((lay.n_tokens, d), dtype=torch.bfloat16, device=self.device)
+        _lib.check(_lib.lib().sida_embed(
+            lay.tokens.data_ptr(), lay.seq_off.data_ptr(), lay.n_seq, lay.n_tokens,
+            self.tok_emb.data_ptr(), self.pos_emb.data_ptr(), d, x.data_ptr(), xb.data_ptr(),
+            self._stream_handle()))
+        return (x, xb) if with_bf16 else x
 
     def attention_mix(self, layer: int, x: torch.Tensor, lay: BatchLayout,
                       xb: torch.Tensor | None = None, scatter=None) -> torch.Tensor:
-        """x + softmax(q k^T / sqrt(d)) v W_o per sequence (ref moe.py:220-233).
-
-        The QKV projection is a cuBLAS bf16 GEMM. For sequences of at most 256
-        tokens (d % 128 == 0) the score / softmax / context core is the fused
-        tcgen05 kernel sida_attention_core; longer sequences use cuBLAS batched
-        products (scores with fp32 outputs) and torch softmax. The output projection is the
-        tcgen05 GEMM of sida_out_proj_scatter with the residual add fused,
-        and -- given ``scatter = (inv, k, x_perm)`` from the layer's hash
-        table -- it also writes the next FFN's expert-sorted bf16 input rows
-        x_perm[inv[t*k + r]] (the row gather of ref moe.py:253-256), so the
-        FFN needs no gather pass. ``xb`` is x already rounded to bf16 (the
+        """x + softmax(q k^T / sqrt(d)) v W_o per sequence (ref moe.py:220-233),
+        three tcgen05 launches: the fused QKV projection (sida_linear_bf16),
+        the attention core (sida_attention_core: scores, softmax and P.V
+        on chip, sequences of up to 512 tokens) and the output projection
+        (sida_out_proj_scatter) with the residual add fused -- given
+        ``scatter = (inv, k, x_perm)`` from the layer's hash table it also
+        writes the next FFN's expert-sorted bf16 input rows x_perm[inv[t*k+r]]
+        (the row gather of ref moe.py:253-256), so the FFN needs no gather
+        pass. ``xb`` is x already rounded to bf16 (the embedding kernel or the
         previous layer's FFN epilogue writes it)."""
         d = self.config.d_model
+        if self.wo_t is None:
+            raise _lib.NativeLibraryError(
+                f"the B200 mixing attention needs d_model % 64 == 0 (got {d})")
+        if lay.max_len > MAX_ATTN_TOKENS:
+            raise _lib.NativeLibraryError(
+                f"the fused attention core serves sequences of at most {MAX_ATTN_TOKENS} "
+                f"tokens (got {lay.max_len})")
         if xb is None:
             xb = x.to(torch.bfloat16)
-        qkv = xb @ self.wqkv[layer]
-        if d % 128 == 0 and lay.max_len <= 256 and not _ATTN_CUBLAS:
-            # fused tcgen05 core: scores, softmax and P.V without HBM round trips
-            ctx = torch.empty((lay.n_tokens, d), dtype=torch.bfloat16, device=x.device)
-            _lib.check(_lib.lib().sida_attention_core(
-                qkv.data_ptr(), lay.seq_off.data_ptr(), lay.n_seq, lay.n_tokens, lay.max_len, d,
-                ctx.data_ptr(), self._stream_handle()))
-            return self._out_proj(layer, x, ctx, scatter)
-        if lay.uniform:
-            qkv = qkv.view(lay.n_seq, lay.max_len, 3 * d)
-        else:
-            qkv = torch.cat([qkv, qkv.new_zeros(1, 3 * d)]).index_select(0, lay.pad_index)
-            qkv = qkv.view(lay.n_seq, lay.max_len, 3 * d)
-        q, k, v = qkv.split(d, dim=2)
-        scores = torch.bmm(q, k.transpose(1, 2), out_dtype=torch.float32)
-        scores.div_(math.sqrt(d))
-        if not lay.uniform:
-            scores.add_(lay.key_mask)
-        attn = torch.softmax(scores, dim=-1).to(torch.bfloat16)
-        ctx = torch.bmm(attn, v).reshape(-1, d)
-        if not lay.uniform:
-            ctx = ctx.index_select(0, lay.valid_rows)
+        h = _lib.lib()
+        sh = self._stream_handle()
+        qkv = torch.empty((lay.n_tokens, 3 * d), dtype=torch.bfloat16, device=x.device)
+        _lib.check(h.sida_linear_bf16(xb.data_ptr(), lay.n_tokens, d, 3 * d,
+                                      self.wqkv_t[layer].data_ptr(), qkv.data_ptr(),
+                                      self._err.data_ptr(), sh))
+        ctx = torch.empty((lay.n_tokens, d), dtype=torch.bfloat16, device=x.device)
+        _lib.check(h.sida_attention_core(qkv.data_ptr(), lay.seq_off.data_ptr(), lay.n_seq,
+                                         lay.n_tokens, lay.max_len, d, ctx.data_ptr(), sh))
         return self._out_proj(layer, x, ctx, scatter)
 
     def _out_proj(self, layer: int, x: torch.Tensor, ctx: torch.Tensor, scatter):
         d = self.config.d_model
-        if self.wo_t is None:  # d not a multiple of 64: cuBLAS
-            if scatter is not None:
-                raise ContractError("fused expert-sorted scatter needs d % 64 == 0")
-            return torch.addmm(x, ctx, self.wo[layer], out_dtype=torch.float32)
         out = torch.empty_like(x)
         if scatter is not None and scatter[0] == "peer":
             # expert parallel: rows go straight to the owners' receive buffers
@@ -500,13 +526,14 @@ class MoEModel:
         return out
 
     def pool_classify(self, x: torch.Tensor, lay: BatchLayout) -> torch.Tensor:
-        """(n_seq, C): per-sequence mean then the classifier (ref moe.py:264-266)."""
-        if lay.uniform:
-            pooled = x.view(lay.n_seq, lay.max_len, -1).mean(dim=1)
-        else:  # padded gather + sum: deterministic (no atomics)
-            xp = torch.cat([x, x.new_zeros(1, x.shape[1])]).index_select(0, lay.pad_index)
-            pooled = xp.view(lay.n_seq, lay.max_len, -1).sum(dim=1) / lay.len_t[:, None]
-        return pooled @ self.wc
+        """(n_seq, C): per-sequence mean then the classifier (ref moe.py:264-266),
+        one sida_pool_classify launch."""
+        c = self.config
+        logits = torch.empty((lay.n_seq, c.num_classes), dtype=torch.float32, device=self.device)
+        _lib.check(_lib.lib().sida_pool_classify(x.data_ptr(), lay.seq_off.data_ptr(), lay.n_seq,
+                                                 c.d_model, self.wc.data_ptr(), c.num_classes,
+                                                 logits.data_ptr(), self._stream_handle()))
+        return logits
 
     def route(self, layer: int, x: torch.Tensor, k: int, stream=None, want_probs: bool = True):
         """Teacher routing on the GPU (ref moe.py:296-301): one fused kernel,

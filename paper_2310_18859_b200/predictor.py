@@ -161,8 +161,7 @@ class DeviceTable:
         self.alpha_perm = torch.empty((L, rows), dtype=torch.float32, device=dev)
         ws_bytes = h.sida_permute_workspace_bytes(L, rows, num_experts)
         ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-        with torch.cuda.stream(stream):
-            self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.err = torch.empty(1, dtype=torch.int32, device=dev)  # zeroed by the call
         _lib.check(h.sida_permute_hist(
             self.ids.data_ptr(), L, rows, num_experts, self.alpha_f32.data_ptr(),
             self.hist.data_ptr(), self.off.data_ptr(), self.perm.data_ptr(), self.inv.data_ptr(),

@@ -147,3 +147,72 @@ def test_peer_maps_round_trip(world, K, L):
                 src, pos = divmod(int(v), sy)
                 assert (src, pos) == keys[j][:2]
             assert off_l[-1] == n_recv
+
+
+@pytest.mark.parametrize("world,K,L,chunks", [(2, 8, 2, 2), (4, 8, 2, 3), (8, 128, 1, 2),
+                                              (1, 4, 2, 1), (2, 128, 1, 4)])
+def test_chunked_layer_plan_round_trip(world, K, L, chunks):
+    """The chunked NCCL path's maps (ep_layer_plan, applied like
+    sida_segment_map / all_to_all_single / the FFN row_map would): each
+    chunk's exchange delivers every row to its owner, the regrouped rows are
+    expert-major / source-minor (ep_regroup's order within the chunk), and the
+    return exchange lands each row back at the dispatch position its source
+    sent it from (the position sida_map_combine reads)."""
+    from paper_2310_18859_b200.expert_parallel import ep_layer_plan
+
+    g = np.random.default_rng(world * 7 + K + chunks)
+    counts = g.integers(0, 5, size=(world, L, K))
+    counts[0, 0, :K // 2] = 0
+    kl = K // world
+    for layer in range(L):
+        plans = [ep_layer_plan(counts, layer, r, world, chunks) for r in range(world)]
+        # each source's rows tagged (src, x_perm position, expert), placed by dmap
+        sends = []
+        for r, p in enumerate(plans):
+            n = int(counts[r, layer].sum())
+            dmap = _seg_map(p["d_start"].astype(np.int64), p["d_val"], K, np.arange(n))
+            assert sorted(dmap.tolist()) == list(range(n))
+            buf = [None] * n
+            for pos in range(n):
+                e = int(np.searchsorted(p["d_start"], pos, side="right")) - 1
+                buf[dmap[pos]] = (r, pos, e)
+            sends.append(buf)
+        n_chunks = len(plans[0]["chunks"])
+        backs = [[None] * len(s) for s in sends]
+        for ci in range(n_chunks):
+            # all_to_all_single of chunk ci
+            recvs = []
+            for q in range(world):
+                parts = []
+                for src in range(world):
+                    ch = plans[src]["chunks"][ci]
+                    cs0 = plans[src]["chunk_start"][ci]
+                    off = cs0 + sum(ch["send_rows"][:q])
+                    parts += sends[src][off:off + ch["send_rows"][q]]
+                assert len(parts) == sum(plans[q]["chunks"][ci]["recv_rows"])
+                recvs.append(parts)
+            for q in range(world):
+                ch = plans[q]["chunks"][ci]
+                e0, e1 = ch["experts"]
+                n = ch["n_recv"]
+                src_map = _seg_map(ch["seg_start"].astype(np.int64), ch["seg_val"],
+                                   (e1 - e0) * world, np.arange(n))
+                x_loc = [recvs[q][j] for j in src_map]
+                assert all(q * kl + e0 <= t[2] < q * kl + e1 for t in x_loc)
+                assert x_loc == sorted(x_loc, key=lambda t: (t[2], t[0], t[1]))
+                assert np.diff(ch["off_local"]).tolist() == \
+                    counts[:, layer, q * kl + e0:q * kl + e1].sum(0).tolist()
+                # FFN writes x_loc row j back to receive position src_map[j]
+                ret = [None] * n
+                for j, v in enumerate(src_map):
+                    ret[v] = x_loc[j]
+                # return all_to_all: recv_rows / send_rows swapped
+                pos = 0
+                for src in range(world):
+                    cnt = ch["recv_rows"][src]
+                    chs = plans[src]["chunks"][ci]
+                    at = plans[src]["chunk_start"][ci] + sum(chs["send_rows"][:q])
+                    backs[src][at:at + cnt] = ret[pos:pos + cnt]
+                    pos += cnt
+        for r in range(world):
+            assert backs[r] == sends[r]

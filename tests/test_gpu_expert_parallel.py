@@ -24,7 +24,13 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q, peer=False):
+C0 = dict(vocab_size=512, d_model=256, num_layers=2, num_experts=8, expert_hidden=1024,
+          max_seq_len=128)
+BASE128 = dict(vocab_size=512, d_model=768, num_layers=2, num_experts=128, expert_hidden=3072,
+               max_seq_len=128)
+
+
+def _worker(rank, world, port, q, peer=False, cfg=None, slots=None, vs_oracle=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     try:
         torch.cuda.set_device(0)
@@ -37,12 +43,13 @@ def _worker(rank, world, port, q, peer=False):
         from paper_2310_18859_b200.expert_parallel import (ExpertParallelEngine, GlooTransport,
                                                            PeerTransport)
 
-        shape = omoe.MoEShape(vocab_size=512, d_model=256, num_layers=2, num_experts=8,
-                              expert_hidden=1024, max_seq_len=128)
+        cfg = cfg or C0
+        shape = omoe.MoEShape(**cfg)
+        L, K, d = cfg["num_layers"], cfg["num_experts"], cfg["d_model"]
         params = omoe.bf16_params(omoe.init_params(shape, 0))
         model = MoEModel(MoEConfig(**shape.__dict__), params=params)
-        pp = opred.init_params(opred.PredictorShape(256, 2, 8), 1)
-        net = PredictorNet(PredictorConfig(), 256, 2, 8, params=pp)
+        pp = opred.init_params(opred.PredictorShape(d, L, K), 1)
+        net = PredictorNet(PredictorConfig(), d, L, K, params=pp)
         eb = model.expert_bytes_each()
         g = torch.Generator(device="cuda").manual_seed(100 + rank)
         B, T = 3 + rank, 64
@@ -50,16 +57,25 @@ def _worker(rank, world, port, q, peer=False):
         toks = torch.randint(0, 512, (B * T,), generator=g, device="cuda", dtype=torch.int32)
 
         transport = PeerTransport(control=GlooTransport()) if peer else GlooTransport()
-        ep = ExpertParallelEngine(model, net, MemoryBudget(8 * eb), transport=transport)
-        for bid in range(2 if peer else 1):  # peer: a second batch reuses the mapped buffers
+        n_local = L * K // world
+        ep = ExpertParallelEngine(model, net, MemoryBudget((slots or n_local) * eb),
+                                  transport=transport)
+        for bid in range(2 if (peer or slots) else 1):  # later batches reuse buffers / slots
             table = ep.hash_tokens(bid, toks, lengths)
             got = ep.forward(table, lengths, tokens_dev=toks)
         torch.cuda.synchronize()
-        single = SidaEngine(model, net, MemoryBudget(16 * eb))
-        t2 = single.hash_tokens(0, toks, lengths)
-        ref, _, _ = single.forward(t2, lengths, tokens_dev=toks)
-        torch.cuda.synchronize()
-        got, ref = got.cpu().numpy(), ref.cpu().numpy()
+        ep.base.check_errors([table])
+        got = got.cpu().numpy()
+        if vs_oracle:
+            seqs = [t.cpu().numpy() for t in toks.view(B, T)]
+            ref = omoe.forward_external(params, shape, seqs, table.ids, table.alphas,
+                                        grouped=True)
+        else:
+            single = SidaEngine(model, net, MemoryBudget(L * K * eb))
+            t2 = single.hash_tokens(0, toks, lengths)
+            ref, _, _ = single.forward(t2, lengths, tokens_dev=toks)
+            torch.cuda.synchronize()
+            ref = ref.cpu().numpy()
         rms = float(np.sqrt(np.mean(ref ** 2)))
         err = float(np.max(np.abs(got - ref) - 2e-2 * np.abs(ref)) / rms)
         q.put((rank, "ok" if err <= 2e-2 else f"logits off by {err:.3e} rms"))
@@ -72,17 +88,38 @@ def _worker(rank, world, port, q, peer=False):
             dist.destroy_process_group()
 
 
+def _run(world=2, **kw):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q), kwargs=kw)
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: "ok" for r in range(world)}, res
+
+
 @pytest.mark.parametrize("peer", [False, True])
 def test_expert_parallel_two_ranks_one_gpu(cuda_device, peer):
     """peer=False: NCCL-style all-to-all (gloo here); peer=True: the exchanges
     fused into the epilogues over CUDA-IPC-mapped buffers (PeerTransport)."""
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, peer)) for r in range(2)]
-    for p in procs:
-        p.start()
-    res = dict(q.get(timeout=300) for _ in procs)
-    for p in procs:
-        p.join(timeout=60)
-    assert res == {0: "ok", 1: "ok"}, res
+    _run(peer=peer)
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_expert_parallel_budget_below_local_working_set(cuda_device, peer):
+    """6 slots per rank for L x K/G = 8 local experts, so
+    every batch evicts experts of earlier layers of the same batch; slots are
+    taken group by group, so every layer still finds its experts."""
+    _run(peer=peer, slots=6)
+
+
+@pytest.mark.parametrize("peer", [False, True])
+def test_expert_parallel_base128_vs_oracle(cuda_device, peer):
+    """Switch-base-128 expert width (d=768, h=3072, K=128, 64 experts per
+    rank), two layers, logits against the oracle forward on each rank's own
+    tokens and hash table (SURVEY §8(e) at the north-star shape)."""
+    _run(peer=peer, cfg=BASE128, vs_oracle=True)

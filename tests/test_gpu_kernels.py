@@ -413,7 +413,10 @@ def test_out_proj_scatter_vs_torch_fp32(cuda_device, n, d, k):
 @pytest.mark.parametrize("lengths,d", [([128] * 3, 768), ([1, 5, 77, 128, 64, 128], 256),
                                        ([100] * 7 + [3], 128), ([128] * 300, 768),
                                        ([256] * 4, 768), ([129, 3, 256, 200, 1], 256),
-                                       ([256] * 150, 768)])
+                                       ([256] * 150, 768), ([512] * 3, 768),
+                                       ([257, 1, 512, 300, 384], 256), ([512] * 64, 768),
+                                       ([300, 511, 7], 128), ([5, 128, 64], 64),
+                                       ([200, 17], 192), ([400, 512], 64)])
 def test_attention_core_vs_torch_fp32(cuda_device, lengths, d):
     """ctx = softmax(q k^T / sqrt(d)) v per sequence (ref moe.py:220-233 core)
     against an fp32 torch reference on the same bf16 q, k, v, at the bf16 bar
@@ -450,9 +453,37 @@ def test_attention_core_contracts(cuda_device):
     qkv = torch.zeros((300, 3 * 128), dtype=torch.bfloat16, device="cuda")
     off = torch.tensor([0, 43, 300], dtype=torch.int32, device="cuda")
     ctx = torch.empty((300, 128), dtype=torch.bfloat16, device="cuda")
-    with pytest.raises(NativeLibraryError):  # sequence longer than 256 tokens
-        _lib.check(_lib.lib().sida_attention_core(qkv.data_ptr(), off.data_ptr(), 2, 300, 257,
+    with pytest.raises(NativeLibraryError):  # sequence longer than 512 tokens
+        _lib.check(_lib.lib().sida_attention_core(qkv.data_ptr(), off.data_ptr(), 2, 300, 513,
                                                   128, ctx.data_ptr(), None))
+    with pytest.raises(NativeLibraryError):  # d not a multiple of 64
+        _lib.check(_lib.lib().sida_attention_core(qkv.data_ptr(), off.data_ptr(), 2, 300, 257,
+                                                  96, ctx.data_ptr(), None))
+
+
+@pytest.mark.parametrize("n,k,nout", [(37, 256, 768), (1000, 768, 2304), (5000, 768, 2304),
+                                      (300, 128, 384)])
+def test_linear_bf16_vs_torch(cuda_device, n, k, nout):
+    """The fused QKV projection GEMM (sida_linear_bf16: GEMM1 tiles, identity
+    epilogue): bf16 out = x W against an fp32 torch product of the same bf16
+    operands, within one bf16 rounding (rtol 2e-2 bar, measured ~4e-3)."""
+    from paper_2310_18859_b200 import _lib
+
+    h = _lib.lib()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(n + k)
+    x = torch.randn((n, k), generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn((k, nout), generator=g, device="cuda") / k ** 0.5).to(torch.bfloat16)
+    buf = torch.zeros(int(h.sida_linear_bytes(k, nout)) // 2, dtype=torch.bfloat16, device="cuda")
+    buf[: k * nout] = w.t().contiguous().view(-1)
+    out = torch.empty((n, nout), dtype=torch.bfloat16, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(h.sida_linear_bf16(x.data_ptr(), n, k, nout, buf.data_ptr(), out.data_ptr(),
+                                  err.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    ref = x.float() @ w.float()
+    close_rms(out.float().cpu().numpy(), ref.cpu().numpy(), 2e-2)
+    assert (out.float() < 0).any()  # no ReLU on the linear path
+    assert err.item() == 0
 
 
 @pytest.mark.parametrize("d,hdim,K,N,k,lag", [
