@@ -754,8 +754,8 @@ def run_ours(args):
                       "marginal): a batch activates a subset of the experts, the regime SiDA "
                       "saves memory in",
             "budgets": budget_runs(model, pred, cfg, lengths,
-                                   [(1.0, "fifo"), (0.8, "spread"), (0.7, "spread"),
-                                    (0.6, "spread"), (0.8, "fifo")], zipf=True, seed=1)}
+                                   [(1.0, "fifo"), (0.9, "spread"), (0.85, "spread"),
+                                    (0.8, "spread"), (0.7, "spread")], zipf=True, seed=1)}
         for r in line["memory_regime_zipf"]["budgets"]:
             r["copy_ms_per_step_at_link"] = r["expert_loads_per_step"] * eb / (link * 1e9) * 1e3
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -98,8 +98,9 @@ int sida_debug_hash_prof(unsigned long long* out);
  * Outputs per layer: hist (L,K), off (L,K+1), perm (L,n_rows) stable by
  * row within expert, inv (L,n_rows) with inv[perm[p]] = p; alpha_perm
  * (optional, L x n_rows float32) = alpha_rows[perm[p]]. err_flag (int32,
- * zeroed by the call, set to 1 when an id lies outside [0, K): the caller
- * reads it at its next synchronisation point -> ContractError).
+ * set to 1 when an id lies outside [0, K), never cleared by the call: a
+ * sticky flag the caller zeroes once and reads at its next synchronisation
+ * point -> ContractError).
  * Replaces the implicit grouping of ref moe.py:253-256 (w1[ids] gather).
  * ------------------------------------------------------------------- */
 size_t sida_permute_workspace_bytes(int n_layers, int n_rows, int num_experts);

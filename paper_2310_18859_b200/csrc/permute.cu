@@ -68,6 +68,7 @@ hist_tiles_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tile
   extern __shared__ int32_t s_hist[];  // [K]
   const int layer = blockIdx.y, tile = blockIdx.x;
   const int lane = threadIdx.x & 31;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int e = threadIdx.x; e < K; e += blockDim.x) s_hist[e] = 0;
   const int r0 = tile * TILE, r1 = min(n_rows, r0 + TILE);
   stage_ids(ids + (size_t)layer * n_rows, r0, r1, s_ids);
@@ -86,58 +87,13 @@ hist_tiles_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tile
   for (int e = threadIdx.x; e < K; e += blockDim.x) c[e] = s_hist[e];
 }
 
-// One CTA per layer, thread e = expert e: totals over tiles, exclusive scan
-// over experts (off, hist), then the base position of every (tile, expert).
-__global__ void __launch_bounds__(1024)
-scan_kernel(const int32_t* __restrict__ counts, int K, int n_tiles, int32_t* __restrict__ tile_base,
-            int32_t* __restrict__ hist, int32_t* __restrict__ off) {
-  __shared__ int32_t s_warp[32];
-  const int layer = blockIdx.x, e = threadIdx.x;
-  const int lane = e & 31, warp = e >> 5;
-  const int32_t* c = counts + (size_t)layer * n_tiles * K;
-  int tot = 0;
-  if (e < K)
-    for (int t = 0; t < n_tiles; ++t) tot += c[(size_t)t * K + e];
-  int incl = tot;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += v;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    const int nw = blockDim.x >> 5;
-    const int w = lane < nw ? s_warp[lane] : 0;
-    int wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += v;
-    }
-    s_warp[lane] = wi - w;
-  }
-  __syncthreads();
-  const int excl = s_warp[warp] + incl - tot;
-  if (e < K) {
-    hist[(size_t)layer * K + e] = tot;
-    off[(size_t)layer * (K + 1) + e] = excl;
-    if (e == K - 1) off[(size_t)layer * (K + 1) + K] = excl + tot;
-    int run = excl;
-    int32_t* tb = tile_base + (size_t)layer * n_tiles * K;
-    for (int t = 0; t < n_tiles; ++t) {
-      tb[(size_t)t * K + e] = run;
-      run += c[(size_t)t * K + e];
-    }
-  }
-}
-
 template <int TILE>
 __global__ void __launch_bounds__(kPermThreads, 2)
 scatter_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
-               const int32_t* __restrict__ tile_base, const float* __restrict__ alpha_rows,
+               const int32_t* __restrict__ counts, const float* __restrict__ alpha_rows,
                int32_t* __restrict__ perm, int32_t* __restrict__ inv,
-               float* __restrict__ alpha_perm) {
+               float* __restrict__ alpha_perm, int32_t* __restrict__ hist,
+               int32_t* __restrict__ off) {
   constexpr int R = TILE / kPermWarps;  // contiguous rows per warp
   constexpr int NR = R / 32;            // rounds per warp
   extern __shared__ int32_t smem[];
@@ -149,10 +105,47 @@ scatter_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
   const int layer = blockIdx.y, tile = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r0 = tile * TILE, r1 = min(n_rows, r0 + TILE), n = r1 - r0;
-  const int32_t* tb = tile_base + ((size_t)layer * n_tiles + tile) * K;
   for (int i = threadIdx.x; i < kPermWarps * K; i += blockDim.x) s_cnt[i] = 0;
-  for (int e = threadIdx.x; e < K; e += blockDim.x) s_tbase[e] = tb[e];
   stage_ids(ids + (size_t)layer * n_rows, r0, r1, s_ids);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // hist_tiles' counts are complete
+  // this tile's base positions from the layer's (tile, expert) count matrix
+  // (written by hist_tiles; n_tiles x K ints read from L2): per expert the
+  // total and the count in earlier tiles, then an exclusive scan of the
+  // totals over experts; tile 0 also publishes hist / off
+  const int32_t* cl = counts + (size_t)layer * n_tiles * K;
+  for (int e = threadIdx.x; e < K; e += blockDim.x) {
+    int tot = 0, pre = 0;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int c = __ldg(cl + (size_t)t * K + e);
+      tot += c;
+      pre += t < tile ? c : 0;
+    }
+    s_texc[e] = tot;
+    s_tbase[e] = pre;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int carry = 0;
+    for (int b = 0; b < K; b += 32) {
+      const int e = b + lane;
+      const int v = e < K ? s_texc[e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (e < K) {
+        s_tbase[e] += carry + incl - v;
+        if (tile == 0) {
+          hist[(size_t)layer * K + e] = v;
+          off[(size_t)layer * (K + 1) + e] = carry + incl - v;
+        }
+      }
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tile == 0 && lane == 0) off[(size_t)layer * (K + 1) + K] = carry;
+  }
   __syncthreads();
 
   // pass 1: in-order stable local ranks, per warp over its R rows
@@ -270,30 +263,40 @@ extern "C" size_t sida_permute_workspace_bytes(int n_layers, int n_rows, int num
 template <int TILE>
 static int permute_launch(const int32_t* ids, int n_layers, int n_rows, int K, const float* alpha_rows,
                           int32_t* hist, int32_t* off, int32_t* perm, int32_t* inv,
-                          float* alpha_perm, int32_t* counts, int32_t* tile_base, int32_t* err,
+                          float* alpha_perm, int32_t* counts, int32_t* err,
                           cudaStream_t s) {
   const int n_tiles = perm_tiles(n_rows, TILE);
   dim3 grid(n_tiles, n_layers);
   hist_tiles_kernel<TILE><<<grid, kPermThreads, K * sizeof(int32_t), s>>>(ids, n_rows, K, n_tiles,
                                                                          counts, err);
   SIDA_LAUNCH_CHECK();
-  const int scan_threads = std::max(32, ceil_div(K, 32) * 32);
-  scan_kernel<<<n_layers, scan_threads, 0, s>>>(counts, K, n_tiles, tile_base, hist, off);
-  SIDA_LAUNCH_CHECK();
-  if (n_rows > 0) {
-    const size_t smem = (2ull * TILE + (size_t)(kPermWarps + 2) * K + 1) * sizeof(int32_t);
-    static bool configured = false;
-    if (!configured) {
-      SIDA_CUDA(cudaFuncSetAttribute(scatter_kernel<TILE>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)((2ull * TILE + (kPermWarps + 2) * kMaxExperts + 1) *
-                                           sizeof(int32_t))));
-      configured = true;
-    }
-    scatter_kernel<TILE><<<grid, kPermThreads, smem, s>>>(ids, n_rows, K, n_tiles, tile_base,
-                                                          alpha_rows, perm, inv, alpha_perm);
-    SIDA_LAUNCH_CHECK();
+  // the scatter also publishes hist / off, so it runs even for zero rows;
+  // programmatic dependent launch: its CTAs stage their ids while the
+  // histogram grid drains and wait (griddepcontrol.wait) only before reading
+  // the count matrix
+  const size_t smem = (2ull * TILE + (size_t)(kPermWarps + 2) * K + 1) * sizeof(int32_t);
+  static bool configured = false;
+  if (!configured) {
+    SIDA_CUDA(cudaFuncSetAttribute(scatter_kernel<TILE>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)((2ull * TILE + (kPermWarps + 2) * kMaxExperts + 1) *
+                                         sizeof(int32_t))));
+    configured = true;
   }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kPermThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SIDA_CUDA(cudaLaunchKernelEx(&cfg, scatter_kernel<TILE>, ids, n_rows, K, n_tiles,
+                               (const int32_t*)counts, alpha_rows, perm, inv, alpha_perm, hist,
+                               off));
+  count_launch();
   return SIDA_OK;
 }
 
@@ -311,20 +314,18 @@ extern "C" int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, i
   SIDA_REQUIRE(err_flag && hist && off && (n_rows == 0 || (ids && perm && inv)), SIDA_ERR_CONTRACT,
                "null pointer passed to sida_permute_hist");
   cudaStream_t s = as_stream(stream);
-  SIDA_CUDA(cudaMemsetAsync(err_flag, 0, sizeof(int32_t), s));
   const int tile = perm_tile(n_rows, n_layers);
   const size_t n = (size_t)n_layers * num_experts * perm_tiles(n_rows, tile);
   int32_t* counts = static_cast<int32_t*>(workspace);
-  int32_t* tile_base = counts + n;
   switch (tile) {
     case 1024: return permute_launch<1024>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
-                                           perm, inv, alpha_perm, counts, tile_base, err_flag, s);
+                                           perm, inv, alpha_perm, counts, err_flag, s);
     case 2048: return permute_launch<2048>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
-                                           perm, inv, alpha_perm, counts, tile_base, err_flag, s);
+                                           perm, inv, alpha_perm, counts, err_flag, s);
     case 4096: return permute_launch<4096>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
-                                           perm, inv, alpha_perm, counts, tile_base, err_flag, s);
+                                           perm, inv, alpha_perm, counts, err_flag, s);
     default: return permute_launch<8192>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
-                                         perm, inv, alpha_perm, counts, tile_base, err_flag, s);
+                                         perm, inv, alpha_perm, counts, err_flag, s);
   }
 }
 

@@ -34,7 +34,7 @@ from .offload import (
     plan_placement_spread,
     run_waves,
 )
-from .predictor import ExpertHashTable, hash_device
+from .predictor import DeviceTableRing, ExpertHashTable
 
 
 def prepare_waves(plan, required, store: ExpertStore) -> list[list[Wave]]:
@@ -188,12 +188,17 @@ class SidaEngine:
         self._graphs: dict = {}
         self._graph_seen: dict = {}
         self.graph_replays = 0
+        # device table ring behind hash_tokens (one batch hashed ahead + slack)
+        self.ring = DeviceTableRing(3, dev, strict=False)
 
     # -- hash stream ------------------------------------------------------------------
     def hash_tokens(self, batch_id: int, tokens_dev: torch.Tensor, lengths) -> ExpertHashTable:
-        """Hash + permute for device-resident tokens on the hash stream."""
-        return hash_device(self.predictor, self.model, tokens_dev, list(lengths),
-                           self.eval_top_k, batch_id, self.hash_stream)
+        """Hash + permute for device-resident tokens on the hash stream, into
+        the next slot of the engine's device table ring (forward releases it;
+        with three tables outstanding, or ids out of order, the table is built
+        in fresh allocations instead)."""
+        return self.ring.produce(self.predictor, self.model, lengths, self.eval_top_k,
+                                 self.hash_stream, batch_id, tokens_dev=tokens_dev)
 
     # -- compute stream ---------------------------------------------------------------
     def forward(self, table: ExpertHashTable, lengths, tokens_dev: torch.Tensor | None = None,
@@ -222,6 +227,7 @@ class SidaEngine:
         if self._graphable(bp, dt, lengths):
             logits = self._forward_graph(bp, dt, lengths, tokens_dev)
             ev1.record(cs)
+            DeviceTableRing.release(table, cs)
             return logits, self._record(table, lengths, bp), (ev0, ev1)
 
         def issue(idx: int):
@@ -285,6 +291,7 @@ class SidaEngine:
                     self.ffn_events.append((e_a, e_b, x.shape[0], len(required[layer])))
             logits = model.pool_classify(x, lay)
         ev1.record(cs)
+        DeviceTableRing.release(table, cs)
         return logits, self._record(table, lengths, bp), (ev0, ev1)
 
     def _record(self, table, lengths, bp: _BatchPlan) -> dict:
@@ -302,13 +309,16 @@ class SidaEngine:
             "utilization": util,
         }
 
-    def check_errors(self, tables=()) -> None:
+    def check_errors(self, tables=(), extra_flags=()) -> None:
         """Raise ContractError if a kernel flagged a contract violation since
-        the last check (synchronises; call where the host already waits)."""
+        the last check (synchronises; call where the host already waits):
+        the FFN / out-projection flags, the ring slots' sticky permute flags,
+        and those of ``tables`` built outside a ring."""
         flags = [(FFN_SLOT_MSG, self.store.err_flag), (OUTPROJ_MSG, self.model._err)]
+        flags += [(PERMUTE_MSG, f) for f in list(self.ring.error_flags()) + list(extra_flags)]
         for t in tables:
             dt = getattr(t, "_dev", None)
-            if dt is not None:
+            if dt is not None and getattr(t, "_slot", None) is None:
                 flags.append((PERMUTE_MSG, dt.err))
         check_device_flags(flags)
 

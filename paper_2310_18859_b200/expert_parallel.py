@@ -37,17 +37,14 @@ from . import _lib
 from .errors import ContractError, UnservableError
 from .moe import BatchLayout, MoEModel
 from .offload import (
-    FFN_SLOT_MSG,
-    OUTPROJ_MSG,
-    PERMUTE_MSG,
     ExpertStore,
     MemoryBudget,
     ResidencyState,
     apply_group_inplace,
-    check_device_flags,
     plan_placement,
     plan_placement_spread,
 )
+from .predictor import DeviceTableRing
 
 
 # ----------------------------------------------------------------------- host math
@@ -437,13 +434,8 @@ class ExpertParallelEngine:
         table._ep_counts = self._gather_counts(table._dev)
         return table
 
-    def check_errors(self, tables=()) -> None:
-        flags = [(FFN_SLOT_MSG, self.store.err_flag), (OUTPROJ_MSG, self.model._err)]
-        for t in tables:
-            dt = getattr(t, "_dev", None)
-            if dt is not None:
-                flags.append((PERMUTE_MSG, dt.err))
-        check_device_flags(flags)
+    def check_errors(self, tables=(), extra_flags=()) -> None:
+        self.base.check_errors(tables, extra_flags)
 
     def _gather_counts(self, dt):
         """(G, L, K) histograms of every rank's batch: one all-gather per
@@ -492,6 +484,7 @@ class ExpertParallelEngine:
         else:
             logits = self._forward_nccl(dt, counts, issuer, lengths, tokens_dev)
         ev1.record(cs)
+        DeviceTableRing.release(table, cs)
         resident_req = [k for k in local.required_experts() if k in self.state.resident]
         util = (sum(self.state.resident[k] for k in resident_req) / self.state.used_bytes
                 if self.state.used_bytes else 1.0)

@@ -505,10 +505,8 @@ class ExpertStore:
         (default ``layer``; 0 for the single-layer tables of router mode)."""
         st = stream or torch.cuda.current_stream(model.device)
         tl = layer if table_layer is None else table_layer
-        table_hist = dev_table.hist
-        dev_table.ready.synchronize()
         st.wait_event(dev_table.ready)
-        need = [int(e) for e in np.nonzero(table_hist[tl].cpu().numpy())[0]]
+        need = [int(e) for e in np.nonzero(dev_table.hist_host()[tl])[0]]
         if getattr(self, "cycle_layers", False):
             for key in [k for k in self.slot_of if k[0] != layer]:
                 self.free_slot(key)  # reuse waits on the slot's reader event

@@ -12,6 +12,7 @@ The resulting `ExpertHashTable` is device-resident; its numpy views
 from __future__ import annotations
 
 import json
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -133,6 +134,126 @@ class PredictorNet:
         return tab, vocab, tmax
 
 
+def _fresh(device):
+    """Allocator of per-table buffers from the caching allocator."""
+    def new(name, shape, dtype):
+        return torch.empty(shape, dtype=dtype, device=device)
+    return new
+
+
+class TableSlot:
+    """Long-lived device buffers one hash table is built in (one slot of a
+    `DeviceTableRing`); grows to the largest batch seen. ``consumed`` is the
+    event after which the slot's previous table is no longer read."""
+
+    def __init__(self, device):
+        self.device = device
+        self.bufs: dict = {}
+        self.consumed = None
+        self.busy = False
+        self.table = None  # weakref to the table built in the slot
+        # sticky permute contract flag of every table built in this slot
+        self.err = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def get(self, name, shape, dtype):
+        n = int(np.prod(shape))
+        buf = self.bufs.get(name)
+        if buf is None or buf.numel() < n or buf.dtype != dtype:
+            buf = torch.empty(max(n, 1), dtype=dtype, device=self.device)
+            self.bufs[name] = buf
+        return buf[:n].view(shape)
+
+
+class DeviceTableRing:
+    """The device-resident form of the hash-table queue (ref pipeline.py:53-84
+    holds host tables in a bounded FIFO): ``capacity`` table slots of device
+    buffers (`TableSlot`), written by the hash stream and read by the compute
+    stream. Back-pressure is device-side: before a slot is rewritten the hash
+    stream waits on the event recorded after the forward that read its
+    previous table (`release`, done by the engines' forward), so no host
+    thread, lock or queue object sits between hashing and inference. Tables
+    are produced in strictly increasing batch_id order and a slot whose table
+    was not consumed yet is never overwritten (ContractError), like
+    HashTableQueue.put / get."""
+
+    def __init__(self, capacity: int, device, strict: bool = True):
+        if capacity < 1:
+            raise ContractError("queue capacity must be >= 1")
+        self.capacity = capacity
+        self.slots = [TableSlot(device) for _ in range(capacity)]
+        self.n = 0
+        self._last_id: int | None = None
+        # strict: the queue contract (ordered ids, never overwrite an unread
+        # table). Non-strict (an engine's own ring): a full ring or an
+        # out-of-order id builds the table in fresh allocations instead.
+        self.strict = strict
+
+    def produce(self, predictor, model, lengths, eval_top_k: int, stream, batch_id: int,
+                tokens_dev=None, batch=None, host_ids: bool = False):
+        """Hash + permute one batch into the next slot on ``stream``: device
+        tokens (``tokens_dev``) or a host ``batch`` (tokens uploaded into the
+        slot). ``host_ids`` also starts an async copy of ids / alphas to pinned
+        memory (read after the slot is reused, e.g. for the hit rate)."""
+        if eval_top_k < 1 or eval_top_k > predictor.num_experts:
+            raise ContractError(f"k={eval_top_k} out of range for width-{predictor.num_experts} rows")
+        slot = self.slots[self.n % self.capacity]
+        in_order = self._last_id is None or batch_id > self._last_id
+        if not self.strict and (slot.busy or not in_order):
+            with torch.cuda.stream(stream):
+                if tokens_dev is None:
+                    toks = model.validate_tokens(batch)
+                    tokens_dev = torch.from_numpy(toks).pin_memory().to(model.device,
+                                                                        non_blocking=True)
+                return hash_device(predictor, model, tokens_dev, list(lengths), eval_top_k,
+                                   batch_id, stream)
+        if not in_order:
+            raise ContractError("hash tables must be enqueued in batch_id order")
+        if slot.busy:
+            raise ContractError("hash-table ring full: forward the oldest table first")
+        self._last_id = batch_id
+        self.n += 1
+        with torch.cuda.stream(stream):
+            if slot.consumed is not None:
+                stream.wait_event(slot.consumed)
+            if tokens_dev is None:
+                toks = model.validate_tokens(batch)
+                tokens_dev = slot.get("tokens", (toks.size,), torch.int32)
+                tokens_dev.copy_(torch.from_numpy(toks).pin_memory(), non_blocking=True)
+            table = hash_device(predictor, model, tokens_dev, list(lengths), eval_top_k,
+                                batch_id, stream, slot=slot)
+            if host_ids:
+                dt = table._dev
+                ids = torch.empty(dt.ids.shape, dtype=dt.ids.dtype, pin_memory=True)
+                al = torch.empty(dt.alpha.shape, dtype=dt.alpha.dtype, pin_memory=True)
+                ids.copy_(dt.ids, non_blocking=True)
+                al.copy_(dt.alpha, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                table._host_async = (ids, al, ev)
+        prev = slot.table() if slot.table is not None else None
+        if prev is not None:
+            prev._stale = True  # its device arrays now hold this batch
+        slot.busy = True
+        slot.table = weakref.ref(table)
+        table._slot = slot
+        return table
+
+    @staticmethod
+    def release(table, stream) -> None:
+        """Mark the table's slot reusable once ``stream`` (the consumer) has
+        passed this point (no-op for tables outside a ring)."""
+        slot = getattr(table, "_slot", None)
+        if slot is None:
+            return
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        slot.consumed = ev
+        slot.busy = False
+
+    def error_flags(self):
+        return [s.err for s in self.slots]
+
+
 class DeviceTable:
     """Device half of an ExpertHashTable: ids/alphas plus the per-layer
     permutation (hist, off, perm, inv, alpha_perm) and the event after which
@@ -150,18 +271,21 @@ class DeviceTable:
         self.err = None             # int32 (1,): set by the permute on an out-of-range id
         self.ready = torch.cuda.Event()
 
-    def permute(self, num_experts: int, stream) -> None:
+    def permute(self, num_experts: int, stream, slot: "TableSlot | None" = None) -> None:
         h = _lib.lib()
         L, rows = self.num_layers, self.n_tokens * self.k
         dev = self.ids.device
-        self.hist = torch.empty((L, num_experts), dtype=torch.int32, device=dev)
-        self.off = torch.empty((L, num_experts + 1), dtype=torch.int32, device=dev)
-        self.perm = torch.empty((L, rows), dtype=torch.int32, device=dev)
-        self.inv = torch.empty((L, rows), dtype=torch.int32, device=dev)
-        self.alpha_perm = torch.empty((L, rows), dtype=torch.float32, device=dev)
+        new = slot.get if slot is not None else _fresh(dev)
+        self.hist = new("hist", (L, num_experts), torch.int32)
+        self.off = new("off", (L, num_experts + 1), torch.int32)
+        self.perm = new("perm", (L, rows), torch.int32)
+        self.inv = new("inv", (L, rows), torch.int32)
+        self.alpha_perm = new("alpha_perm", (L, rows), torch.float32)
         ws_bytes = h.sida_permute_workspace_bytes(L, rows, num_experts)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-        self.err = torch.empty(1, dtype=torch.int32, device=dev)  # zeroed by the call
+        ws = new("perm_ws", (ws_bytes,), torch.uint8)
+        # sticky contract flag (never cleared by the kernel): the slot's own,
+        # or a fresh zeroed one per table
+        self.err = slot.err if slot is not None else torch.zeros(1, dtype=torch.int32, device=dev)
         _lib.check(h.sida_permute_hist(
             self.ids.data_ptr(), L, rows, num_experts, self.alpha_f32.data_ptr(),
             self.hist.data_ptr(), self.off.data_ptr(), self.perm.data_ptr(), self.inv.data_ptr(),
@@ -180,6 +304,14 @@ class DeviceTable:
 
     def layer(self, layer: int):
         return self.off[layer], self.perm[layer], self.alpha_perm[layer]
+
+    def hist_host(self) -> np.ndarray:
+        """(L, K) expert histograms on the host: one D2H per table (waits for
+        the permute), cached -- the planner and the per-layer paths read it."""
+        if getattr(self, "_hist_host", None) is None:
+            self.ready.synchronize()
+            self._hist_host = self.hist.cpu().numpy()
+        return self._hist_host
 
     def tokens_for(self, model: MoEModel, batch: SequenceBatch, stream=None) -> torch.Tensor:
         """The batch's int32 tokens on the device. A table built on the host
@@ -212,16 +344,34 @@ class ExpertHashTable:
             raise ContractError("hash table needs ids or a device table")
 
     # -- numpy view (boundary iv) ----------------------------------------------------
+    def _check_live(self) -> None:
+        if getattr(self, "_stale", False):
+            raise ContractError(f"hash table {self.batch_id}: its device-ring slot was reused; "
+                                "read ids/alphas before the ring wraps (or build it outside a ring)")
+
+    def _from_async(self) -> bool:
+        pend = getattr(self, "_host_async", None)
+        if pend is None:
+            return False
+        ids, al, ev = pend
+        ev.synchronize()
+        self._ids = ids.numpy().astype(np.int64)
+        self._alphas = al.numpy().copy()
+        self._host_async = None
+        return True
+
     @property
     def ids(self) -> np.ndarray:
-        if self._ids is None:
+        if self._ids is None and not self._from_async():
+            self._check_live()
             self._dev.ready.synchronize()
             self._ids = self._dev.ids.cpu().numpy().astype(np.int64)
         return self._ids
 
     @property
     def alphas(self) -> np.ndarray:
-        if self._alphas is None:
+        if self._alphas is None and not self._from_async():
+            self._check_live()
             self._dev.ready.synchronize()
             self._alphas = self._dev.alpha.cpu().numpy()
         return self._alphas
@@ -247,8 +397,7 @@ class ExpertHashTable:
         """(L, K) per-layer expert counts (device hist when available)."""
         if self._hist is None:
             if self._dev is not None and self._dev.hist is not None:
-                self._dev.ready.synchronize()
-                self._hist = self._dev.hist.cpu().numpy()
+                self._hist = self._dev.hist_host()
             else:
                 K = int(self.ids.max()) + 1
                 self._hist = np.stack([np.bincount(self.ids[l].ravel(), minlength=K)
@@ -343,9 +492,12 @@ def build_hash_table(predictor: PredictorNet, batch: SequenceBatch, eval_top_k: 
 
 
 def hash_device(predictor: PredictorNet, model: MoEModel | None, tokens, lengths, eval_top_k: int,
-                batch_id: int, stream, emb=None, device=None) -> ExpertHashTable:
+                batch_id: int, stream, emb=None, device=None,
+                slot: TableSlot | None = None) -> ExpertHashTable:
     """Hash + permute for tokens already resident in HBM (int32 ``tokens`` on
-    the device, or float64 embeddings ``emb``), enqueued on ``stream``."""
+    the device, or float64 embeddings ``emb``), enqueued on ``stream``;
+    ``slot`` (a `DeviceTableRing` slot) holds the outputs instead of fresh
+    allocations."""
     h = _lib.lib()
     st = stream
     device = device or (model.device if model is not None else emb.device)
@@ -356,13 +508,14 @@ def hash_device(predictor: PredictorNet, model: MoEModel | None, tokens, lengths
     np.cumsum(lengths, out=off[1:])
     use_tables = model is not None
     with torch.cuda.stream(st):
+        new = slot.get if slot is not None else _fresh(device)
         seq_off = torch.from_numpy(off).pin_memory().to(device, non_blocking=True)
-        ids = torch.empty((L, n_tok, eval_top_k), dtype=torch.int32, device=device)
-        alpha = torch.empty((L, n_tok, eval_top_k), dtype=torch.float64, device=device)
-        alpha_f32 = torch.empty((L, n_tok, eval_top_k), dtype=torch.float32, device=device)
+        ids = new("ids", (L, n_tok, eval_top_k), torch.int32)
+        alpha = new("alpha", (L, n_tok, eval_top_k), torch.float64)
+        alpha_f32 = new("alpha_f32", (L, n_tok, eval_top_k), torch.float32)
         ws_bytes = h.sida_hash_workspace_bytes(n_tok, n_seq, max_len, predictor.d_model,
                                                c.compress_dim, c.lstm_hidden, L, K)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+        ws = new("hash_ws", (ws_bytes,), torch.uint8)
         params = predictor.packed(device)
         tables, vocab, tmax = predictor.tables(model, device, st)
         _lib.check(h.sida_hash_forward(
@@ -371,7 +524,7 @@ def hash_device(predictor: PredictorNet, model: MoEModel | None, tokens, lengths
             c.lstm_hidden, L, K, eval_top_k, ids.data_ptr(), alpha.data_ptr(),
             alpha_f32.data_ptr(), ws.data_ptr(), ws_bytes, st.cuda_stream))
         dt = DeviceTable(ids, alpha, alpha_f32, n_tok, eval_top_k, tokens=tokens)
-        dt.permute(K, st)
+        dt.permute(K, st, slot=slot)
         ws.record_stream(st)
     return ExpertHashTable(batch_id, lengths, device_table=dt)
 

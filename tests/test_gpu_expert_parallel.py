@@ -62,7 +62,7 @@ def _worker(rank, world, port, q, peer=False, cfg=None, slots=None, vs_oracle=Fa
                                   transport=transport)
         for bid in range(2 if (peer or slots) else 1):  # later batches reuse buffers / slots
             table = ep.hash_tokens(bid, toks, lengths)
-            got = ep.forward(table, lengths, tokens_dev=toks)
+            got, rec, _ = ep.forward(table, lengths, tokens_dev=toks)
         torch.cuda.synchronize()
         ep.base.check_errors([table])
         got = got.cpu().numpy()

@@ -109,7 +109,11 @@ def test_c1_every_layer_in_isolation(cuda_device, c1):
         xa64 = xa.cpu().numpy().astype(np.float64)
         moe_ref = omoe.moe_apply_grouped(params, layer, xa64, ids[layer], alphas[layer])
         close_rms(x.cpu().numpy(), moe_ref, 2e-2)
-        close_rms(x.cpu().numpy() - xa64, moe_ref - xa64, 2e-2)  # the FFN term alone
+        # the FFN term alone (its own scale): bf16 input rows, bf16 weights and
+        # a bf16 hidden layer give a relative rms error of a few 1e-3; bar 1e-2
+        f_gpu, f_ref = x.cpu().numpy() - xa64, moe_ref - xa64
+        rel = float(np.sqrt(np.mean((f_gpu - f_ref) ** 2) / np.mean(f_ref ** 2)))
+        assert rel <= 1e-2, (layer, rel)
     assert store.err_flag.item() == 0
 
 
