@@ -171,6 +171,7 @@ class SidaEngine:
         self.store.residency_state = self.state
         self.peak = 0
         self.ffn_events: list | None = None  # set to a list to time every layer's FFN
+        self.trace: list | None = None       # set to a list: (name, stream, ev0, ev1) timeline
         self.mix_events: list = []           # (filled alongside ffn_events) attention_mix
         # hash-driven cross-batch prefetch: during the last `lookahead` layers
         # of batch j, the (already hashed) batch j+1 is planned and its leading
@@ -192,13 +193,25 @@ class SidaEngine:
         self.ring = DeviceTableRing(3, dev, strict=False)
 
     # -- hash stream ------------------------------------------------------------------
+    def _mark(self, stream):
+        if self.trace is None:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        return ev
+
     def hash_tokens(self, batch_id: int, tokens_dev: torch.Tensor, lengths) -> ExpertHashTable:
         """Hash + permute for device-resident tokens on the hash stream, into
         the next slot of the engine's device table ring (forward releases it;
         with three tables outstanding, or ids out of order, the table is built
         in fresh allocations instead)."""
-        return self.ring.produce(self.predictor, self.model, lengths, self.eval_top_k,
-                                 self.hash_stream, batch_id, tokens_dev=tokens_dev)
+        t0 = self._mark(self.hash_stream)
+        table = self.ring.produce(self.predictor, self.model, lengths, self.eval_top_k,
+                                  self.hash_stream, batch_id, tokens_dev=tokens_dev)
+        if t0 is not None:
+            self.trace.append((f"hash+permute b{batch_id}", "hash", t0,
+                               self._mark(self.hash_stream)))
+        return table
 
     # -- compute stream ---------------------------------------------------------------
     def forward(self, table: ExpertHashTable, lengths, tokens_dev: torch.Tensor | None = None,
@@ -271,8 +284,10 @@ class SidaEngine:
                     x_perm = torch.empty((lay.n_tokens * dt.k, model.config.d_model),
                                          dtype=torch.bfloat16, device=x.device)
                     scatter = (dt.inv[layer], dt.k, x_perm)
+                t_a = self._mark(cs)
                 x = model.attention_mix(layer, x, lay, xb=xb, scatter=scatter)
                 xp = scatter[2] if scatter is not None else None
+                t_f = self._mark(cs)
                 if self.ffn_events is not None:
                     e_a = torch.cuda.Event(enable_timing=True)
                     e_a.record(cs)
@@ -289,6 +304,10 @@ class SidaEngine:
                     e_b = torch.cuda.Event(enable_timing=True)
                     e_b.record(cs)
                     self.ffn_events.append((e_a, e_b, x.shape[0], len(required[layer])))
+                if t_a is not None:
+                    t_e = self._mark(cs)
+                    self.trace.append((f"attention L{layer}", "compute", t_a, t_f))
+                    self.trace.append((f"ffn L{layer} (waits own copies)", "compute", t_f, t_e))
             logits = model.pool_classify(x, lay)
         ev1.record(cs)
         DeviceTableRing.release(table, cs)

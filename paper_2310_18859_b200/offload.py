@@ -420,6 +420,7 @@ class ExpertStore:
         self.bytes_loaded = 0
         self.peak_slots = 0
         self.rows = RowUploader(dev, model.config.num_experts)
+        self.trace: list | None = None  # (name, stream, start, end) events per copy when set
 
     @classmethod
     def full(cls, model) -> "ExpertStore":
@@ -486,8 +487,15 @@ class ExpertStore:
             if ev is not None:
                 cs.wait_event(ev)
             src = self.model.expert_image(layer, e)
+            if self.trace is not None:
+                t0 = torch.cuda.Event(enable_timing=True)
+                t0.record(cs)
             _lib.check(h.sida_expert_copy(self.base_ptr + slot * self.slot_stride, src.data_ptr(),
                                           self.slot_stride, cs.cuda_stream, None, None))
+            if self.trace is not None:
+                t1 = torch.cuda.Event(enable_timing=True)
+                t1.record(cs)
+                self.trace.append((f"copy L{layer} E{e}", "copy", t0, t1))
             self.n_loads += 1
             self.bytes_loaded += self.slot_stride
         done = torch.cuda.Event()
