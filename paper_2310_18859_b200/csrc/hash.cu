@@ -692,6 +692,7 @@ __host__ __device__ constexpr int block_smem() {
 struct BlockArgs {
   AttnArgs a;
   const double* hwp;  // heads packed (H, L*K): hwp[i][l*K + e] = head_w[l][i][e]
+  double* r_out;      // non-null: write R = ctx + h2 (N, H) here and skip the heads
 };
 
 __device__ __forceinline__ void dmma_884(double& d0, double& d1, double a, double b) {
@@ -851,10 +852,15 @@ attn_block_kernel(const BlockArgs ba) {
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
         const int c = tx + 16 * m;
-        if (r < rows && c < H) sQ[r * kQP + c] = acc[i][m] + a.h2[(size_t)(base + r0 + r) * H + c];
+        if (r < rows && c < H) {
+          const double v = acc[i][m] + a.h2[(size_t)(base + r0 + r) * H + c];
+          if (ba.r_out) ba.r_out[(size_t)(base + r0 + r) * H + c] = v;
+          else sQ[r * kQP + c] = v;
+        }
       }
     }
   }
+  if (ba.r_out) return;  // heads in heads_dmma_kernel
   __syncthreads();
 
   // ---- heads. Logit columns in chunks of <= kBT: whole layers when K <= kBT
@@ -1029,6 +1035,128 @@ attn_block_kernel(const BlockArgs ba) {
         }
       }
       __syncthreads();
+    }
+  }
+}
+
+// ---- heads for 8 <= K <= 128, K % 8 == 0 (ref predictor.py:253-259, numkit.py:28-33,87-93):
+// logits Z = R hw + hb for all L layers, softmax over each layer's K experts, top-k with
+// ties to the lower index. CTA = 8 warps x 8 tokens; per 128-column chunk of the (H, L*K)
+// packed head weights (whole layers: 128 / K layers per chunk) the chunk is staged in
+// smem once for the CTA and every warp computes its 8 x 128 logits on the FP64 tensor
+// cores (m8n8k4: lane (g, t) holds row g, columns 8j + 2t, 8j + 2t + 1), so each row's K
+// logits of a layer sit in the four lanes of its quad and every reduction is two
+// shuffles. The softmax divides only the picked probabilities: the top-k runs on
+// e = exp(z - max) (division by the positive sum is monotone), and an index below the
+// pick whose e is within 1e-15 relative is re-checked by its exact quotient, so a tie
+// the division creates still resolves to the lower index as in the reference.
+constexpr int kHTok = 64;  // tokens per heads CTA
+constexpr int heads_smem_bytes() { return (48 * kWP + 128 + kHTok * kQP) * 8; }
+
+__global__ void __launch_bounds__(256, 2)
+heads_dmma_kernel(const double* __restrict__ R, int n_tokens, int H, int L, int K,
+                  const double* __restrict__ hwp, const double* __restrict__ hb, int topk,
+                  int32_t* __restrict__ ids, double* __restrict__ alpha,
+                  float* __restrict__ alpha_f32) {
+  extern __shared__ double smem_d[];
+  double* sW = smem_d;             // KP x kWP chunk of the packed head weights
+  double* sB = sW + 48 * kWP;      // 128 biases of the chunk
+  double* sR = sB + 128;           // kHTok x kQP residual rows
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int KP = (H + 3) & ~3;
+  const int n0 = blockIdx.x * kHTok;
+  const int rows = min(kHTok, n_tokens - n0);
+  for (int i = tid; i < kHTok * KP; i += 256) {
+    const int r = i / KP, c = i - r * KP;
+    sR[r * kQP + c] = (r < rows && c < H) ? R[(size_t)(n0 + r) * H + c] : 0.0;
+  }
+  const int LK = L * K;
+  const int lpc = 128 / K, segs = K / 8;
+  const int row = warp * 8 + g;
+  const bool valid = row < rows;
+  const int n = n0 + row;
+  for (int l0 = 0; l0 < L; l0 += lpc) {
+    const int nl = min(lpc, L - l0), ncol = nl * K;
+    __syncthreads();  // the previous chunk's readers are done
+    for (int i = tid; i < KP * 128; i += 256) {
+      const int c = i >> 7, j = i & 127;
+      sW[c * kWP + j] = (j < ncol && c < H) ? __ldg(hwp + (size_t)c * LK + (size_t)l0 * K + j) : 0.0;
+    }
+    if (tid < 128) sB[tid] = tid < ncol ? __ldg(hb + (size_t)l0 * K + tid) : 0.0;
+    __syncthreads();
+    double acc[16][2];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = 0.0;
+    for (int k0 = 0; k0 < KP; k0 += 4) {
+      const double a = sR[(warp * 8 + g) * kQP + k0 + t];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) dmma_884(acc[j][0], acc[j][1], a, sW[(k0 + t) * kWP + j * 8 + g]);
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      acc[j][0] += sB[j * 8 + 2 * t];
+      acc[j][1] += sB[j * 8 + 2 * t + 1];
+    }
+    for (int li = 0; li < nl; ++li) {
+      const int j0 = li * segs, j1 = j0 + segs;
+      double zmax = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j >= j0 && j < j1) zmax = fmax(zmax, fmax(acc[j][0], acc[j][1]));
+      zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, 1));
+      zmax = fmax(zmax, __shfl_xor_sync(0xffffffffu, zmax, 2));
+      // e = exp(z - max) in place (only this layer's columns are touched)
+      double ssum = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j >= j0 && j < j1) {
+          acc[j][0] = exp(acc[j][0] - zmax);
+          acc[j][1] = exp(acc[j][1] - zmax);
+          ssum += acc[j][0] + acc[j][1];
+        }
+      }
+      ssum += __shfl_xor_sync(0xffffffffu, ssum, 1);
+      ssum += __shfl_xor_sync(0xffffffffu, ssum, 2);
+      const int l = l0 + li;
+      for (int rk = 0; rk < topk; ++rk) {
+        double best = -1.0;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)  // local ids ascend with (j, q): first max = lowest id
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (j >= j0 && j < j1 && acc[j][q] > best) {
+              best = acc[j][q];
+              bi = (j - j0) * 8 + 2 * t + q;
+            }
+        seg_argmax(best, bi, 4);
+        const double p = best / ssum;
+        // a lower id whose e is within rounding of best can divide to the same p
+        const double near = best * (1.0 - 1e-15);
+        int cand = bi;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int id = (j - j0) * 8 + 2 * t + q;
+            if (j >= j0 && j < j1 && acc[j][q] >= near && id < cand && acc[j][q] / ssum == p)
+              cand = id;
+          }
+        cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, 1));
+        cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, 2));
+        if (valid && t == 0) {
+          const size_t at = ((size_t)l * n_tokens + n) * topk + rk;
+          ids[at] = cand;
+          alpha[at] = p;
+          if (alpha_f32) alpha_f32[at] = (float)p;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (j >= j0 && j < j1 && (j - j0) * 8 + 2 * t + q == cand) acc[j][q] = -1.0;
+      }
     }
   }
 }
@@ -1258,6 +1386,16 @@ rows_dmma_kernel(const double* __restrict__ A, int n_rows, int Kd, const double*
   }
 }
 
+// SIDA_HASH_HEADS_SPLIT=0: heads inside attn_block_kernel (A/B switch)
+static int heads_split() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SIDA_HASH_HEADS_SPLIT");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+
 // SIDA_HASH_DMMA=0: the CUDA-core fp64 kernel below (A/B switch)
 static int use_dmma() {
   static int v = -1;
@@ -1372,7 +1510,10 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
   a.prof = nullptr;
   const int n_blocks_ub = ceil_div(n_tokens, rpb) + n_seq;
   if (blocked) {
-    BlockArgs ba{a, tb.hwp};
+    // K a multiple of 8 up to 128: the heads run in their own kernel (heads_dmma_kernel,
+    // 16 warps per SM) on R = ctx + h2 written to the dead xw buffer
+    const bool split = K % 8 == 0 && K >= 8 && K <= 128 && H <= 48 && heads_split();
+    BlockArgs ba{a, tb.hwp, split ? xw : nullptr};
     if (max_len <= kBT) {
       constexpr int sm = block_smem<64, 128>();
       static bool cfg64 = false;
@@ -1393,6 +1534,19 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
       attn_block_kernel<32, kMaxLen><<<n_blocks_ub, 256, sm, s>>>(ba);
     }
     SIDA_LAUNCH_CHECK();
+    if (split) {
+      constexpr int hs = heads_smem_bytes();
+      static bool cfgh = false;
+      if (!cfgh) {
+        SIDA_CUDA(cudaFuncSetAttribute(heads_dmma_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, hs));
+        cfgh = true;
+      }
+      heads_dmma_kernel<<<ceil_div(n_tokens, kHTok), 256, hs, s>>>(xw, n_tokens, H, L, K, tb.hwp,
+                                                                  w.hb, topk, ids, alpha,
+                                                                  alpha_f32);
+      SIDA_LAUNCH_CHECK();
+    }
     return SIDA_OK;
   }
   if (getenv("SIDA_HASH_PROF")) {

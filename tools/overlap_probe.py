@@ -20,11 +20,12 @@ p = argparse.ArgumentParser()
 p.add_argument("--steps", type=int, default=10)
 p.add_argument("--batch", type=int, default=256)
 p.add_argument("--seq", type=int, default=128)
+p.add_argument("--experts", type=int, default=8)
 a = p.parse_args()
-cfg = MoEConfig(vocab_size=32128, d_model=768, num_layers=12, num_experts=8, expert_hidden=3072,
+cfg = MoEConfig(vocab_size=32128, d_model=768, num_layers=12, num_experts=a.experts, expert_hidden=3072,
                 max_seq_len=512)
 model = MoEModel.synthetic(cfg, 0)
-pred = PredictorNet(PredictorConfig(), 768, 12, 8, Rng(1))
+pred = PredictorNet(PredictorConfig(), 768, 12, a.experts, Rng(1))
 eng = SidaEngine(model, pred, MemoryBudget(model.total_expert_bytes()))
 n = a.batch * a.seq
 lengths = [a.seq] * a.batch
