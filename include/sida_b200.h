@@ -170,7 +170,13 @@ int sida_debug_gemm_prof(unsigned long long* out);
  * for both (swap-AB: 256 features x 16..256 token rows in steps of 16),
  * 2 token-M GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2,
  * 4 both GEMMs fused per <= 128-row token tile with the bf16 hidden kept in
- * shared memory (d % 256 == 0, d <= 768; otherwise as 1).
+ * shared memory (d % 256 == 0, d <= 768; otherwise as 1), 5 both GEMMs in
+ * ONE persistent launch with the hidden rows handed from GEMM1 to GEMM2
+ * through L2 (token-N tiles of up to 320 rows, d % 256 == 0, h % 1024 == 0;
+ * auto mode runs it for such shapes only with SIDA_XFFN=1).
+ * The one-launch path keeps a small per-(device, stream) state buffer
+ * (epoch-tagged m-tile flags) allocated on its first call, which therefore
+ * must not happen inside a CUDA-graph capture.
  * Process-wide; the initial value comes from SIDA_FFN_SWAP.
  * sida_get_ffn_tiles returns the current mode. */
 int sida_set_ffn_tiles(int mode);

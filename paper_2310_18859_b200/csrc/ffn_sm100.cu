@@ -1532,7 +1532,7 @@ static bool choose_fx(int n_rows, int listed, int d, int h) {
 }
 
 extern "C" int sida_set_ffn_tiles(int mode) {
-  SIDA_REQUIRE(mode >= -1 && mode <= 4, SIDA_ERR_CONTRACT, "ffn tile mode %d not in -1..4", mode);
+  SIDA_REQUIRE(mode >= -1 && mode <= 5, SIDA_ERR_CONTRACT, "ffn tile mode %d not in -1..5", mode);
   tn_init();
   g_tn_mode = mode;
   return SIDA_OK;
@@ -1541,6 +1541,30 @@ extern "C" int sida_set_ffn_tiles(int mode) {
 extern "C" int sida_get_ffn_tiles(void) {
   tn_init();
   return g_tn_mode;
+}
+
+// One persistent launch for both expert GEMMs (expert_ffn.cu): mode 5, or
+// auto mode with SIDA_XFFN=1. Measured slower than the two token-M launches
+// (tools/ffn_probe.py, one B200: base-8 0.389 vs 0.293 ms, base-128 0.464 vs
+// 0.442 ms per layer), so auto keeps the two launches.
+extern "C" int sida_expert_ffn_applicable(int d, int h);
+extern "C" int sida_expert_ffn_launch(const uint16_t* x_perm, int n_rows, int d, int h,
+                                      const int32_t* off, int num_experts,
+                                      const int32_t* expert_slot, const int32_t* expert_list,
+                                      int n_list, const void* arena, size_t slot_stride,
+                                      int n_slots, const int32_t* row_map, const float* alpha,
+                                      const float* resid, float* out, uint16_t* out_bf16,
+                                      uint16_t* hidden, int32_t* err_flag, void* stream);
+
+static bool choose_xffn(int d, int h) {
+  tn_init();
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("SIDA_XFFN");
+    env = e ? atoi(e) : 0;
+  }
+  if (!sida_expert_ffn_applicable(d, h)) return false;
+  return g_tn_mode == 5 || (g_tn_mode == -1 && env);
 }
 
 extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h,
@@ -1567,6 +1591,10 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   const uint8_t* ar = static_cast<const uint8_t*>(arena);
   const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
 
+  if (choose_xffn(d, h))
+    return sida_expert_ffn_launch(x_perm, n_rows, d, h, off, num_experts, expert_slot,
+                                  expert_list, n_list, arena, slot_stride, n_slots, row_map,
+                                  alpha, resid, out, out_bf16, hidden, err_flag, stream);
   if (choose_fx(n_rows, listed, d, h)) {
     sm100::FxParams f{};
     f.n_rows = n_rows; f.d = d; f.h = h;

@@ -191,7 +191,7 @@ def ffn_tiles():
     _l.check(h.sida_set_ffn_tiles(prev))
 
 
-@pytest.mark.parametrize("tiles", [-1, 0, 1, 2, 3, 4])
+@pytest.mark.parametrize("tiles", [-1, 0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("d,hdim,K,N,k", [
     (64, 128, 4, 300, 1), (256, 1024, 8, 1024, 1), (768, 3072, 8, 2048, 1),
     (128, 256, 8, 700, 2), (768, 3072, 4, 257, 3), (256, 1024, 32, 1500, 1),
@@ -199,7 +199,9 @@ def ffn_tiles():
 def test_grouped_ffn_bf16_vs_oracle(cuda_device, ffn_tiles, tiles, d, hdim, K, N, k):
     """tiles: -1 auto, 0 token-M (128/256-row token tiles), 1 token-N
     (swap-AB: 256 features x 16..256 tokens), 2/3 mixed per GEMM, 4 fused
-    per token tile (hidden on chip); token-N needs d, h % 256."""
+    per token tile (hidden on chip), 5 both GEMMs in one launch with the hidden
+    rows passed through L2 (d % 256, h % 1024);
+    token-N needs d, h % 256."""
     from paper_2310_18859_b200.offload import ExpertStore
     from paper_2310_18859_b200.predictor import ExpertHashTable
 
@@ -276,6 +278,40 @@ def test_ffn_rejects_nonresident_expert(cuda_device):
     x = torch.zeros((10, 64), device="cuda")
     torch.cuda.current_stream().wait_event(dt.ready)
     run_waves(model, [wave], x, dt, store, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert store.err_flag.item() == 1
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_one_launch_ffn_waves_and_nonresident_expert(cuda_device, ffn_tiles, k):
+    """The one-launch expert FFN (mode 5) over expert-list waves equals one
+    full launch bit for bit; an expert with rows but no slot raises the error
+    flag and the launch completes (its GEMM2 items never wait on flags)."""
+    from paper_2310_18859_b200.offload import ExpertStore, Wave, run_waves
+    from paper_2310_18859_b200.predictor import ExpertHashTable
+
+    ffn_tiles(5)
+    d, hdim, K, N = 256, 1024, 8, 3000
+    shape, params, model = _moe_setup(d, hdim, K)
+    g = np.random.default_rng(11)
+    ids = _ids_for(N, k, K, g)
+    alphas = g.uniform(0.05, 1.0, size=ids.shape)
+    dt = ExpertHashTable(0, [N], ids, alphas).on_device(model)
+    x = torch.from_numpy(g.normal(0, 1.0, (N, d))).float().cuda()
+    store = ExpertStore.full(model)
+    st = torch.cuda.current_stream()
+    store.run_layer(model, 0, x, dt)  # loads every expert of the layer into its slot
+    torch.cuda.synchronize()
+    full_row = store.slot_row(0, list(range(K)))
+    one = run_waves(model, [Wave(0, [], list(range(K)), full_row)], x, dt, store, st)
+    two = run_waves(model, [Wave(0, [], [0, 2, 4, 6], full_row), Wave(0, [], [1, 3, 5, 7], full_row)],
+                    x, dt, store, st)
+    torch.cuda.synchronize()
+    assert torch.equal(one, two)
+    assert store.err_flag.item() == 0
+    bad = full_row.copy()
+    bad[3] = -1
+    run_waves(model, [Wave(0, [], list(range(K)), bad)], x, dt, store, st)
     torch.cuda.synchronize()
     assert store.err_flag.item() == 1
 
@@ -544,7 +580,7 @@ def test_ffn_token_n_tiles_match_token_m_tiles(cuda_device, ffn_tiles, K, N, ske
     dt = ExpertHashTable(0, [N], ids, alphas).on_device(model)
     store = ExpertStore.full(model)
     outs = []
-    for mode in (0, 1, 2, 3, 4):
+    for mode in (0, 1, 2, 3, 4, 5):
         ffn_tiles(mode)
         ob = torch.empty((N, d), dtype=torch.bfloat16, device="cuda")
         outs.append((store.run_layer(model, 0, x, dt, out_bf16=ob), ob))

@@ -68,6 +68,21 @@ if os.environ.get("SIDA_GEMM_PROF"):
         tot = b[:, 3].mean()
         print(f"GEMM{gi + 1}: " + ", ".join(f"{n}={b[:, i].mean():.0f}" for i, n in enumerate(names))
               + f"  | mma waits epi {b[:, 1].mean() / tot:.1%} tma {b[:, 2].mean() / tot:.1%}")
+if os.environ.get("SIDA_XFFN_PROF"):
+    from paper_2310_18859_b200 import _lib
+    buf = np.zeros((148, 8), dtype=np.uint64)
+    _lib.check(_lib.load().sida_debug_xffn_prof(buf.ctypes.data_as(__import__("ctypes").c_void_p)))
+    b = buf.astype(np.float64)
+    lead = b[0::2]
+    tot = lead[:, 4].mean()
+    names = ["prod_wait_empty", "prod_wait_flag", "mma_wait_full", "mma_wait_chunk", "mma_total",
+             "epi_wait_tile", "epi_total", "prologue"]
+    print("xffn (leader CTAs, mean): " + ", ".join(f"{n}={lead[:, i].mean():.0f}"
+                                                  for i, n in enumerate(names)))
+    print(f"  mma waits: full {lead[:, 2].mean() / tot:.1%}, chunk {lead[:, 3].mean() / tot:.1%};"
+          f" producer waits empty {lead[:, 0].mean() / tot:.1%}, flags {lead[:, 1].mean() / tot:.1%};"
+          f" epilogue wait {lead[:, 5].mean() / tot:.1%}; mma_total spread "
+          f"{lead[:, 4].min():.0f}..{lead[:, 4].max():.0f}")
 if a.no_cublas:
     sys.exit(0)
 # cuBLAS reference on the same shapes (dense bmm, no gather/epilogue fusion)
