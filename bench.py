@@ -47,6 +47,10 @@ sys.path.insert(0, REPO)
 SWITCH = dict(vocab_size=32128, d_model=768, num_layers=12, expert_hidden=3072,
               max_seq_len=512, routing_k=1, num_classes=2)
 ZIPF_A = 1.1  # ref corpus.py CorpusSpec.zipf_a default
+# batches hashed ahead of the one being served: with 2, forward(j) plans on a
+# table whose hash ran during step j-2, so the host never blocks on the
+# low-priority hash stream and keeps the compute stream fed
+HASH_AHEAD = int(os.environ.get("SIDA_HASH_AHEAD", "2"))
 
 
 def parse():
@@ -307,14 +311,15 @@ def run_stream(engine, toks, lengths, steps, warmup):
     import torch
 
     cs = engine.compute_stream
-    tables = {0: engine.hash_tokens(0, toks[0], lengths)}
+    tables = {i: engine.hash_tokens(i, toks[i % len(toks)], lengths) for i in range(HASH_AHEAD)}
     timed = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for j in range(warmup + steps):
         if j == warmup:
             torch.cuda.synchronize()
             e0.record(cs)
-        tables[j + 1] = engine.hash_tokens(j + 1, toks[(j + 1) % len(toks)], lengths)
+        a = j + HASH_AHEAD
+        tables[a] = engine.hash_tokens(a, toks[a % len(toks)], lengths)
         t = tables.pop(j)
         engine.forward(t, lengths, tokens_dev=toks[j % len(toks)], next_table=tables[j + 1])
         if j >= warmup:
@@ -603,8 +608,8 @@ def run_ours(args):
         return v
 
     cs = engine.compute_stream
-    # ---- device-resident pipeline: hash(j+1) on the hash stream overlaps forward(j)
-    tables = {0: engine.hash_tokens(0, toks[0], lengths)}
+    # ---- device-resident pipeline: hash(j+2) on the hash stream overlaps forward(j)
+    tables = {i: engine.hash_tokens(i, toks[i], lengths) for i in range(HASH_AHEAD)}
     ev_start = torch.cuda.Event(enable_timing=True)
     ev_end = torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(local)
@@ -619,7 +624,8 @@ def run_ours(args):
             sampler.__enter__()
             ev_start.record(cs)
             t_wall0 = time.perf_counter()
-        tables[j + 1] = engine.hash_tokens(j + 1, toks[j + 1], lengths)
+        a = j + HASH_AHEAD
+        tables[a] = engine.hash_tokens(a, toks[a % len(toks)], lengths)
         engine.forward(tables.pop(j), lengths, tokens_dev=toks[j], next_table=tables[j + 1])
     ev_end.record(cs)
     torch.cuda.synchronize()

@@ -1076,7 +1076,11 @@ heads_dmma_kernel(const double* __restrict__ R, int n_tokens, int H, int L, int 
   const int row = warp * 8 + g;
   const bool valid = row < rows;
   const int n = n0 + row;
-  for (int l0 = 0; l0 < L; l0 += lpc) {
+  // blockIdx.y: this CTA's share of the 128-column chunks (short CTAs: the
+  // compute stream's persistent GEMM grids get their SMs back quickly)
+  const int n_chunks = ceil_div(L, lpc);
+  const int c_lo = blockIdx.y * n_chunks / gridDim.y, c_hi = (blockIdx.y + 1) * n_chunks / gridDim.y;
+  for (int l0 = c_lo * lpc; l0 < min(L, c_hi * lpc); l0 += lpc) {
     const int nl = min(lpc, L - l0), ncol = nl * K;
     __syncthreads();  // the previous chunk's readers are done
     for (int i = tid; i < KP * 128; i += 256) {
@@ -1542,7 +1546,16 @@ extern "C" int sida_hash_forward(const double* params, const double* tables, int
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, hs));
         cfgh = true;
       }
-      heads_dmma_kernel<<<ceil_div(n_tokens, kHTok), 256, hs, s>>>(xw, n_tokens, H, L, K, tb.hwp,
+      // split the 128-column chunks over blockIdx.y (SIDA_HEADS_SPLIT_Y, default: one
+      // chunk per CTA) so no heads CTA holds an SM for long
+      static int split_y = -1;
+      if (split_y < 0) {
+        const char* e = getenv("SIDA_HEADS_SPLIT_Y");
+        split_y = e ? atoi(e) : 0;
+      }
+      const int n_chunks = ceil_div(L, 128 / K);
+      const int gy = split_y > 0 ? std::min(split_y, n_chunks) : n_chunks;
+      heads_dmma_kernel<<<dim3(ceil_div(n_tokens, kHTok), gy), 256, hs, s>>>(xw, n_tokens, H, L, K, tb.hwp,
                                                                   w.hb, topk, ids, alpha,
                                                                   alpha_f32);
       SIDA_LAUNCH_CHECK();

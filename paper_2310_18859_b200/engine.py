@@ -157,11 +157,15 @@ class SidaEngine:
         self.eval_top_k = eval_top_k
         self.prefetch = prefetch
         dev = model.device
-        # compute at the highest stream priority: the persistent GEMM grids get
-        # SMs first; the hash (one batch ahead) fills what is left
-        lo, hi = torch.cuda.Stream.priority_range()
-        if os.environ.get("SIDA_FLAT_PRIORITY"):  # A/B switch for measurements
-            lo = hi = 0
+        # hash and compute streams at the same priority: measured at the bench
+        # shape (tools/pipe_ab.py, base-128, 32K tokens) 8.84-8.97 ms per step
+        # against 9.57-10.35 ms with the compute stream prioritised (the starved
+        # hash kernels then land on SMs late and hold back whole persistent GEMM
+        # grids) and 9.74-9.83 ms with the hash serialised on the compute stream.
+        # SIDA_STREAM_PRIORITY=1 restores the prioritised arrangement (A/B).
+        lo = hi = 0
+        if os.environ.get("SIDA_STREAM_PRIORITY") == "1":
+            lo, hi = torch.cuda.Stream.priority_range()
         self.hash_stream, self.compute_stream = streams or (
             torch.cuda.Stream(device=dev, priority=lo), torch.cuda.Stream(device=dev, priority=hi))
         if os.environ.get("SIDA_HASH_SERIAL") and streams is None:  # A/B: one stream

@@ -19,6 +19,8 @@ p.add_argument("--seq", type=int, default=128)
 p.add_argument("--steps", type=int, default=10)
 p.add_argument("--budget-frac", type=float, default=0.9)
 p.add_argument("--victim-policy", default="spread")
+p.add_argument("--ahead", type=int, default=2, help="batches hashed ahead of the forward")
+p.add_argument("--profile", action="store_true", help="cProfile the timed forwards")
 a = p.parse_args()
 cfg = MoEConfig(vocab_size=32128, d_model=768, num_layers=12, num_experts=a.experts,
                 expert_hidden=3072, max_seq_len=512)
@@ -31,17 +33,22 @@ n = a.batch * a.seq
 lengths = [a.seq] * a.batch
 toks = [torch.randint(0, cfg.vocab_size, (n,), device="cuda", dtype=torch.int32)
         for _ in range(a.steps + 5)]
-tabs = {0: eng.hash_tokens(0, toks[0], lengths)}
+A = a.ahead
+tabs = {i: eng.hash_tokens(i, toks[i], lengths) for i in range(A)}
 for j in range(3):
-    tabs[j + 1] = eng.hash_tokens(j + 1, toks[j + 1], lengths)
+    tabs[j + A] = eng.hash_tokens(j + A, toks[j + A], lengths)
     eng.forward(tabs.pop(j), lengths, tokens_dev=toks[j], next_table=tabs[j + 1])
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 host = []
+if a.profile:
+    import cProfile
+    prof = cProfile.Profile()
+    prof.enable()
 e0.record(eng.compute_stream)
 for j in range(3, 3 + a.steps):
     t0 = time.perf_counter()
-    tabs[j + 1] = eng.hash_tokens(j + 1, toks[j + 1], lengths)
+    tabs[j + A] = eng.hash_tokens(j + A, toks[(j + A) % len(toks)], lengths)
     t1 = time.perf_counter()
     eng.forward(tabs.pop(j), lengths, tokens_dev=toks[j], next_table=tabs[j + 1])
     host.append((t1 - t0, time.perf_counter() - t1))
@@ -51,5 +58,9 @@ torch.cuda.synchronize()
 dev = e0.elapsed_time(e1) / a.steps
 hh = sum(h for h, _ in host) / len(host) * 1e3
 ff = sum(f for _, f in host) / len(host) * 1e3
+if a.profile:
+    import pstats
+    prof.disable()
+    pstats.Stats(prof).sort_stats("tottime").print_stats(18)
 print(f"host per step: hash {hh:.2f} ms + forward {ff:.2f} ms = {hh + ff:.2f} ms; "
       f"device step {dev:.2f} ms")
