@@ -5,21 +5,29 @@
 // (ref moe.py:253-256). The GPU path groups the (token, rank) rows of each
 // layer by expert with a stable counting sort whose output is bit-identical
 // to np.argsort(ids[l].reshape(-1), kind="stable") (oracle/permute.py).
-// Rows are cut into tiles of TILE rows (1024..8192, chosen so that L x tiles
-// covers >= 2 CTAs per SM); one CTA of 256 threads per (layer, tile):
+// Rows are cut into tiles of TILE rows (1024 or 2048); three launches, the
+// last two programmatically dependent on their predecessor:
 //
-//   hist_tiles : 128-bit id loads into shared memory, warp-aggregated
-//                (__match_any_sync) shared histogram -> counts[l][tile][e]
-//   scan       : per layer, one thread per expert: totals over tiles
-//                (coalesced across experts), block exclusive scan -> off,
-//                then each (tile, expert) base position
-//   scatter    : the tile's ids staged again in shared memory; each warp
-//                walks its contiguous rows in order and takes the in-warp
-//                stable rank from __match_any_sync + popc, per-warp running
-//                counts give the cross-warp prefix; inv is written row-ordered
-//                (coalesced), then perm / alpha_perm are written from a
-//                shared-memory copy of the tile in sorted order, so every
-//                (tile, expert) run is a contiguous store.
+//   rank_tiles  one CTA of 256 threads per (layer, tile): the tile's ids
+//               staged in shared memory by 128-bit loads; each warp walks its
+//               contiguous rows in order, the in-warp stable rank from the
+//               mask of lanes with the same expert (one ballot per id bit)
+//               + popc and per-warp running counts per expert; a per-expert prefix over the warps turns them into
+//               the row's rank among the tile's rows of its expert. Writes
+//               the tile's per-expert counts and one code per row
+//               (expert | rank << 10), both coalesced.
+//   tile_base   one CTA per layer, threads = (tile chunk, expert): the
+//               exclusive scan of the counts over tiles (each (tile, expert)
+//               run's offset inside its expert), then a block scan of the
+//               expert totals with warp-shuffle prefix sums -> hist, off.
+//   place_tiles one CTA per (layer, tile): position of row r = off[e] +
+//               base[tile][e] + rank; inv written row-ordered (coalesced),
+//               the tile's rows staged in shared memory in sorted order so
+//               that perm / alpha_perm are written as contiguous runs per
+//               (tile, expert).
+//
+// Every row's expert is matched once (the rank pass), and no CTA re-reads
+// the count matrix column of its layer.
 //
 // Since SiDA's hash table holds every layer's ids before inference starts
 // (ref pipeline.py:208-215), all L layers are permuted in one chain on the
@@ -33,13 +41,12 @@ namespace sida {
 constexpr int kPermThreads = 256;
 constexpr int kPermWarps = kPermThreads / 32;
 constexpr int kMaxExperts = 1024;
+constexpr int kRankShift = 10;  // code = expert | rank_in_tile << 10 (K <= 1024, TILE <= 2^21)
 
-// Tile rows for (rows, layers): >= 2 CTAs per SM when the batch allows it.
+// Tile rows for (rows, layers): 2048, or 1024 when that is needed for ~2 CTAs per SM.
 static inline int perm_tile(int n_rows, int n_layers) {
-  const long long want = (long long)n_rows * std::max(n_layers, 1) / (2 * kNumSMs);
-  int t = 1024;
-  while (t < 8192 && 2ll * t <= want) t *= 2;
-  return t;
+  const long long work = (long long)n_rows * std::max(n_layers, 1);
+  return work >= 2048ll * 2 * kNumSMs ? 2048 : 1024;
 }
 
 static inline int perm_tiles(int n_rows, int tile) { return std::max(1, ceil_div(n_rows, tile)); }
@@ -60,104 +67,53 @@ __device__ __forceinline__ void stage_ids(const int32_t* __restrict__ row_ids, i
   }
 }
 
-template <int TILE>
-__global__ void __launch_bounds__(kPermThreads)
-hist_tiles_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
-                  int32_t* __restrict__ counts, int32_t* __restrict__ err) {
-  __shared__ int32_t s_ids[TILE];
-  extern __shared__ int32_t s_hist[];  // [K]
-  const int layer = blockIdx.y, tile = blockIdx.x;
-  const int lane = threadIdx.x & 31;
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (int e = threadIdx.x; e < K; e += blockDim.x) s_hist[e] = 0;
-  const int r0 = tile * TILE, r1 = min(n_rows, r0 + TILE);
-  stage_ids(ids + (size_t)layer * n_rows, r0, r1, s_ids);
-  __syncthreads();
-  const unsigned lt = (1u << lane) - 1u;
-  bool bad = false;
-  for (int i = threadIdx.x; i < TILE; i += blockDim.x) {  // uniform trip count: full warps
-    int e = i < r1 - r0 ? s_ids[i] : -1;
-    if (i < r1 - r0 && (e < 0 || e >= K)) { bad = true; e = -1; }
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
-    if (e >= 0 && (peers & lt) == 0) atomicAdd(&s_hist[e], __popc(peers));
+// Lanes of the warp holding the same key as this lane (keys in [0, 2^nbits)
+// or -1): one ballot per key bit plus one for validity. The same mask as
+// __match_any_sync, without its serialised MIO-pipe cost (ncu: MATCH bound
+// the rank pass at ~90 cycles per warp instruction per SM).
+__device__ __forceinline__ unsigned lanes_with_key(int e, int nbits) {
+  const bool valid = e >= 0;
+  const unsigned vb = __ballot_sync(0xffffffffu, valid);
+  unsigned m = valid ? vb : ~vb;
+  for (int b = 0; b < nbits; ++b) {
+    const bool bit = (e >> b) & 1;
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    m &= bit ? bal : ~bal;
   }
-  if (bad) atomicExch(err, 1);
-  __syncthreads();
-  int32_t* c = counts + ((size_t)layer * n_tiles + tile) * K;
-  for (int e = threadIdx.x; e < K; e += blockDim.x) c[e] = s_hist[e];
+  return m;
 }
 
 template <int TILE>
-__global__ void __launch_bounds__(kPermThreads, 2)
-scatter_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
-               const int32_t* __restrict__ counts, const float* __restrict__ alpha_rows,
-               int32_t* __restrict__ perm, int32_t* __restrict__ inv,
-               float* __restrict__ alpha_perm, int32_t* __restrict__ hist,
-               int32_t* __restrict__ off) {
+__global__ void __launch_bounds__(kPermThreads)
+rank_tiles_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
+                  int32_t* __restrict__ counts, int32_t* __restrict__ codes,
+                  int32_t* __restrict__ err) {
   constexpr int R = TILE / kPermWarps;  // contiguous rows per warp
   constexpr int NR = R / 32;            // rounds per warp
   extern __shared__ int32_t smem[];
-  int32_t* s_ids = smem;                        // [TILE] ids, then sorted rows
-  int32_t* s_ord = s_ids + TILE;                // [TILE] tile row of sorted position q
-  int32_t* s_cnt = s_ord + TILE;                // [warps][K] counts -> warp prefix
-  int32_t* s_tbase = s_cnt + kPermWarps * K;    // [K] global base of (tile, e)
-  int32_t* s_texc = s_tbase + K;                // [K + 1] tile-local exclusive prefix
+  int32_t* s_ids = smem;          // [TILE]
+  int32_t* s_cnt = s_ids + TILE;  // [warps][K] counts -> warp prefix
   const int layer = blockIdx.y, tile = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r0 = tile * TILE, r1 = min(n_rows, r0 + TILE), n = r1 - r0;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int i = threadIdx.x; i < kPermWarps * K; i += blockDim.x) s_cnt[i] = 0;
   stage_ids(ids + (size_t)layer * n_rows, r0, r1, s_ids);
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // hist_tiles' counts are complete
-  // this tile's base positions from the layer's (tile, expert) count matrix
-  // (written by hist_tiles; n_tiles x K ints read from L2): per expert the
-  // total and the count in earlier tiles, then an exclusive scan of the
-  // totals over experts; tile 0 also publishes hist / off
-  const int32_t* cl = counts + (size_t)layer * n_tiles * K;
-  for (int e = threadIdx.x; e < K; e += blockDim.x) {
-    int tot = 0, pre = 0;
-    for (int t = 0; t < n_tiles; ++t) {
-      const int c = __ldg(cl + (size_t)t * K + e);
-      tot += c;
-      pre += t < tile ? c : 0;
-    }
-    s_texc[e] = tot;
-    s_tbase[e] = pre;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    int carry = 0;
-    for (int b = 0; b < K; b += 32) {
-      const int e = b + lane;
-      const int v = e < K ? s_texc[e] : 0;
-      int incl = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (e < K) {
-        s_tbase[e] += carry + incl - v;
-        if (tile == 0) {
-          hist[(size_t)layer * K + e] = v;
-          off[(size_t)layer * (K + 1) + e] = carry + incl - v;
-        }
-      }
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (tile == 0 && lane == 0) off[(size_t)layer * (K + 1) + K] = carry;
-  }
   __syncthreads();
 
-  // pass 1: in-order stable local ranks, per warp over its R rows
+  // in-order stable ranks, per warp over its R rows
   const unsigned lt = (1u << lane) - 1u;
   int32_t* my_cnt = s_cnt + warp * K;
+  int nbits = 0;
+  while ((1 << nbits) < K) ++nbits;
   int loc[NR];
+  bool bad = false;
 #pragma unroll
   for (int j = 0; j < NR; ++j) {
     const int i = warp * R + j * 32 + lane;
     int e = i < n ? s_ids[i] : -1;
-    if (e >= K) e = -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, e);
+    if (i < n && (e < 0 || e >= K)) { bad = true; e = -1; }
+    const unsigned peers = lanes_with_key(e, nbits);
     int base = 0;
     if (e >= 0) base = my_cnt[e];
     __syncwarp();
@@ -165,22 +121,152 @@ scatter_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
     __syncwarp();
     loc[j] = base + __popc(peers & lt);
   }
+  if (bad) atomicExch(err, 1);
   __syncthreads();
-
-  // warp prefix per expert (in place) and the tile's per-expert totals
+  // warp prefix per expert (in place); the tile's per-expert totals
+  int32_t* c = counts + ((size_t)layer * n_tiles + tile) * K;
   for (int e = threadIdx.x; e < K; e += blockDim.x) {
     int run = 0;
 #pragma unroll
     for (int w = 0; w < kPermWarps; ++w) {
-      const int c = s_cnt[w * K + e];
+      const int v = s_cnt[w * K + e];
       s_cnt[w * K + e] = run;
-      run += c;
+      run += v;
     }
-    s_texc[e] = run;  // total; scanned below
+    c[e] = run;
   }
   __syncthreads();
-  // exclusive scan of the totals over experts (one warp, K <= 1024)
+  int32_t* lcode = codes + (size_t)layer * n_rows + r0;
+#pragma unroll
+  for (int j = 0; j < NR; ++j) {
+    const int i = warp * R + j * 32 + lane;
+    if (i < n) {
+      const int e = s_ids[i];
+      lcode[i] = (e >= 0 && e < K) ? (e | ((s_cnt[warp * K + e] + loc[j]) << kRankShift)) : -1;
+    }
+  }
+}
+
+// Block-wide exclusive scan of v over the block's threads (blockDim.x a
+// multiple of 32, <= 1024); returns the exclusive prefix, *total the sum.
+__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
   if (warp == 0) {
+    int w = lane < nw ? s_warp[lane] : 0;
+    int wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < nw) s_warp[lane] = wi - w;
+    if (lane == 31) s_warp[32] = wi;
+  }
+  __syncthreads();
+  *total = s_warp[32];
+  return s_warp[warp] + incl - v;
+}
+
+// One CTA of 1024 threads per layer: thread (q, e) owns expert e's counts over
+// the q-th of Q contiguous tile chunks (Q = 1024 / K rounded to 32, up to 32):
+// chunk sums, a prefix over the chunks in shared memory, then base[l][t][e] =
+// sum of counts[l][t'][e] over t' < t; hist, off from the expert totals by a
+// block scan with warp-shuffle prefix sums.
+__global__ void __launch_bounds__(1024)
+tile_base_kernel(const int32_t* __restrict__ counts, int K, int n_tiles, int32_t* __restrict__ base,
+                 int32_t* __restrict__ hist, int32_t* __restrict__ off) {
+  __shared__ int s_warp[33];
+  __shared__ int s_part[1024];
+  const int layer = blockIdx.x;
+  const int KP = (K + 31) & ~31;
+  const int Q = blockDim.x / KP;
+  const int e = threadIdx.x % KP, q = threadIdx.x / KP;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // rank_tiles' counts are complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int32_t* cl = counts + (size_t)layer * n_tiles * K;
+  int32_t* bl = base + (size_t)layer * n_tiles * K;
+  const int t0 = q < Q ? q * n_tiles / Q : n_tiles, t1 = q < Q ? (q + 1) * n_tiles / Q : n_tiles;
+  const bool mine = q < Q && e < K;
+  int sum = 0;
+  if (mine) {
+    int t = t0;
+    for (; t + 8 <= t1; t += 8) {  // eight loads in flight
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = cl[(size_t)(t + u) * K + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) sum += v[u];
+    }
+    for (; t < t1; ++t) sum += cl[(size_t)t * K + e];
+  }
+  if (q < Q) s_part[threadIdx.x] = sum;
+  __syncthreads();
+  int run = 0, tot = 0;
+  if (mine) {
+    for (int r = 0; r < Q; ++r) {
+      const int v = s_part[r * KP + e];
+      run += r < q ? v : 0;
+      tot += v;
+    }
+    int t = t0;
+    for (; t + 8 <= t1; t += 8) {
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = cl[(size_t)(t + u) * K + e];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        bl[(size_t)(t + u) * K + e] = run;
+        run += v[u];
+      }
+    }
+    for (; t < t1; ++t) {
+      const int v = cl[(size_t)t * K + e];
+      bl[(size_t)t * K + e] = run;
+      run += v;
+    }
+  }
+  // exclusive scan of the expert totals over experts (threads q == 0)
+  int total;
+  const int o = block_exclusive_scan(q == 0 && e < K ? tot : 0, s_warp, &total);
+  if (q == 0 && e < K) {
+    hist[(size_t)layer * K + e] = tot;
+    off[(size_t)layer * (K + 1) + e] = o;
+  }
+  if (threadIdx.x == 0) off[(size_t)layer * (K + 1) + K] = total;
+}
+
+template <int TILE>
+__global__ void __launch_bounds__(kPermThreads)
+place_tiles_kernel(const int32_t* __restrict__ codes, int n_rows, int K, int n_tiles,
+                   const int32_t* __restrict__ counts, const int32_t* __restrict__ base,
+                   const int32_t* __restrict__ off, const float* __restrict__ alpha_rows,
+                   int32_t* __restrict__ perm, int32_t* __restrict__ inv,
+                   float* __restrict__ alpha_perm) {
+  extern __shared__ int32_t smem[];
+  int32_t* s_code = smem;              // [TILE]
+  int32_t* s_ord = s_code + TILE;      // [TILE] tile row of sorted position q
+  int32_t* s_pos0 = s_ord + TILE;      // [K] first output position of (tile, e)
+  int32_t* s_texc = s_pos0 + K;        // [K + 1] tile-local exclusive prefix
+  const int layer = blockIdx.y, tile = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r0 = tile * TILE, r1 = min(n_rows, r0 + TILE), n = r1 - r0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // codes, counts, base, off complete
+  stage_ids(codes + (size_t)layer * n_rows, r0, r1, s_code);
+  const size_t ct = ((size_t)layer * n_tiles + tile) * K;
+  for (int e = threadIdx.x; e < K; e += blockDim.x) {
+    s_texc[e] = counts[ct + e];
+    s_pos0[e] = off[(size_t)layer * (K + 1) + e] + base[ct + e];
+  }
+  __syncthreads();
+  if (warp == 0) {  // exclusive scan of the tile's counts over experts
     int carry = 0;
     for (int b = 0; b < K; b += 32) {
       const int e = b + lane;
@@ -197,20 +283,15 @@ scatter_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
     if (lane == 0) s_texc[K] = carry;
   }
   __syncthreads();
-
-  // pass 2: positions; inv row-ordered, sorted order staged in shared memory
-  int32_t* linv = inv + (size_t)layer * n_rows;
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    const int i = warp * R + j * 32 + lane;
-    int e = i < n ? s_ids[i] : -1;
-    if (e >= K) e = -1;
-    if (e >= 0) {
-      const int within = s_cnt[warp * K + e] + loc[j];
-      linv[r0 + i] = s_tbase[e] + within;
-      s_ord[s_texc[e] + within] = i;
-    } else if (i < n) {
-      linv[r0 + i] = -1;
+  int32_t* linv = inv + (size_t)layer * n_rows + r0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int code = s_code[i];
+    if (code >= 0) {
+      const int e = code & (kMaxExperts - 1), w = code >> kRankShift;
+      linv[i] = s_pos0[e] + w;
+      s_ord[s_texc[e] + w] = i;
+    } else {
+      linv[i] = -1;
     }
   }
   __syncthreads();
@@ -220,8 +301,8 @@ scatter_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tiles,
   float* lap = alpha_perm ? alpha_perm + (size_t)layer * n_rows : nullptr;
   for (int q = threadIdx.x; q < n_valid; q += blockDim.x) {
     const int i = s_ord[q];
-    const int e = s_ids[i];
-    const int pos = s_tbase[e] + (q - s_texc[e]);
+    const int e = s_code[i] & (kMaxExperts - 1);
+    const int pos = s_pos0[e] + (q - s_texc[e]);
     lperm[pos] = r0 + i;
     if (lap) lap[pos] = la[i];
   }
@@ -256,36 +337,17 @@ using namespace sida;
 
 extern "C" size_t sida_permute_workspace_bytes(int n_layers, int n_rows, int num_experts) {
   const int tile = perm_tile(n_rows, n_layers);
-  size_t n = (size_t)n_layers * num_experts * perm_tiles(n_rows, tile);
-  return align_up(2 * n * sizeof(int32_t), 256);
+  const size_t n = (size_t)n_layers * num_experts * perm_tiles(n_rows, tile);
+  return 2 * align_up(n * sizeof(int32_t), 256) +
+         align_up((size_t)n_layers * std::max(n_rows, 1) * sizeof(int32_t), 256);
 }
 
-template <int TILE>
-static int permute_launch(const int32_t* ids, int n_layers, int n_rows, int K, const float* alpha_rows,
-                          int32_t* hist, int32_t* off, int32_t* perm, int32_t* inv,
-                          float* alpha_perm, int32_t* counts, int32_t* err,
-                          cudaStream_t s) {
-  const int n_tiles = perm_tiles(n_rows, TILE);
-  dim3 grid(n_tiles, n_layers);
-  hist_tiles_kernel<TILE><<<grid, kPermThreads, K * sizeof(int32_t), s>>>(ids, n_rows, K, n_tiles,
-                                                                         counts, err);
-  SIDA_LAUNCH_CHECK();
-  // the scatter also publishes hist / off, so it runs even for zero rows;
-  // programmatic dependent launch: its CTAs stage their ids while the
-  // histogram grid drains and wait (griddepcontrol.wait) only before reading
-  // the count matrix
-  const size_t smem = (2ull * TILE + (size_t)(kPermWarps + 2) * K + 1) * sizeof(int32_t);
-  static bool configured = false;
-  if (!configured) {
-    SIDA_CUDA(cudaFuncSetAttribute(scatter_kernel<TILE>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)((2ull * TILE + (kPermWarps + 2) * kMaxExperts + 1) *
-                                         sizeof(int32_t))));
-    configured = true;
-  }
+template <typename Kern, typename... Args>
+static int launch_pdl(Kern kern, dim3 grid, int threads, size_t smem, cudaStream_t s,
+                      Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = grid;
-  cfg.blockDim = dim3(kPermThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -293,11 +355,46 @@ static int permute_launch(const int32_t* ids, int n_layers, int n_rows, int K, c
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SIDA_CUDA(cudaLaunchKernelEx(&cfg, scatter_kernel<TILE>, ids, n_rows, K, n_tiles,
-                               (const int32_t*)counts, alpha_rows, perm, inv, alpha_perm, hist,
-                               off));
+  SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
   count_launch();
   return SIDA_OK;
+}
+
+template <int TILE>
+static int permute_launch(const int32_t* ids, int n_layers, int n_rows, int K, const float* alpha_rows,
+                          int32_t* hist, int32_t* off, int32_t* perm, int32_t* inv,
+                          float* alpha_perm, void* workspace, int32_t* err, cudaStream_t s) {
+  const int n_tiles = perm_tiles(n_rows, TILE);
+  const size_t n = (size_t)n_layers * K * n_tiles;
+  uint8_t* ws = static_cast<uint8_t*>(workspace);
+  int32_t* counts = reinterpret_cast<int32_t*>(ws);
+  int32_t* base = reinterpret_cast<int32_t*>(ws + align_up(n * sizeof(int32_t), 256));
+  int32_t* codes = reinterpret_cast<int32_t*>(ws + 2 * align_up(n * sizeof(int32_t), 256));
+  const dim3 grid(n_tiles, n_layers);
+  const size_t smem1 = ((size_t)TILE + (size_t)kPermWarps * K) * sizeof(int32_t);
+  const size_t smem3 = (2ull * TILE + 2ull * K + 1) * sizeof(int32_t);
+  static bool configured = false;
+  if (!configured) {
+    SIDA_CUDA(cudaFuncSetAttribute(rank_tiles_kernel<TILE>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(((size_t)TILE + (size_t)kPermWarps * kMaxExperts) *
+                                         sizeof(int32_t))));
+    configured = true;
+  }
+  if (n_rows > 0) {
+    rank_tiles_kernel<TILE><<<grid, kPermThreads, smem1, s>>>(ids, n_rows, K, n_tiles, counts, codes,
+                                                              err);
+    SIDA_LAUNCH_CHECK();
+  } else {
+    SIDA_CUDA(cudaMemsetAsync(counts, 0, n * sizeof(int32_t), s));
+  }
+  // tile_base publishes hist / off, so it runs even for zero rows
+  int st = launch_pdl(tile_base_kernel, dim3(n_layers), 1024, 0, s, (const int32_t*)counts, K,
+                      n_tiles, base, hist, off);
+  if (st || n_rows == 0) return st;
+  return launch_pdl(place_tiles_kernel<TILE>, grid, kPermThreads, smem3, s, (const int32_t*)codes,
+                    n_rows, K, n_tiles, (const int32_t*)counts, (const int32_t*)base,
+                    (const int32_t*)off, alpha_rows, perm, inv, alpha_perm);
 }
 
 extern "C" int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, int num_experts,
@@ -313,20 +410,14 @@ extern "C" int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, i
   SIDA_REQUIRE(!alpha_perm || alpha_rows, SIDA_ERR_CONTRACT, "alpha_perm needs alpha_rows");
   SIDA_REQUIRE(err_flag && hist && off && (n_rows == 0 || (ids && perm && inv)), SIDA_ERR_CONTRACT,
                "null pointer passed to sida_permute_hist");
+  SIDA_REQUIRE(workspace && ((uintptr_t)workspace & 255) == 0, SIDA_ERR_CONTRACT,
+               "permute workspace must be 256-byte aligned");
   cudaStream_t s = as_stream(stream);
-  const int tile = perm_tile(n_rows, n_layers);
-  const size_t n = (size_t)n_layers * num_experts * perm_tiles(n_rows, tile);
-  int32_t* counts = static_cast<int32_t*>(workspace);
-  switch (tile) {
-    case 1024: return permute_launch<1024>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
-                                           perm, inv, alpha_perm, counts, err_flag, s);
-    case 2048: return permute_launch<2048>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
-                                           perm, inv, alpha_perm, counts, err_flag, s);
-    case 4096: return permute_launch<4096>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
-                                           perm, inv, alpha_perm, counts, err_flag, s);
-    default: return permute_launch<8192>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off,
-                                         perm, inv, alpha_perm, counts, err_flag, s);
-  }
+  if (perm_tile(n_rows, n_layers) == 2048)
+    return permute_launch<2048>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off, perm,
+                                inv, alpha_perm, workspace, err_flag, s);
+  return permute_launch<1024>(ids, n_layers, n_rows, num_experts, alpha_rows, hist, off, perm, inv,
+                              alpha_perm, workspace, err_flag, s);
 }
 
 // dst[p] = src[idx[p]] for bf16 rows (16-byte vectors): the expert-parallel

@@ -21,6 +21,7 @@ p.add_argument("--d", type=int, default=768)
 p.add_argument("--h", type=int, default=3072)
 p.add_argument("--iters", type=int, default=20)
 p.add_argument("--no-cublas", action="store_true")
+p.add_argument("--exact", action="store_true", help="exactly tokens/experts rows per expert")
 p.add_argument("--alias-slots", type=int, default=0,
                help="map every expert onto this many slots (weights L2-resident: isolates "
                     "the HBM weight stream)")
@@ -30,7 +31,8 @@ cfg = MoEConfig(vocab_size=64, d_model=a.d, num_layers=1, num_experts=a.experts,
 model = MoEModel.synthetic(cfg, 0)
 store = ExpertStore.full(model)
 N, K = a.tokens, a.experts
-ids = torch.randint(0, K, (1, N, 1), device="cuda", dtype=torch.int32)
+ids = (torch.arange(N, device="cuda", dtype=torch.int32) % K).view(1, N, 1) if a.exact else \
+    torch.randint(0, K, (1, N, 1), device="cuda", dtype=torch.int32)
 al = torch.rand((1, N, 1), device="cuda", dtype=torch.float64)
 dt = DeviceTable(ids, al, al.float(), N, 1)
 dt.permute(K, torch.cuda.current_stream())

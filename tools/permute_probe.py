@@ -31,4 +31,16 @@ for _ in range(a.iters):
     _lib.check(_lib.lib().sida_gather_rows_bf16(x.data_ptr(), dt.perm[0].data_ptr(), N, 1, a.d,
                                                 xp.data_ptr(), st.cuda_stream))
 torch.cuda.synchronize()
-print("ok")
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+reps = 20
+e0.record(st)
+for _ in range(reps):
+    dt.permute(K, st)
+e1.record(st)
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / reps
+# SURVEY §8(d) algorithmic bytes: ids + perm + inv (4 B each per row) + 8 K, plus the
+# alpha row read and alpha_perm write of this path (4 B each)
+byts = L * (N * (4 + 4 + 4 + 4 + 4) + 8 * K)
+print(f"permute L={L} rows={N} K={K}: {ms * 1e3:.1f} us per call, {byts / ms / 1e6:.0f} GB/s "
+      f"({byts / 1e6:.1f} MB)")
