@@ -161,8 +161,9 @@ int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, int d, int h
 
 /* Observability: per-CTA cycle counters of the last sida_grouped_ffn_bf16
  * call when the process runs with SIDA_GEMM_PROF=1 (producer wait, MMA wait
- * on epilogue / on TMA, MMA loop, epilogue wait, epilogue loop, tiles).
- * out: uint64 [2 GEMMs][148 CTAs][8]. Synchronises the device. */
+ * on epilogue / on TMA, MMA loop, epilogue wait, epilogue loop, tiles, -,
+ * then %globaltimer ns at entry, past the PDL wait, at exit).
+ * out: uint64 [2 GEMMs][148 CTAs][12]. Synchronises the device. */
 int sida_debug_gemm_prof(unsigned long long* out);
 
 /* Expert-FFN tile family for sida_grouped_ffn_bf16: -1 auto, 0 token-M

@@ -88,11 +88,19 @@ struct GemmParams {
   int32_t* err_flag;
   unsigned long long* prof;    // optional per-CTA cycle counters (sida_debug_gemm_prof)
   int linear;                  // GEMM1 epilogue without the ReLU (sida_linear_bf16)
+  // CTA-pair launches: an expert's last tile holding <= 128 rows runs as an
+  // M=128 pair MMA (64 rows per CTA) at half the tensor time of M=256
+  int half_tiles;
 };
 
 // prof slots per CTA: producer wait(empty), MMA wait(tmem_empty), MMA wait(full),
 // MMA loop total, epilogue wait(tmem_full), epilogue loop total, tiles
-constexpr int kProfSlots = 8;
+constexpr int kProfSlots = 12;  // + [8] entry, [9] after the PDL wait, [10] exit (%globaltimer ns)
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ unsigned long long clk() { return clock64(); }
 
 // PTX shims: sm100_ptx.cuh
@@ -100,6 +108,7 @@ __device__ __forceinline__ unsigned long long clk() { return clock64(); }
 // ------------------------------------------------------------ tile schedule
 struct TileInfo {
   int expert, row0, row_end, ncol0, slot;
+  bool half;  // M=128 pair tile (see GemmParams::half_tiles)
 };
 
 // Destination of bf16 output row v: local out_bf16, or a (peer rank, row)
@@ -133,6 +142,7 @@ __device__ __forceinline__ TileInfo decode_mt(int mt, int nt, const int32_t* s_p
   ti.row_end = expert_row(p, ti.expert + 1);
   ti.ncol0 = nt * BN;
   ti.slot = p.expert_slot ? p.expert_slot[ti.expert] : 0;
+  ti.half = p.half_tiles && TM == 2 * BM && BN % 128 == 0 && ti.row_end - ti.row0 <= BM;
   return ti;
 }
 
@@ -205,16 +215,36 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const uint32_t rank = CG == 1 ? 0u : cluster_rank();
   const bool leader = rank == 0;
   const int unit = blockIdx.x / CG, n_units = gridDim.x / CG;  // CTA pairs walk tiles together
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 8] = gtime();
 
-  if (threadIdx.x == 0) {
+  if (warp == 2) {
+    // m-tile prefix over the listed experts: one warp, 32 experts per step
+    // (a serial loop here costs one dependent L2 round trip per expert,
+    // ~35 us at 128 experts, exposed because two of these CTAs cannot share
+    // an SM, so the prologue cannot overlap the previous launch's tail)
     int acc = 0;
-    for (int i = 0; i < n_list; ++i) {
-      const int e = p.expert_list ? p.expert_list[i] : i;
-      s_expert[i] = e;
-      s_prefix[i] = acc;
-      acc += ceil_div(expert_row(p, e + 1) - expert_row(p, e), TM);
+    for (int i0 = 0; i0 < n_list; i0 += 32) {
+      const int i = i0 + lane;
+      int cnt = 0, e = 0;
+      if (i < n_list) {
+        e = p.expert_list ? p.expert_list[i] : i;
+        cnt = ceil_div(expert_row(p, e + 1) - expert_row(p, e), TM);
+      }
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (i < n_list) {
+        s_expert[i] = e;
+        s_prefix[i] = acc + incl - cnt;
+      }
+      acc += __shfl_sync(0xffffffffu, incl, 31);
     }
-    s_prefix[n_list] = acc;
+    if (lane == 0) s_prefix[n_list] = acc;
+  }
+  if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -256,6 +286,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   // residual) are read only after it has completed and flushed
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 9] = gtime();
 
   const int n_ntiles = p.ndim / BN;            // (STAGE 3: GEMM1 column tiles)
   const int n2tiles = STAGE == 3 ? p2.ndim / BN : 0;
@@ -322,7 +353,10 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           if (p.prof) w_empty += clk() - c0;
           const uint32_t fb = CG == 1 ? smem_u32(&full[stage]) : map_rank(smem_u32(&full[stage]), 0);
           if (leader) mbar_expect_tx(&full[stage], CG * (kABytes + kBBytes));
-          tma_load_2d<CG>(sA + stage * kABytes, ta, kb * BK, ti.row0 + rank * BM, fb);
+          // (an M=128 pair tile takes rows [64 r, 64 r + 64) of CTA r: the first
+          // half of its 128-row box)
+          tma_load_2d<CG>(sA + stage * kABytes, ta, kb * BK, ti.row0 + rank * (ti.half ? BM / 2 : BM),
+                          fb);
           tma_load_3d<CG>(sB + stage * kBBytes, tb, kb * BK, ti.ncol0 + rank * BNL, ti.slot, fb);
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -333,7 +367,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   } else if (warp == 1) {
     // ===== MMA issuer (single thread of the leader CTA)
     if (lane == 0 && leader) {
-      constexpr uint32_t idesc = idesc_bf16<TM, BN>();
+      constexpr uint32_t idesc_full = idesc_bf16<TM, BN>();
+      constexpr uint32_t idesc_half = idesc_bf16<(TM > BM ? TM / 2 : TM), BN>();
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -351,6 +386,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           continue;
         }
         const int n_kblocks = ((STAGE == 3 && g2) ? p2.kdim : p.kdim) / BK;
+        const uint32_t idesc = ti.half ? idesc_half : idesc_full;
         ++n_tiles;
         const unsigned long long c0 = p.prof ? clk() : 0;
         if constexpr (CG == 1) mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -410,7 +446,11 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       if (ti.slot < 0) continue;
       const bool st2 = STAGE == 2 || (STAGE == 3 && g2);
       const GemmParams& gp = (STAGE == 3 && g2) ? p2 : p;
-      const int qrow0 = ti.row0 + rank * BM + quarter * 32;  // first row of this warp's quarter
+      // first row of this warp's quarter. An M=128 pair tile's accumulator
+      // (64 rows per CTA) sits in TMEM as two halves: N columns [0, BN/2) in
+      // lanes 0-63 and [BN/2, BN) in lanes 64-127, each over BN/2 columns
+      const int qrow0 = ti.half ? ti.row0 + rank * (BM / 2) + (quarter & 1) * 32
+                                : ti.row0 + rank * BM + quarter * 32;
       const int my_row = qrow0 + lane;
       const bool valid = my_row < ti.row_end;
       const uint16_t* bias = reinterpret_cast<const uint16_t*>(
@@ -427,24 +467,27 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
             if (r < gp.bf16_k) brow[r] = gp.bf16_map[static_cast<size_t>(orow) * gp.bf16_k + r];
         }
       }
-      const int cbase = ti.ncol0 + half * kHalfCols;
+      const int cbase = ti.half ? ti.ncol0 + (quarter >> 1) * kHalfCols + half * (kHalfCols / 2)
+                                : ti.ncol0 + half * kHalfCols;
+      const int nchunks = ti.half ? kChunks / 2 : kChunks;
       const unsigned long long c2 = p.prof ? clk() : 0;
       mbar_wait(&tmem_full[acc], acc_phase);
       if (p.prof) w_full += clk() - c2;
       tc_fence_after();
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) +
-                             acc * (kTmemCols / 2) + half * kHalfCols;
+                             acc * (kTmemCols / 2) + half * (ti.half ? kHalfCols / 2 : kHalfCols);
       uint32_t v[2][32];
       tmem_ld32_nowait(t_row, v[0]);
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
+        if (kChunks % 2 == 0 && c == kChunks / 2 && nchunks == kChunks / 2) break;
         const int col0 = cbase + c * 32;
         const uint4* bvec = reinterpret_cast<const uint4*>(bias + col0);
         uint4 braw[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) braw[q] = __ldg(bvec + q);
         tmem_wait_ld();
-        if (c + 1 < kChunks) tmem_ld32_nowait(t_row + (c + 1) * 32, v[(c + 1) & 1]);
+        if (c + 1 < nchunks) tmem_ld32_nowait(t_row + (c + 1) * 32, v[(c + 1) & 1]);
         const uint32_t* vv = v[c & 1];
         float f[32];
 #pragma unroll
@@ -576,6 +619,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 
   tc_fence_before();
   if constexpr (CG == 1) __syncthreads(); else cluster_sync();
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 10] = gtime();
   if (warp == 1) {
     tc_fence_after();
     if constexpr (CG == 1)
@@ -650,17 +694,32 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
   const bool leader = rank == 0;
   const int unit = blockIdx.x >> 1, n_units = gridDim.x >> 1;
 
-  if (threadIdx.x == 0) {
+  if (warp == 2) {
+    // token-tile prefix over the listed experts: one warp, 32 experts per step
     int acc = 0;
-    for (int i = 0; i < n_list; ++i) {
-      const int e = p.expert_list ? p.expert_list[i] : i;
-      int base, cnt;
-      tn_split(expert_row(p, e + 1) - expert_row(p, e), base, cnt);
-      s_expert[i] = e;
-      s_prefix[i] = acc;
-      acc += cnt;
+    for (int i0 = 0; i0 < n_list; i0 += 32) {
+      const int i = i0 + lane;
+      int cnt = 0, e = 0;
+      if (i < n_list) {
+        e = p.expert_list ? p.expert_list[i] : i;
+        int base;
+        tn_split(expert_row(p, e + 1) - expert_row(p, e), base, cnt);
+      }
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (i < n_list) {
+        s_expert[i] = e;
+        s_prefix[i] = acc + incl - cnt;
+      }
+      acc += __shfl_sync(0xffffffffu, incl, 31);
     }
-    s_prefix[n_list] = acc;
+    if (lane == 0) s_prefix[n_list] = acc;
+  }
+  if (threadIdx.x == 0) {
     for (int i = 0; i < kTnStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -1467,7 +1526,7 @@ static unsigned long long* prof_buffer(int gemm) {
 }
 
 // Observability: copy the per-CTA cycle counters of the last FFN call
-// (enabled by SIDA_GEMM_PROF=1) into out[2][148][8]; synchronises the device.
+// (enabled by SIDA_GEMM_PROF=1) into out[2][148][12]; synchronises the device.
 extern "C" int sida_debug_gemm_prof(unsigned long long* out) {
   SIDA_REQUIRE(g_prof, SIDA_ERR_UNSUPPORTED, "run with SIDA_GEMM_PROF=1 to collect counters");
   SIDA_CUDA(cudaDeviceSynchronize());
@@ -1489,7 +1548,12 @@ static int choose_cg(int gemm, int n_rows, int listed) {
     forced = e ? atoi(e) : 0;
   }
   if (forced == 1 || forced == 2) return forced;
-  return n_rows >= (gemm == 1 ? 1024 : 192) * listed ? 2 : 1;
+  (void)gemm;
+  // pair tiles whenever experts average >= 96 rows: with the M=128 pair tile
+  // for an expert's last <= 128 rows (half_tiles) they cost no more tensor
+  // time than 128-row single-CTA tiles and stream each expert's weights to
+  // the SMs fewer times (2.5 -> 1.5 per expert at 256 +- 16 rows)
+  return n_rows >= 96 * listed ? 2 : 1;
 }
 
 // Tile family per expert GEMM (sida_set_ffn_tiles, or SIDA_FFN_SWAP at load):
@@ -1612,6 +1676,7 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   p1.expert_list = expert_list; p1.n_list = n_list;
   p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
   p1.hidden = hidden; p1.err_flag = err_flag; p1.prof = prof_buffer(0);
+  p1.half_tiles = 1;
   int st = choose_tn(1, n_rows, listed, d, h) ? sm100::launch_tn<1>(x_perm, ar, n_slots, p1, listed, s)
               : sm100::dispatch_gemm<1>(x_perm, ar, n_slots, p1, listed,
                                         choose_cg(1, n_rows, listed), s);
@@ -1835,6 +1900,7 @@ extern "C" int sida_grouped_ffn_bf16_peer(const uint16_t* x_loc, int n_rows, int
   p1.off = off; p1.num_experts = num_experts; p1.expert_slot = expert_slot;
   p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
   p1.hidden = hidden; p1.err_flag = err_flag;
+  p1.half_tiles = 1;
   int st = sm100::dispatch_gemm<1>(x_loc, ar, n_slots, p1, num_experts,
                                    choose_cg(1, n_rows, num_experts), s);
   if (st) return st;

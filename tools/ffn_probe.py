@@ -61,12 +61,23 @@ fl = 4.0 * N * a.d * a.h
 print(f"ffn layer: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s  (N={N}, K={K}, d={a.d}, h={a.h})")
 if os.environ.get("SIDA_GEMM_PROF"):
     from paper_2310_18859_b200 import _lib
-    buf = np.zeros((2, 148, 8), dtype=np.uint64)
+    buf = np.zeros((2, 148, 12), dtype=np.uint64)
     _lib.check(_lib.load().sida_debug_gemm_prof(buf.ctypes.data))
     names = ["prod_wait_empty", "mma_wait_epi", "mma_wait_tma", "mma_total", "epi_wait_full",
              "epi_total", "tiles"]
     for gi in range(2):
         b = buf[gi].astype(np.float64)
+        lead = b[b[:, 3] > 0]
+        if len(lead):
+            print(f"GEMM{gi + 1} per issuing CTA: mma_total min {lead[:, 3].min():.0f} mean "
+                  f"{lead[:, 3].mean():.0f} max {lead[:, 3].max():.0f}; epi_total min "
+                  f"{b[:, 5].min():.0f} max {b[:, 5].max():.0f}; tiles {lead[:, 6].min():.0f}.."
+                  f"{lead[:, 6].max():.0f} ({len(lead)} issuers)")
+        ent, wt, ex = b[:, 8], b[:, 9], b[:, 10]
+        t0 = buf[0][:, 8].astype(np.float64).min()
+        print(f"GEMM{gi + 1} timeline (us from GEMM1's first CTA entry): entry {(ent.min() - t0) / 1e3:.1f}"
+              f"..{(ent.max() - t0) / 1e3:.1f}, past PDL wait {(wt.min() - t0) / 1e3:.1f}.."
+              f"{(wt.max() - t0) / 1e3:.1f}, exit {(ex.min() - t0) / 1e3:.1f}..{(ex.max() - t0) / 1e3:.1f}")
         tot = b[:, 3].mean()
         print(f"GEMM{gi + 1}: " + ", ".join(f"{n}={b[:, i].mean():.0f}" for i, n in enumerate(names))
               + f"  | mma waits epi {b[:, 1].mean() / tot:.1%} tma {b[:, 2].mean() / tot:.1%}")
