@@ -165,6 +165,8 @@ int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, int d, int h
  * then %globaltimer ns at entry, past the PDL wait, at exit).
  * out: uint64 [2 GEMMs][148 CTAs][12]. Synchronises the device. */
 int sida_debug_gemm_prof(unsigned long long* out);
+/* Observability: collect the counters above from now on (on = 1) or stop. */
+int sida_set_gemm_prof(int on);
 
 /* Expert-FFN tile family for sida_grouped_ffn_bf16: -1 auto, 0 token-M
  * tiles for both GEMMs (128/256 token rows x BN features), 1 token-N tiles

@@ -44,6 +44,7 @@ SIGNATURES = {
     "sida_grouped_ffn_bf16_fused": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _i, _vp, _sz, _i,
                                          _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]),
     "sida_debug_gemm_prof": (_i, [_vp]),
+    "sida_set_gemm_prof": (_i, [_i]),
     "sida_set_ffn_tiles": (_i, [_i]),
     "sida_get_ffn_tiles": (_i, []),
     "sida_grouped_ffn_f32": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -1513,16 +1513,24 @@ using namespace sida;
 
 static unsigned long long* g_prof = nullptr;  // [2 GEMMs][148 CTAs][kProfSlots]
 
+static int g_prof_on = -1;  // SIDA_GEMM_PROF=1 at load, or sida_set_gemm_prof
+
 static unsigned long long* prof_buffer(int gemm) {
-  static int enabled = -1;
-  if (enabled < 0) enabled = getenv("SIDA_GEMM_PROF") != nullptr;
-  if (!enabled) return nullptr;
+  if (g_prof_on < 0) g_prof_on = getenv("SIDA_GEMM_PROF") != nullptr;
+  if (!g_prof_on) return nullptr;
   if (!g_prof) {
     const size_t bytes = 2ull * kNumSMs * sm100::kProfSlots * sizeof(unsigned long long);
     if (cudaMalloc(&g_prof, bytes) != cudaSuccess) return nullptr;
     cudaMemset(g_prof, 0, bytes);
   }
   return g_prof + (size_t)gemm * kNumSMs * sm100::kProfSlots;
+}
+
+// Observability: turn the FFN GEMM profile counters on or off at run time.
+extern "C" int sida_set_gemm_prof(int on) {
+  g_prof_on = on ? 1 : 0;
+  if (on) SIDA_REQUIRE(prof_buffer(0), SIDA_ERR_CUDA, "profile buffer allocation failed");
+  return SIDA_OK;
 }
 
 // Observability: copy the per-CTA cycle counters of the last FFN call
