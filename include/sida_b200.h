@@ -143,22 +143,6 @@ int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, int h, cons
                           float* out, uint16_t* out_bf16, uint16_t* hidden, int32_t* err_flag,
                           void* stream);
 
-/* The same layer FFN as ONE persistent launch: GEMM1 and GEMM2 tiles
- * interleaved (GEMM2 tiles of m-tile mt run `lag` m-tiles after its GEMM1
- * tiles and wait on a per-m-tile release count in mflags), so the hidden rows
- * are consumed from L2 and the two launch tails become one. mflags: int32
- * workspace of sida_ffn_flags_count(n_rows, listed experts) entries (zeroed
- * by the call); d, h multiples of 256. Results identical to the two-launch
- * entry point (same tiles, same epilogues). */
-size_t sida_ffn_flags_count(int n_rows, int n_listed);
-int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, int d, int h,
-                                const int32_t* off, int num_experts, const int32_t* expert_slot,
-                                const int32_t* expert_list, int n_list, const void* arena,
-                                size_t slot_stride, int n_slots, const int32_t* row_map,
-                                const float* alpha, const float* resid, float* out,
-                                uint16_t* out_bf16, uint16_t* hidden, int32_t* err_flag,
-                                int32_t* mflags, int lag, void* stream);
-
 /* Observability: per-CTA cycle counters of the last sida_grouped_ffn_bf16
  * call when the process runs with SIDA_GEMM_PROF=1 (producer wait, MMA wait
  * on epilogue / on TMA, MMA loop, epilogue wait, epilogue loop, tiles, -,
@@ -172,8 +156,7 @@ int sida_set_gemm_prof(int on);
  * tiles for both GEMMs (128/256 token rows x BN features), 1 token-N tiles
  * for both (swap-AB: 256 features x 16..256 token rows in steps of 16),
  * 2 token-M GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2,
- * 4 both GEMMs fused per <= 128-row token tile with the bf16 hidden kept in
- * shared memory (d % 256 == 0, d <= 768; otherwise as 1), 5 both GEMMs in
+ * (4, a per-token-tile fused kernel, was retired: contract error), 5 both GEMMs in
  * ONE persistent launch with the hidden rows handed from GEMM1 to GEMM2
  * through L2 (token-N tiles of up to 320 rows, d % 256 == 0, h % 1024 == 0;
  * auto mode runs it for such shapes only with SIDA_XFFN=1).

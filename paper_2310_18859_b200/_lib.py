@@ -40,9 +40,6 @@ SIGNATURES = {
     "sida_slot_bytes": (_sz, [_i, _i]),
     "sida_grouped_ffn_bf16": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _i, _vp, _sz, _i, _vp, _vp,
                                    _vp, _vp, _vp, _vp, _vp, _vp]),
-    "sida_ffn_flags_count": (_sz, [_i, _i]),
-    "sida_grouped_ffn_bf16_fused": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _vp, _i, _vp, _sz, _i,
-                                         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _vp]),
     "sida_debug_gemm_prof": (_i, [_vp]),
     "sida_set_gemm_prof": (_i, [_i]),
     "sida_set_ffn_tiles": (_i, [_i]),

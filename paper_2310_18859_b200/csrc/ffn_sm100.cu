@@ -154,38 +154,11 @@ __device__ __forceinline__ TileInfo decode_tile(int t, int n_ntiles, const int32
   return decode_mt(mt, t - mt * n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
 }
 
-// Fused FFN tile order over MT m-tiles: step s issues the n1 GEMM1 tiles of
-// m-tile s, then the n2 GEMM2 tiles of m-tile s - lag, so every GEMM2 tile
-// comes after the GEMM1 tiles it reads (deadlock-free with in-order
-// persistent units) and the hidden rows in between (lag m-tiles) stay in L2.
-__device__ __forceinline__ void fused_order(int t, int MT, int n1, int n2, int lag, bool& g2,
-                                            int& mt, int& nt) {
-  const int a = min(lag, MT);
-  if (t < a * n1) {
-    g2 = false; mt = t / n1; nt = t - mt * n1;
-    return;
-  }
-  t -= a * n1;
-  const int nb = (MT - a) * (n1 + n2);
-  if (t < nb) {
-    const int s = t / (n1 + n2), r = t - s * (n1 + n2);
-    if (r < n1) { g2 = false; mt = a + s; nt = r; }
-    else { g2 = true; mt = a + s - lag; nt = r - n1; }
-    return;
-  }
-  t -= nb;
-  g2 = true; mt = MT - a + t / n2; nt = t - (t / n2) * n2;
-}
-
 template <int BN, int STAGE, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const GemmParams p, const __grid_constant__ CUtensorMap tmA2,
-                    const __grid_constant__ CUtensorMap tmB2, const GemmParams p2,
-                    int32_t* __restrict__ mflags, int lag) {
-  // STAGE 1: GEMM1 (bias+ReLU -> hidden), 2: GEMM2 (alpha, unpermute,
-  // residual), 3: both in one persistent launch (p: GEMM1, p2: GEMM2; GEMM2
-  // tiles of an m-tile wait on mflags[mt] = CG * (h / BN) GEMM1 tile releases)
+                    const GemmParams p) {
+  // STAGE 1: GEMM1 (bias+ReLU -> hidden), 2: GEMM2 (alpha, unpermute, residual)
   constexpr int TM = BM * CG;                    // rows per tile (per CTA pair)
   constexpr int BNL = BN / CG;                   // B rows this CTA loads
   constexpr uint32_t kABytes = BM * BK * 2;
@@ -259,10 +232,6 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
-    if (STAGE == 3) {
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA2)) : "memory");
-      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB2)) : "memory");
-    }
   }
   if (warp == 1) {
     if constexpr (CG == 1) {
@@ -288,38 +257,16 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 9] = gtime();
 
-  const int n_ntiles = p.ndim / BN;            // (STAGE 3: GEMM1 column tiles)
-  const int n2tiles = STAGE == 3 ? p2.ndim / BN : 0;
+  const int n_ntiles = p.ndim / BN;
   const int MT = s_prefix[n_list];
-  // STAGE 3 work items: per m-tile, n2tiles GEMM1 items of `sub` column tiles
-  // each (sub = n1 / n2: every item costs h/BK... = the same MMA work as one
-  // GEMM2 tile, so the static round-robin over items stays balanced) and
-  // n2tiles GEMM2 items of one tile
-  const int sub = STAGE == 3 ? n_ntiles / n2tiles : 1;
-  const int total = STAGE == 3 ? MT * 2 * n2tiles : MT * n_ntiles;
-  auto item_subs = [&](int it) -> int {
-    if constexpr (STAGE == 3) {
-      bool g2;
-      int mt, nt;
-      fused_order(it, MT, n2tiles, n2tiles, lag, g2, mt, nt);
-      return g2 ? 1 : sub;
-    }
-    return 1;
+  const int total = MT * n_ntiles;
+  auto item_subs = [&](int) -> int { return 1; };
+  // work item -> (GEMM2?, m-tile, tile info)
+  auto get_tile = [&](int it, int, bool& g2, int& mt) -> TileInfo {
+    g2 = STAGE == 2;
+    mt = it / n_ntiles;
+    return decode_mt(mt, it - mt * n_ntiles, s_prefix, s_expert, n_list, p, BN, TM);
   };
-  // (item, sub-tile) -> (GEMM2?, m-tile, tile info)
-  auto get_tile = [&](int it, int j, bool& g2, int& mt) -> TileInfo {
-    int nt;
-    if constexpr (STAGE == 3) {
-      fused_order(it, MT, n2tiles, n2tiles, lag, g2, mt, nt);
-      if (!g2) nt = nt * sub + j;
-    } else {
-      g2 = STAGE == 2;
-      mt = it / n_ntiles;
-      nt = it - mt * n_ntiles;
-    }
-    return decode_mt(mt, nt, s_prefix, s_expert, n_list, p, BN, TM);
-  };
-  const int flag_target = CG * n_ntiles;
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs): own 128 rows of A, own BN/CG rows of B
@@ -334,19 +281,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         int mt;
         const TileInfo ti = get_tile(it, j, g2, mt);
         if (ti.slot < 0) continue;
-        if (STAGE == 3 && g2) {
-          // the hidden rows of this m-tile: every GEMM1 column tile released
-          int v;
-          while (true) {
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(mflags + mt) : "memory");
-            if (v >= flag_target) break;
-            __nanosleep(64);
-          }
-          asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
-        const CUtensorMap* ta = (STAGE == 3 && g2) ? &tmA2 : &tmA;
-        const CUtensorMap* tb = (STAGE == 3 && g2) ? &tmB2 : &tmB;
-        const int nkb = ((STAGE == 3 && g2) ? p2.kdim : p.kdim) / BK;
+        const CUtensorMap* ta = &tmA;
+        const CUtensorMap* tb = &tmB;
+        const int nkb = p.kdim / BK;
         for (int kb = 0; kb < nkb; ++kb) {
           const unsigned long long c0 = p.prof ? clk() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
@@ -385,7 +322,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           atomicExch(p.err_flag, 1);
           continue;
         }
-        const int n_kblocks = ((STAGE == 3 && g2) ? p2.kdim : p.kdim) / BK;
+        const int n_kblocks = p.kdim / BK;
         const uint32_t idesc = ti.half ? idesc_half : idesc_full;
         ++n_tiles;
         const unsigned long long c0 = p.prof ? clk() : 0;
@@ -444,8 +381,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       int mt;
       const TileInfo ti = get_tile(it, j, g2, mt);
       if (ti.slot < 0) continue;
-      const bool st2 = STAGE == 2 || (STAGE == 3 && g2);
-      const GemmParams& gp = (STAGE == 3 && g2) ? p2 : p;
+      const bool st2 = STAGE == 2;
+      const GemmParams& gp = p;
       // first row of this warp's quarter. An M=128 pair tile's accumulator
       // (64 rows per CTA) sits in TMEM as two halves: N columns [0, BN/2) in
       // lanes 0-63 and [BN/2, BN) in lanes 64-127, each over BN/2 columns
@@ -600,15 +537,6 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         mbar_arrive_cluster(CG == 1 ? eb : map_rank(eb, 0));
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-      if (STAGE == 3 && !st2) {
-        // this CTA's rows of hidden tile (mt, nt) are stored: release them to
-        // the GEMM2 producers (stores -> CTA barrier -> gpu fence -> count)
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
-        if (warp == 2 && lane == 0) {
-          __threadfence();
-          atomicAdd(mflags + mt, 1);
-        }
-      }
     }
       }
     if (p.prof && warp == 2 && lane == 0) {
@@ -914,377 +842,6 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
   }
 }
 
-// ------------------------------------------------------------ fused FFN (token-N)
-// Both expert GEMMs of a token tile in one CTA pair, the hidden activations
-// never leaving the SMs. Work item = (expert, tile of <= 128 of its rows).
-// For every 256-wide slice c of h:
-//   GEMM1(c): acc1 (TMEM, 256 h-features x N tokens, M = 256 per pair) =
-//             W1^T[c] X^T over K = d (weights and token rows streamed by TMA)
-//   epi1(c):  relu(acc1 + b1) -> bf16, written by the epilogue warps straight
-//             into the SW128 K-major B-operand layout of GEMM2 in shared
-//             memory (token rows split between the two CTAs: half of every
-//             warp's stores go to the peer over DSMEM), double-buffered
-//   GEMM2(c): out (TMEM, d x N, d/256 accumulators) += W2^T[:, c] H[c]^T
-// MMA order G1(c), G2(c-1), G1(c+1), ...: epi1(c) overlaps G2(c-1), so the
-// single acc1 buffer never stalls the tensor core. After the last slice the
-// epilogue applies b2, alpha, the residual and the unpermute (row_map) as
-// the token-N GEMM2 epilogue does. HBM traffic = weights + x + residual +
-// outputs (no hidden round trip: 2 x N x h x 2 bytes per layer saved).
-// TMEM: d/256 accumulators of 128 columns + acc1 (128 columns) <= 512, so
-// d <= 768.
-constexpr int kFxTok = 128;                    // max tokens per item (UMMA N)
-constexpr int kFxStages = 6;
-constexpr uint32_t kFxW = 128 * BK * 2;        // weight slice per CTA per stage (16 KB)
-constexpr uint32_t kFxX = 64 * BK * 2;         // token slice per CTA per stage (8 KB)
-constexpr uint32_t kFxStage = kFxW + kFxX;
-constexpr uint32_t kFxHid = 4 * 64 * 128;      // hidden slice per CTA: 4 k-blocks x 64 rows
-
-__device__ __forceinline__ void fx_split(int R, int& base, int& count) {
-  if (R <= 0) { base = 16; count = 0; return; }
-  const int n = ceil_div(R, kFxTok);
-  base = min(kFxTok, (ceil_div(R, n) + 15) & ~15);
-  count = ceil_div(R, base);
-}
-
-struct FxParams {
-  int n_rows, d, h;
-  const int32_t* off;
-  int num_experts;
-  const int32_t* expert_slot;
-  const int32_t* expert_list;
-  int n_list;
-  const uint8_t* arena;
-  size_t slot_stride, b1_off, b2_off;
-  const int32_t* row_map;
-  const float* alpha;
-  const float* resid;
-  float* out;
-  uint16_t* out_bf16;
-  int32_t* err_flag;
-};
-
-__global__ void __launch_bounds__(kThreads, 1)
-fused_ffn_tn_kernel(const __grid_constant__ CUtensorMap tmW1,  // (d, h, slot), box 64x128
-                    const __grid_constant__ CUtensorMap tmW2,  // (h, d, slot), box 64x128
-                    const __grid_constant__ CUtensorMap tmX,   // (d, rows), box 64x64
-                    const FxParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sStage = smem;
-  uint8_t* sHid = smem + kFxStages * kFxStage;  // 2 buffers
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sHid + 2 * kFxHid);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + kFxStages;
-  uint64_t* acc1_full = bars + 2 * kFxStages;
-  uint64_t* acc1_empty = acc1_full + 1;
-  uint64_t* hid_full = acc1_empty + 1;   // [2]
-  uint64_t* hid_empty = hid_full + 2;    // [2]
-  uint64_t* out_full = hid_empty + 2;
-  uint64_t* out_empty = out_full + 1;
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(out_empty + 1);
-  int32_t* s_prefix = reinterpret_cast<int32_t*>(s_tmem + 4);
-  int32_t* s_expert = s_prefix + kMaxListed + 1;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_list = p.expert_list ? p.n_list : p.num_experts;
-  const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
-  const int unit = blockIdx.x >> 1, n_units = gridDim.x >> 1;
-  const int n_c = p.h / 256, n_dt = p.d / 256, n_kd = p.d / BK;
-
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int i = 0; i < n_list; ++i) {
-      const int e = p.expert_list ? p.expert_list[i] : i;
-      const int R = (p.off[e + 1] - p.off[e]);
-      int base, cnt;
-      fx_split(R, base, cnt);
-      s_expert[i] = e;
-      s_prefix[i] = acc;
-      acc += cnt;
-    }
-    s_prefix[n_list] = acc;
-    for (int i = 0; i < kFxStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    mbar_init(acc1_full, 1);
-    mbar_init(acc1_empty, 2 * kEpiWarps);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&hid_full[i], 2 * kEpiWarps);
-      mbar_init(&hid_empty[i], 1);
-    }
-    mbar_init(out_full, 1);
-    mbar_init(out_empty, 2 * kEpiWarps);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW1)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmW2)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(s_tmem)),
-                 "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *s_tmem;
-  const uint32_t acc1_col = 384;  // out accumulators at columns 0, 128, 256
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-
-  const int total = s_prefix[n_list];
-  auto get_item = [&](int it, int& row0, int& nrows, int& slot) {
-    int lo = 0, hi = n_list - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (s_prefix[mid] <= it) lo = mid; else hi = mid - 1;
-    }
-    const int e = s_expert[lo];
-    const int seg0 = p.off[e];
-    const int R = p.off[e + 1] - seg0;
-    int base, cnt;
-    fx_split(R, base, cnt);
-    const int j = it - s_prefix[lo];
-    row0 = seg0 + j * base;
-    nrows = min(base, R - j * base);
-    slot = p.expert_slot[e];
-  };
-
-  if (warp == 0) {
-    // ===== TMA producer (both CTAs)
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      auto next_stage = [&]() {
-        if (++stage == kFxStages) { stage = 0; phase ^= 1; }
-      };
-      for (int it = unit; it < total; it += n_units) {
-        int row0, nrows, slot;
-        get_item(it, row0, nrows, slot);
-        if (slot < 0) continue;
-        const int half = ((nrows + 15) & ~15) >> 1;
-        const int xrow = row0 + static_cast<int>(rank) * half;
-        for (int c = 0; c <= n_c; ++c) {
-          if (c < n_c) {  // GEMM1(c): W1^T rows c*256 + rank*128, token rows
-            for (int kb = 0; kb < n_kd; ++kb) {
-              mbar_wait(&empty[stage], phase ^ 1);
-              const uint32_t fb = map_rank(smem_u32(&full[stage]), 0);
-              if (leader) mbar_expect_tx(&full[stage], 2 * kFxStage);
-              uint8_t* st = sStage + stage * kFxStage;
-              tma_load_3d<2>(st, &tmW1, kb * BK, c * 256 + rank * 128, slot, fb);
-              tma_load_2d<2>(st + kFxW, &tmX, kb * BK, xrow, fb);
-              next_stage();
-            }
-          }
-          if (c > 0) {  // GEMM2(c-1): W2^T rows mt*256 + rank*128, h cols (c-1)*256 + kb*64
-            for (int mt = 0; mt < n_dt; ++mt)
-              for (int kb = 0; kb < 4; ++kb) {
-                mbar_wait(&empty[stage], phase ^ 1);
-                const uint32_t fb = map_rank(smem_u32(&full[stage]), 0);
-                if (leader) mbar_expect_tx(&full[stage], 2 * kFxW);
-                tma_load_3d<2>(sStage + stage * kFxStage, &tmW2, (c - 1) * 256 + kb * BK,
-                               mt * 256 + rank * 128, slot, fb);
-                next_stage();
-              }
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    // ===== MMA issuer (leader CTA, one lane)
-    if (lane == 0 && leader) {
-      int stage = 0;
-      uint32_t phase = 0;
-      uint32_t u_acc1 = 0, u_hid[2] = {0, 0}, u_out = 0;
-      for (int it = unit; it < total; it += n_units) {
-        int row0, nrows, slot;
-        get_item(it, row0, nrows, slot);
-        if (slot < 0) {
-          atomicExch(p.err_flag, 1);
-          continue;
-        }
-        const uint32_t idesc = idesc_bf16_rt(256, (nrows + 15) & ~15);
-        for (int c = 0; c <= n_c; ++c) {
-          if (c < n_c) {
-            mbar_wait_cluster(acc1_empty, (u_acc1 & 1) ^ 1);
-            ++u_acc1;
-            tc_fence_after();
-            for (int kb = 0; kb < n_kd; ++kb) {
-              mbar_wait(&full[stage], phase);
-              tc_fence_after();
-              const uint32_t a0 = smem_u32(sStage + stage * kFxStage);
-              const uint32_t b0 = a0 + kFxW;
-#pragma unroll
-              for (int k = 0; k < BK / UMMA_K; ++k)
-                umma_bf16<2>(tmem_base + acc1_col, sw128_desc(a0 + k * UMMA_K * 2),
-                             sw128_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0);
-              tc_commit<2>(&empty[stage]);
-              if (++stage == kFxStages) { stage = 0; phase ^= 1; }
-            }
-            tc_commit<2>(acc1_full);
-          }
-          if (c > 0) {
-            const int cc = c - 1, buf = cc & 1;
-            mbar_wait_cluster(&hid_full[buf], u_hid[buf] & 1);
-            ++u_hid[buf];
-            if (cc == 0) {
-              mbar_wait_cluster(out_empty, (u_out & 1) ^ 1);
-              ++u_out;
-            }
-            tc_fence_after();
-            const uint32_t hb = smem_u32(sHid + buf * kFxHid);
-            for (int mt = 0; mt < n_dt; ++mt)
-              for (int kb = 0; kb < 4; ++kb) {
-                mbar_wait(&full[stage], phase);
-                tc_fence_after();
-                const uint32_t a0 = smem_u32(sStage + stage * kFxStage);
-#pragma unroll
-                for (int k = 0; k < BK / UMMA_K; ++k)
-                  umma_bf16<2>(tmem_base + mt * 128, sw128_desc(a0 + k * UMMA_K * 2),
-                               sw128_desc(hb + kb * 8192 + k * UMMA_K * 2), idesc,
-                               (cc | kb | k) != 0);
-                tc_commit<2>(&empty[stage]);
-                if (++stage == kFxStages) { stage = 0; phase ^= 1; }
-              }
-            tc_commit<2>(&hid_empty[buf]);
-          }
-        }
-        tc_commit<2>(out_full);
-      }
-    }
-  } else {
-    // ===== epilogue warps (both CTAs): quarter q = TMEM lanes 32q.., half hh
-    // = token columns [64 hh, 64 hh + 64)
-    const int q = warp & 3;
-    const int hh = (warp - 2) >> 2;
-    const bool odd = lane & 1;
-    uint32_t u_acc1 = 0, u_hid[2] = {0, 0}, u_out = 0;
-    for (int it = unit; it < total; it += n_units) {
-      int row0, nrows, slot;
-      get_item(it, row0, nrows, slot);
-      if (slot < 0) continue;
-      const int nmma = (nrows + 15) & ~15;
-      const int half = nmma >> 1;
-      const int nch = ceil_div(nmma, 32);
-      const uint8_t* sbase = p.arena + static_cast<size_t>(slot) * p.slot_stride;
-      const uint16_t* b1 = reinterpret_cast<const uint16_t*>(sbase + p.b1_off);
-      const uint16_t* b2 = reinterpret_cast<const uint16_t*>(sbase + p.b2_off);
-      const int f_loc = static_cast<int>(rank) * 128 + q * 32 + lane;  // within a 256 slice
-      const int kb2 = f_loc >> 6;
-      const int fin = f_loc & 63;
-      for (int c = 0; c < n_c; ++c) {
-        const int buf = c & 1;
-        const float bias = bf16_to_f32(b1[c * 256 + f_loc]);
-        mbar_wait(acc1_full, u_acc1 & 1);
-        ++u_acc1;
-        tc_fence_after();
-        uint32_t v[2][32];
-        const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc1_col;
-        const int c0 = hh * 2;
-        if (c0 < nch) tmem_ld32_nowait(t_lane + c0 * 32, v[0]);
-        if (c0 + 1 < nch) tmem_ld32_nowait(t_lane + (c0 + 1) * 32, v[1]);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        // TMEM reads are ordered by the tcgen05 fence: a plain arrive (a
-        // .release.cluster one would first drain this warp's pending stores)
-        if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(acc1_empty), 0));
-        // hidden buffer `buf` free (GEMM2(c-2) done reading it)
-        mbar_wait(&hid_empty[buf], (u_hid[buf] & 1) ^ 1);
-        ++u_hid[buf];
-        const uint32_t hbuf = smem_u32(sHid + buf * kFxHid) + kb2 * 8192;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          if (c0 + i >= nch) break;
-#pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float y0 = fmaxf(__uint_as_float(v[i][j]) + bias, 0.f);
-            const float y1 = fmaxf(__uint_as_float(v[i][j + 1]) + bias, 0.f);
-            const float other = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
-            const uint32_t w = odd ? bf16x2_rn(other, y1) : bf16x2_rn(y0, other);
-            const int tcol = (c0 + i) * 32 + j + (odd ? 1 : 0);
-            if (tcol < nmma) {
-              const int dst = tcol >= half ? 1 : 0;
-              const int r = tcol - dst * half;
-              const int fe = fin & ~1;
-              const uint32_t a = hbuf + r * 128 + ((((fe >> 3) ^ (r & 7))) << 4) + (fe & 7) * 2;
-              asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(map_rank(a, dst)), "r"(w)
-                           : "memory");
-            }
-          }
-        }
-        // the DSMEM stores -> the tensor core's (async proxy) reads of both CTAs
-        asm volatile("fence.proxy.async.shared::cluster;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(&hid_full[buf]), 0));
-      }
-      // ---- output: alpha (acc + b2) + resid, unpermuted (as the token-N GEMM2)
-      mbar_wait(out_full, u_out & 1);
-      ++u_out;
-      tc_fence_after();
-      const int nv = ceil_div(nrows, 32);
-      for (int mt = 0; mt < n_dt; ++mt) {
-        const int f = mt * 256 + static_cast<int>(rank) * 128 + q * 32 + lane;
-        const float bias = bf16_to_f32(b2[f]);
-        for (int ch = hh; ch < nv; ch += 2) {
-          uint32_t v[32];
-          tmem_ld32_nowait(tmem_base + (static_cast<uint32_t>(q * 32) << 16) + mt * 128 + ch * 32,
-                           v);
-          const int tok0 = row0 + ch * 32;
-          const int cnt = min(32, nrows - ch * 32);
-          const int my_tok = tok0 + lane;
-          int orow_l = my_tok;
-          float a_l = 1.f;
-          if (lane < cnt) {
-            if (p.row_map) orow_l = p.row_map[my_tok];
-            if (p.alpha) a_l = p.alpha[my_tok];
-          }
-          float x[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int o = __shfl_sync(0xffffffffu, orow_l, j);
-            x[j] = (p.resid && j < cnt) ? __ldg(p.resid + static_cast<size_t>(o) * p.d + f) : 0.f;
-          }
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int o = __shfl_sync(0xffffffffu, orow_l, j);
-            const float a = __shfl_sync(0xffffffffu, a_l, j);
-            if (j < cnt) {
-              const float y = x[j] + (__uint_as_float(v[j]) + bias) * a;
-              const size_t at = static_cast<size_t>(o) * p.d + f;
-              if (p.out) p.out[at] = y;
-              if (p.out_bf16) p.out_bf16[at] = __bfloat16_as_ushort(__float2bfloat16_rn(y));
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(out_empty), 0));
-    }
-  }
-
-  tc_fence_before();
-  cluster_sync();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(512));
-  }
-}
-
-constexpr size_t fx_smem_bytes() {
-  return 1024 + kFxStages * kFxStage + 2 * kFxHid + (2 * kFxStages + 8) * 8 + 16 +
-         (2 * kMaxListed + 2) * 4;
-}
-
 constexpr size_t tn_smem_bytes() {
   return 1024 + kTnStages * (128 * BK * 2 + (kTnMax / 2) * BK * 2) + (2 * kTnStages + 4) * 8 + 16 +
          (2 * kMaxListed + 2) * 4;
@@ -1354,9 +911,7 @@ static int pdl_enabled() {
 
 template <int BN, int STAGE, int CG>
 static int launch_gemm(const void* a_base, const void* b_base, int n_slots, const GemmParams& p,
-                       int n_listed, cudaStream_t s, const void* a2_base = nullptr,
-                       const void* b2_base = nullptr, const GemmParams* p2 = nullptr,
-                       int32_t* mflags = nullptr, int lag = 0) {
+                       int n_listed, cudaStream_t s) {
   auto kern = grouped_gemm_kernel<BN, STAGE, CG>;
   static bool configured = false;
   if (!configured) {
@@ -1364,21 +919,12 @@ static int launch_gemm(const void* a_base, const void* b_base, int n_slots, cons
                                    (int)smem_bytes<BN, STAGE, CG>()));
     configured = true;
   }
-  CUtensorMap ta, tb, ta2, tb2;
+  CUtensorMap ta, tb;
   int st = make_map_2d(&ta, a_base, p.kdim, p.n_rows, BM);
   if (st) return st;
   st = make_map_3d(&tb, b_base, p.kdim, p.ndim, n_slots, p.slot_stride, BN / CG);
   if (st) return st;
-  const GemmParams& q2 = p2 ? *p2 : p;
-  if (STAGE == 3) {
-    if ((st = make_map_2d(&ta2, a2_base, q2.kdim, q2.n_rows, BM))) return st;
-    if ((st = make_map_3d(&tb2, b2_base, q2.kdim, q2.ndim, n_slots, q2.slot_stride, BN / CG)))
-      return st;
-  } else {
-    ta2 = ta;
-    tb2 = tb;
-  }
-  const int col_tiles = p.ndim / BN + (STAGE == 3 ? q2.ndim / BN : 0);
+  const int col_tiles = p.ndim / BN;
   const int max_tiles = (ceil_div(p.n_rows, BM * CG) + n_listed) * col_tiles;
   const int units = std::max(1, std::min(max_tiles, kNumSMs / CG));
   cudaLaunchConfig_t cfg{};
@@ -1395,7 +941,7 @@ static int launch_gemm(const void* a_base, const void* b_base, int n_slots, cons
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p, ta2, tb2, q2, mflags, lag));
+  SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   count_launch();
   return SIDA_OK;
 }
@@ -1457,43 +1003,6 @@ static int launch_tn(const void* x_base, const void* w_base, int n_slots, const 
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   SIDA_CUDA(cudaLaunchKernelEx(&cfg, kern, tw, tx, p));
-  count_launch();
-  return SIDA_OK;
-}
-
-// Fused token-N FFN launch (both GEMMs, hidden kept on chip).
-static int launch_fx(const void* x_perm, const uint8_t* arena, int n_slots, const FxParams& p,
-                     int n_listed, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    SIDA_CUDA(cudaFuncSetAttribute(fused_ffn_tn_kernel,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)fx_smem_bytes()));
-    configured = true;
-  }
-  const size_t w2_off = (size_t)p.h * p.d * 2;
-  CUtensorMap tw1, tw2, tx;
-  int st = make_map_3d(&tw1, arena, p.d, p.h, n_slots, p.slot_stride, 128);
-  if (st) return st;
-  if ((st = make_map_3d(&tw2, arena + w2_off, p.h, p.d, n_slots, p.slot_stride, 128))) return st;
-  if ((st = make_map_2d(&tx, x_perm, p.d, p.n_rows, 64))) return st;
-  const int max_items = ceil_div(p.n_rows, kFxTok) + n_listed;
-  const int units = std::max(1, std::min(max_items, kNumSMs / 2));
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(units * 2);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = fx_smem_bytes();
-  cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled();
-  cfg.attrs = attr;
-  cfg.numAttrs = 2;
-  SIDA_CUDA(cudaLaunchKernelEx(&cfg, fused_ffn_tn_kernel, tw1, tw2, tx, p));
   count_launch();
   return SIDA_OK;
 }
@@ -1566,7 +1075,8 @@ static int choose_cg(int gemm, int n_rows, int listed) {
 
 // Tile family per expert GEMM (sida_set_ffn_tiles, or SIDA_FFN_SWAP at load):
 // -1 auto, 0 token-M for both GEMMs, 1 token-N (swap-AB) for both, 2 token-M
-// GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2, 4 fused. Auto is
+// GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2, 5 the one-launch
+// FFN of expert_ffn.cu (4, a per-token-tile fused kernel, was retired). Auto is
 // token-M with the per-GEMM CTA-group choice above, which measured fastest
 // everywhere (profiles/r1/ffn_tile_families.txt); token-N is used in auto
 // mode only inside [SIDA_FFN_SWAP_LO, SIDA_FFN_SWAP_HI) rows per expert for
@@ -1590,21 +1100,15 @@ static bool choose_tn(int gemm, int n_rows, int listed, int d, int h) {
     case 1: return true;
     case 2: return gemm == 2;
     case 3: return gemm == 1;
-    case 4: return true;  // (when the fused launch does not apply)
     default: break;
   }
   return gemm == 2 && n_rows >= g_tn_lo * listed && n_rows < g_tn_hi * listed;
 }
 
-// Mode 4: both GEMMs fused per token tile (fused_ffn_tn_kernel), d <= 768.
-static bool choose_fx(int n_rows, int listed, int d, int h) {
-  tn_init();
-  (void)n_rows; (void)listed;
-  return g_tn_mode == 4 && d % 256 == 0 && d <= 768 && h % 256 == 0;
-}
-
 extern "C" int sida_set_ffn_tiles(int mode) {
-  SIDA_REQUIRE(mode >= -1 && mode <= 5, SIDA_ERR_CONTRACT, "ffn tile mode %d not in -1..5", mode);
+  SIDA_REQUIRE(mode >= -1 && mode <= 5 && mode != 4, SIDA_ERR_CONTRACT,
+               "ffn tile mode %d not in -1..3, 5 (4, the per-token-tile fused FFN, was retired)",
+               mode);
   tn_init();
   g_tn_mode = mode;
   return SIDA_OK;
@@ -1667,17 +1171,6 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
     return sida_expert_ffn_launch(x_perm, n_rows, d, h, off, num_experts, expert_slot,
                                   expert_list, n_list, arena, slot_stride, n_slots, row_map,
                                   alpha, resid, out, out_bf16, hidden, err_flag, stream);
-  if (choose_fx(n_rows, listed, d, h)) {
-    sm100::FxParams f{};
-    f.n_rows = n_rows; f.d = d; f.h = h;
-    f.off = off; f.num_experts = num_experts; f.expert_slot = expert_slot;
-    f.expert_list = expert_list; f.n_list = n_list;
-    f.arena = ar; f.slot_stride = slot_stride; f.b1_off = b1_off; f.b2_off = b2_off;
-    f.row_map = row_map; f.alpha = alpha; f.resid = resid; f.out = out; f.out_bf16 = out_bf16;
-    f.err_flag = err_flag;
-    return sm100::launch_fx(x_perm, ar, n_slots, f, listed, s);
-  }
-
   sm100::GemmParams p1{};
   p1.n_rows = n_rows; p1.kdim = d; p1.ndim = h;
   p1.off = off; p1.num_experts = num_experts; p1.expert_slot = expert_slot;
@@ -1776,58 +1269,6 @@ extern "C" int sida_linear_bf16(const uint16_t* x, int n_rows, int k, int n, con
   p.bias_off = static_cast<size_t>(n) * k * 2;
   p.hidden = out; p.err_flag = err_flag; p.linear = 1;
   return sm100::dispatch_gemm<1>(x, w_t, 1, p, 1, n_rows >= 1024 ? 2 : 1, as_stream(stream));
-}
-
-// Both expert GEMMs of one layer in ONE persistent launch (STAGE 3): GEMM1
-// and GEMM2 tiles interleaved with a lag of `lag` m-tiles, GEMM2 tiles of an
-// m-tile gated on mflags[mt] (zeroed here) so the bf16 hidden rows are
-// consumed while still in L2 and the two launch tails become one.
-extern "C" size_t sida_ffn_flags_count(int n_rows, int n_listed) {
-  return static_cast<size_t>(ceil_div(n_rows, sm100::BM) + n_listed);
-}
-
-extern "C" int sida_grouped_ffn_bf16_fused(const uint16_t* x_perm, int n_rows, int d, int h,
-                                           const int32_t* off, int num_experts,
-                                           const int32_t* expert_slot, const int32_t* expert_list,
-                                           int n_list, const void* arena, size_t slot_stride,
-                                           int n_slots, const int32_t* row_map,
-                                           const float* alpha, const float* resid, float* out,
-                                           uint16_t* out_bf16, uint16_t* hidden,
-                                           int32_t* err_flag, int32_t* mflags, int lag,
-                                           void* stream) {
-  SIDA_REQUIRE(d % 256 == 0 && h % 256 == 0, SIDA_ERR_UNSUPPORTED,
-               "fused FFN needs d, h multiples of 256 (d=%d h=%d)", d, h);
-  SIDA_REQUIRE(n_rows >= 0 && num_experts >= 1 && n_slots >= 1 && lag >= 1, SIDA_ERR_CONTRACT,
-               "bad ffn dims rows=%d K=%d slots=%d lag=%d", n_rows, num_experts, n_slots, lag);
-  const int listed = expert_list ? n_list : num_experts;
-  SIDA_REQUIRE(listed <= sm100::kMaxListed, SIDA_ERR_UNSUPPORTED, "more than %d experts listed",
-               sm100::kMaxListed);
-  SIDA_REQUIRE(slot_stride % 16 == 0 && slot_stride >= sida_slot_bytes(d, h), SIDA_ERR_CONTRACT,
-               "slot stride %zu invalid", slot_stride);
-  SIDA_REQUIRE(err_flag && mflags && (out || out_bf16) && hidden && x_perm && off && expert_slot &&
-                   arena,
-               SIDA_ERR_CONTRACT, "null pointer passed to sida_grouped_ffn_bf16_fused");
-  if (n_rows == 0 || listed == 0) return SIDA_OK;
-  cudaStream_t s = as_stream(stream);
-  SIDA_CUDA(cudaMemsetAsync(mflags, 0, sida_ffn_flags_count(n_rows, listed) * sizeof(int32_t), s));
-  const int cg = choose_cg(1, n_rows, listed);  // one tile shape for both interleaved GEMMs
-  const uint8_t* ar = static_cast<const uint8_t*>(arena);
-  const size_t w2_off = (size_t)h * d * 2, b1_off = 2 * w2_off, b2_off = b1_off + (size_t)h * 2;
-  sm100::GemmParams p1{};
-  p1.n_rows = n_rows; p1.kdim = d; p1.ndim = h;
-  p1.off = off; p1.num_experts = num_experts; p1.expert_slot = expert_slot;
-  p1.expert_list = expert_list; p1.n_list = n_list;
-  p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
-  p1.hidden = hidden; p1.err_flag = err_flag;
-  sm100::GemmParams p2 = p1;
-  p2.kdim = h; p2.ndim = d; p2.bias_off = b2_off;
-  p2.row_map = row_map; p2.alpha = alpha; p2.resid = resid; p2.out = out;
-  p2.out_bf16 = out_bf16;
-  if (cg == 2)
-    return sm100::launch_gemm<256, 3, 2>(x_perm, ar, n_slots, p1, listed, s, hidden, ar + w2_off,
-                                         &p2, mflags, lag);
-  return sm100::launch_gemm<256, 3, 1>(x_perm, ar, n_slots, p1, listed, s, hidden, ar + w2_off,
-                                       &p2, mflags, lag);
 }
 
 // ---------------------------------------------------------------------------

@@ -21,7 +21,6 @@ bf16, sida_slot_bytes(d, h) bytes) streamed into HBM slots by
 from __future__ import annotations
 
 import math
-import os
 import time
 from dataclasses import dataclass
 
@@ -32,12 +31,6 @@ from . import _lib
 from .errors import ContractError
 
 
-# SIDA_FFN_FUSED=1: the two expert GEMMs as one interleaved persistent launch
-# (sida_grouped_ffn_bf16_fused) instead of two; measured slower (base-8 0.316
-# vs 0.293 ms, base-128 0.553 vs 0.461 ms), so off by default. SIDA_FFN_LAG:
-# GEMM2 lag in m-tiles.
-_FFN_FUSED = os.environ.get("SIDA_FFN_FUSED", "0") == "1"
-_FFN_LAG = int(os.environ.get("SIDA_FFN_LAG", "32"))
 # longest sequence the fused attention core serves (csrc/attention.cu)
 MAX_ATTN_TOKENS = 512
 
@@ -595,13 +588,7 @@ class MoEModel:
                 arena.base_ptr, arena.slot_stride, arena.n_slots, perm.data_ptr(),
                 alpha_perm.data_ptr(), _lib.ptr(resid), target.data_ptr(),
                 _lib.ptr(out_bf16 if k == 1 else None), hidden.data_ptr(), err.data_ptr())
-        if _FFN_FUSED and c.d_model % 256 == 0 and c.expert_hidden % 256 == 0:
-            listed = n_list if expert_list is not None else c.num_experts
-            flags = torch.empty(int(h.sida_ffn_flags_count(rows, listed)), dtype=torch.int32,
-                                device=self.device)
-            _lib.check(h.sida_grouped_ffn_bf16_fused(*args, flags.data_ptr(), _FFN_LAG, sh))
-        else:
-            _lib.check(h.sida_grouped_ffn_bf16(*args, sh))
+        _lib.check(h.sida_grouped_ffn_bf16(*args, sh))
         return target
 
     def combine(self, y: torch.Tensor, x: torch.Tensor, k: int, out: torch.Tensor | None = None,
