@@ -148,8 +148,11 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
   // let the output projection (launched with programmatic serialization)
-  // start its prologue while this grid drains
+  // start its prologue while this grid drains; this grid is itself launched
+  // that way behind the QKV GEMM, so everything above overlapped that GEMM's
+  // tail and qkv is read only after it has completed
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == 0) {
     // ===== TMA producer: 12 (Q, K) k-blocks, then d/NC V chunks, one ring
@@ -367,8 +370,18 @@ static int launch_core(const CUtensorMap& tm, const int32_t* seq_off, int n_seq,
                                    (int)Cfg<NKEY, NCT>::kSmem));
     configured = true;
   }
-  attn_core_kernel<NKEY, NCT><<<dim3(n_seq, nq), kThreads, Cfg<NKEY, NCT>::kSmem, s>>>(
-      tm, seq_off, d, scale_log2e, ctx);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(n_seq, nq);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg<NKEY, NCT>::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SIDA_CUDA(cudaLaunchKernelEx(&cfg, attn_core_kernel<NKEY, NCT>, tm, seq_off, d, scale_log2e,
+                               ctx));
   SIDA_LAUNCH_CHECK();
   return SIDA_OK;
 }

@@ -460,7 +460,7 @@ expert_ffn_kernel(const __grid_constant__ CUtensorMap tmW1,  // (d, h, slot) box
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(&chunk_empty[ch]), 0));
           };
-          if (p.diag == 1) {
+          if (p.diag == 1 || (p.diag == 2 && g2) || (p.diag == 3 && !g2)) {
             tmem_wait_ld();
             release();
           } else if (!g2) {
