@@ -138,11 +138,14 @@ def _fast_params(d, h, K, seed):
     return p
 
 
-@pytest.mark.parametrize("K,N,skew", [(128, 32768, False), (256, 20000, True)])
+@pytest.mark.parametrize("K,N,skew", [(128, 32768, False), (256, 20000, True), (64, 20000, True)])
 def test_grouped_ffn_north_star_shapes_vs_oracle(cuda_device, K, N, skew):
     """Base-128 at 32K tokens (balanced ids, SURVEY §8(d) seed 3) and base-256
     at 20K tokens with Zipf-skewed ids (empty and one-row experts) through
-    the production FFN launch against the oracle's contraction."""
+    the production FFN launch against the oracle's contraction; base-64 at
+    20K skewed runs CTA-pair tiles (312 rows per expert on average) with
+    experts of every size: whole 256-row pair tiles, M=128 remainder pair
+    tiles, one-row and empty experts."""
     from paper_2310_18859_b200 import MoEConfig, MoEModel
     from paper_2310_18859_b200.offload import ExpertStore
     from paper_2310_18859_b200.predictor import ExpertHashTable
