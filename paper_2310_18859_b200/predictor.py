@@ -163,6 +163,25 @@ class TableSlot:
             self.bufs[name] = buf
         return buf[:n].view(shape)
 
+    def upload_tokens(self, toks: np.ndarray, stream) -> torch.Tensor:
+        """Host token ids -> this slot's device token buffer through the slot's
+        own pinned staging buffer (no pinned allocation per batch; the host
+        rewrites it only after the previous copy out of it has completed)."""
+        n = toks.size
+        st = getattr(self, "_stage", None)
+        if st is None or st.numel() < n:
+            st = torch.empty(max(n, 1), dtype=torch.int32, pin_memory=True)
+            self._stage, self._stage_ev = st, None
+        if self._stage_ev is not None:
+            self._stage_ev.synchronize()
+        st[:n].numpy()[:] = toks
+        dev = self.get("tokens", (n,), torch.int32)
+        with torch.cuda.stream(stream):
+            dev.copy_(st[:n], non_blocking=True)
+            self._stage_ev = torch.cuda.Event()
+            self._stage_ev.record(stream)
+        return dev
+
 
 class DeviceTableRing:
     """The device-resident form of the hash-table queue (ref pipeline.py:53-84
@@ -187,6 +206,16 @@ class DeviceTableRing:
         # table). Non-strict (an engine's own ring): a full ring or an
         # out-of-order id builds the table in fresh allocations instead.
         self.strict = strict
+
+    def restart(self) -> None:
+        """Start a new stream of batch ids (a new serve_sida call on a ring kept
+        warm across calls). Tables a previous call left unconsumed (it raised)
+        are abandoned once the device is idle."""
+        if any(s.busy for s in self.slots):
+            torch.cuda.synchronize(self.slots[0].device)
+            for s in self.slots:
+                s.busy = False
+        self._last_id = None
 
     def produce(self, predictor, model, lengths, eval_top_k: int, stream, batch_id: int,
                 tokens_dev=None, batch=None, host_ids: bool = False):
@@ -216,9 +245,7 @@ class DeviceTableRing:
             if slot.consumed is not None:
                 stream.wait_event(slot.consumed)
             if tokens_dev is None:
-                toks = model.validate_tokens(batch)
-                tokens_dev = slot.get("tokens", (toks.size,), torch.int32)
-                tokens_dev.copy_(torch.from_numpy(toks).pin_memory(), non_blocking=True)
+                tokens_dev = slot.upload_tokens(model.validate_tokens(batch), stream)
             table = hash_device(predictor, model, tokens_dev, list(lengths), eval_top_k,
                                 batch_id, stream, slot=slot)
             if host_ids:
