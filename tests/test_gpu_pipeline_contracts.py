@@ -143,3 +143,31 @@ def test_report_json_and_csv_from_a_run(cuda_device, tmp_path):
     assert len(data["batches"]) == 4
     assert data["aggregate"]["throughput_samples_per_s"] > 0
     assert data["aggregate"]["hash_hit_rate"] == 1.0
+
+
+def test_engine_ring_reused_across_calls_and_after_a_failed_call(cuda_device):
+    """serve_sida keeps its device table ring (and pinned token staging) with
+    the engine: repeated calls over the same batches give identical logits,
+    and a call that raises mid-stream (a token outside the vocabulary in its
+    third batch) leaves the engine serving correctly afterwards."""
+    from paper_2310_18859_b200 import (ContractError, MemoryBudget, PredictorConfig,
+                                       PredictorNet, Rng, SequenceBatch, serve_sida)
+    from paper_2310_18859_b200.engine import SidaEngine
+
+    model = make_model()
+    pred = PredictorNet(PredictorConfig(), BASE["d_model"], BASE["num_layers"],
+                        BASE["num_experts"], Rng(1))
+    budget = MemoryBudget(3 * model.expert_bytes_each())
+    eng = SidaEngine(model, pred, budget)
+    batches = make_stream(model, 5)
+    runs = [serve_sida(model, pred, batches, budget, engine=eng, compute_hit_rate=False)
+            for _ in range(2)]
+    assert eng._serve_ring is not None
+    bad = list(batches)
+    bad[2] = SequenceBatch(2, [np.array([0, BASE["vocab_size"]])])
+    with pytest.raises(ContractError):
+        serve_sida(model, pred, bad, budget, engine=eng, compute_hit_rate=False)
+    runs.append(serve_sida(model, pred, batches, budget, engine=eng, compute_hit_rate=False))
+    for r in runs[1:]:
+        for a, b in zip(runs[0].logits, r.logits):
+            assert np.array_equal(a, b)
