@@ -269,8 +269,9 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   };
 
   if (warp == 0) {
-    // ===== TMA producer (both CTAs): own 128 rows of A, own BN/CG rows of B
-    if (lane == 0) {
+    // ===== TMA producer (both CTAs): own 128 rows of A, own BN/CG rows of B;
+    // the warp walks the schedule in lockstep, one elected lane issues
+    {
       int stage = 0;
       uint32_t phase = 0;
       unsigned long long w_empty = 0;
@@ -289,21 +290,26 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           mbar_wait(&empty[stage], phase ^ 1);
           if (p.prof) w_empty += clk() - c0;
           const uint32_t fb = CG == 1 ? smem_u32(&full[stage]) : map_rank(smem_u32(&full[stage]), 0);
-          if (leader) mbar_expect_tx(&full[stage], CG * (kABytes + kBBytes));
-          // (an M=128 pair tile takes rows [64 r, 64 r + 64) of CTA r: the first
-          // half of its 128-row box)
-          tma_load_2d<CG>(sA + stage * kABytes, ta, kb * BK, ti.row0 + rank * (ti.half ? BM / 2 : BM),
-                          fb);
-          tma_load_3d<CG>(sB + stage * kBBytes, tb, kb * BK, ti.ncol0 + rank * BNL, ti.slot, fb);
+          if (elect_one()) {
+            if (leader) mbar_expect_tx(&full[stage], CG * (kABytes + kBBytes));
+            // (an M=128 pair tile takes rows [64 r, 64 r + 64) of CTA r: the
+            // first half of its 128-row box)
+            tma_load_2d<CG>(sA + stage * kABytes, ta, kb * BK,
+                            ti.row0 + rank * (ti.half ? BM / 2 : BM), fb);
+            tma_load_3d<CG>(sB + stage * kBBytes, tb, kb * BK, ti.ncol0 + rank * BNL, ti.slot, fb);
+          }
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
       }
-      if (p.prof) p.prof[blockIdx.x * kProfSlots + 0] = w_empty;
+      if (p.prof && lane == 0) p.prof[blockIdx.x * kProfSlots + 0] = w_empty;
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (single thread of the leader CTA)
-    if (lane == 0 && leader) {
+    // ===== MMA issuer: the whole warp walks the schedule in lockstep (the
+    // descriptors stay warp-uniform, in uniform registers), one elected lane
+    // issues the MMAs and the commits (leader CTA)
+    if (leader) {
       constexpr uint32_t idesc_full = idesc_bf16<TM, BN>();
       constexpr uint32_t idesc_half = idesc_bf16<(TM > BM ? TM / 2 : TM), BN>();
       int stage = 0;
@@ -319,7 +325,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
         int mt;
         const TileInfo ti = get_tile(it, j, g2, mt);
         if (ti.slot < 0) {
-          atomicExch(p.err_flag, 1);
+          if (lane == 0) atomicExch(p.err_flag, 1);
           continue;
         }
         const int n_kblocks = p.kdim / BK;
@@ -338,19 +344,23 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * kABytes);
           const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k) {
-            umma_bf16<CG>(d_tmem, sw128_desc(a0 + k * UMMA_K * 2),
-                          sw128_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0);
+            for (int k = 0; k < BK / UMMA_K; ++k) {
+              umma_bf16<CG>(d_tmem, sw128_desc(a0 + k * UMMA_K * 2),
+                            sw128_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0);
+            }
+            tc_commit<CG>(&empty[stage]);
           }
-          tc_commit<CG>(&empty[stage]);
+          __syncwarp();
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
-        tc_commit<CG>(&tmem_full[acc]);
+        if (elect_one()) tc_commit<CG>(&tmem_full[acc]);
+        __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       }
-      if (p.prof) {
+      if (p.prof && lane == 0) {
         unsigned long long* pr = p.prof + blockIdx.x * kProfSlots;
         pr[1] = w_epi;
         pr[2] = w_tma;
