@@ -156,7 +156,8 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
 
   if (warp == 0) {
     // ===== TMA producer: 12 (Q, K) k-blocks, then d/NC V chunks, one ring
-    if (lane == 0) {
+    // (the warp walks the ring in lockstep, one elected lane issues)
+    {
       int slot = 0;
       uint32_t phase = 0;
       const int n_loads = n_kb + n_chunks * C::kVPerChunk;
@@ -164,7 +165,8 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
         mbar_wait(&empty[slot], phase ^ 1);
         uint8_t* dst = ring + slot * kSlot;
         const uint32_t fb = smem_u32(&full[slot]);
-        if (i < n_kb) {
+        if (!elect_one()) {
+        } else if (i < n_kb) {
           mbar_expect_tx(&full[slot], C::kQKBytes);
           tma_load_2d<1>(dst, &tm_qkv, i * BK, row0 + q0, fb);              // Q rows
 #pragma unroll
@@ -183,12 +185,14 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
               tma_load_2d<1>(dst + gcol * (C::kVKeys * 128) + kh * 128 * 128, &tm_qkv,
                              c0 + gcol * 64, k0 + kh * 128, fb);
         }
+        __syncwarp();
         if (++slot == kSlots) { slot = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (one thread)
-    if (lane == 0) {
+    // ===== MMA issuer: warp-uniform walk, one elected lane issues the MMAs
+    // and their commits (descriptors in uniform registers)
+    {
       constexpr uint32_t idesc_s = idesc_bf16<BM, C::kSN>();
       constexpr uint32_t idesc_c = idesc_bf16<BM, NCT>() | (1u << 16);  // B (V) MN-major
       int slot = 0;
@@ -198,16 +202,20 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
         tc_fence_after();
         const uint32_t a0 = smem_u32(ring + slot * kSlot);
         const uint32_t b0 = a0 + BM * 128;
+        if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
+          for (int k = 0; k < BK / 16; ++k)
 #pragma unroll
-          for (int nh = 0; nh < NKEY / C::kSN; ++nh)  // 512 keys: two N=256 halves
-            umma_bf16<1>(tmem + nh * C::kSN, sw128_desc(a0 + k * 32),
-                         sw128_desc(b0 + nh * C::kSN * 128 + k * 32), idesc_s, (i | k) != 0);
-        tc_commit<1>(&empty[slot]);
+            for (int nh = 0; nh < NKEY / C::kSN; ++nh)  // 512 keys: two N=256 halves
+              umma_bf16<1>(tmem + nh * C::kSN, sw128_desc(a0 + k * 32),
+                           sw128_desc(b0 + nh * C::kSN * 128 + k * 32), idesc_s, (i | k) != 0);
+          tc_commit<1>(&empty[slot]);
+        }
+        __syncwarp();
         if (++slot == kSlots) { slot = 0; phase ^= 1; }
       }
-      tc_commit<1>(s_full);
+      if (elect_one()) tc_commit<1>(s_full);
+      __syncwarp();
       mbar_wait(p_full, 0);  // P in smem (and S fully read: its TMEM columns free)
       tc_fence_after();
       const uint32_t p0 = smem_u32(sP);
@@ -219,20 +227,24 @@ attn_core_kernel(const __grid_constant__ CUtensorMap tm_qkv, const int32_t* __re
           mbar_wait(&full[slot], phase);
           tc_fence_after();
           const uint32_t v0 = smem_u32(ring + slot * kSlot);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < C::kVKeys / 16; ++k) {  // 16 keys per MMA, V rows 16k..
-            const uint64_t vb = sw128_mn_desc(v0 + k * 16 * 128, C::kVKeys * 128);
-            if constexpr (C::kPT)  // P from TMEM: keys hv*256 + 16k.. = columns /2
-              umma_bf16_ts(d_tmem, tmem + hv * (C::kVKeys / 2) + k * 8, vb, idesc_c,
-                           (hv | k) != 0);
-            else                   // P from smem: atom k/4, 16-key step k%4
-              umma_bf16<1>(d_tmem, sw128_desc(p0 + (k >> 2) * (BM * 128) + (k & 3) * 32), vb,
-                           idesc_c, k != 0);
+            for (int k = 0; k < C::kVKeys / 16; ++k) {  // 16 keys per MMA, V rows 16k..
+              const uint64_t vb = sw128_mn_desc(v0 + k * 16 * 128, C::kVKeys * 128);
+              if constexpr (C::kPT)  // P from TMEM: keys hv*256 + 16k.. = columns /2
+                umma_bf16_ts(d_tmem, tmem + hv * (C::kVKeys / 2) + k * 8, vb, idesc_c,
+                             (hv | k) != 0);
+              else                   // P from smem: atom k/4, 16-key step k%4
+                umma_bf16<1>(d_tmem, sw128_desc(p0 + (k >> 2) * (BM * 128) + (k & 3) * 32), vb,
+                             idesc_c, k != 0);
+            }
+            tc_commit<1>(&empty[slot]);
           }
-          tc_commit<1>(&empty[slot]);
+          __syncwarp();
           if (++slot == kSlots) { slot = 0; phase ^= 1; }
         }
-        tc_commit<1>(&c_full[b]);
+        if (elect_one()) tc_commit<1>(&c_full[b]);
+        __syncwarp();
       }
     }
   } else {

@@ -286,8 +286,9 @@ expert_ffn_kernel(const __grid_constant__ CUtensorMap tmW1,  // (d, h, slot) box
   };
 
   if (warp == 0) {
-    // ===== TMA producer (both CTAs): 128 weight rows + this CTA's half of the tokens
-    if (lane == 0) {
+    // ===== TMA producer (both CTAs): 128 weight rows + this CTA's half of the
+    // tokens; the warp walks the schedule in lockstep, one elected lane issues
+    {
       // experts held by one token tile stream their weights once: evict-first;
       // experts split over several tiles re-read them: normal policy
       const uint64_t pol_first = evict_first_policy();
@@ -309,7 +310,7 @@ expert_ffn_kernel(const __grid_constant__ CUtensorMap tmW1,  // (d, h, slot) box
             const unsigned long long c0 = p.prof ? clk() : 0;
             while (true) {
               asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flags + mt) : "memory");
-              if (v == flag_target) break;
+              if (__shfl_sync(0xffffffffu, v, 0) == flag_target) break;
               __nanosleep(32);
             }
             asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -327,24 +328,27 @@ expert_ffn_kernel(const __grid_constant__ CUtensorMap tmW1,  // (d, h, slot) box
             mbar_wait(&empty[stage], phase ^ 1);
             if (p.prof) w_empty += clk() - c1;
             const uint32_t fb = map_rank(smem_u32(&full[stage]), 0);
-            if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBoxBytes));
-            tma_w(sA + stage * kABytes, tw, kb * BK, t.f0 + static_cast<int>(rank) * 128, t.slot,
-                  fb, pol);
-            for (int b = 0; b < nbox; ++b)
-              tma_load_2d<2>(sB + stage * kBBytes + b * kBoxBytes, tx, kb * BK, xrow + b * kBox,
-                             fb);
+            if (elect_one()) {
+              if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBoxBytes));
+              tma_w(sA + stage * kABytes, tw, kb * BK, t.f0 + static_cast<int>(rank) * 128,
+                    t.slot, fb, pol);
+              for (int b = 0; b < nbox; ++b)
+                tma_load_2d<2>(sB + stage * kBBytes + b * kBoxBytes, tx, kb * BK,
+                               xrow + b * kBox, fb);
+            }
+            __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
         }
       }
-      if (p.prof) {
+      if (p.prof && lane == 0) {
         p.prof[blockIdx.x * kProf + 0] = w_empty;
         p.prof[blockIdx.x * kProf + 1] = w_flag;
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (leader CTA, one lane)
-    if (lane == 0 && leader) {
+    // ===== MMA issuer (leader CTA): warp-uniform walk, one elected lane issues
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_par = 0;  // bit c: parity of chunk c's next release
@@ -359,7 +363,7 @@ expert_ffn_kernel(const __grid_constant__ CUtensorMap tmW1,  // (d, h, slot) box
         for (int j = 0; j < nsub; ++j) {
           const Tile t = tile(g2, mt, nt, j);
           if (t.slot < 0) {
-            atomicExch(p.err_flag, 1);
+            if (lane == 0) atomicExch(p.err_flag, 1);
             continue;
           }
           const int nch = (t.n16 + 31) >> 5;
@@ -379,27 +383,31 @@ expert_ffn_kernel(const __grid_constant__ CUtensorMap tmW1,  // (d, h, slot) box
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + stage * kABytes);
             const uint32_t b0 = smem_u32(sB + stage * kBBytes);
-            int col = pos * 32, rem = t.n16, o = 0;
-            while (rem > 0) {
-              const int n = min(rem, min(256, 512 - col));
-              const uint32_t idesc = idesc_m256(n);
+            if (elect_one()) {
+              int col = pos * 32, rem = t.n16, o = 0;
+              while (rem > 0) {
+                const int n = min(rem, min(256, 512 - col));
+                const uint32_t idesc = idesc_m256(n);
 #pragma unroll
-              for (int k = 0; k < BK / UMMA_K; ++k)
-                umma_bf16<2>(tmem_base + col, sw128_desc(a0 + k * UMMA_K * 2),
-                             sw128_desc(b0 + o * 128 + k * UMMA_K * 2), idesc, (kb | k) != 0);
-              o += n >> 1;
-              rem -= n;
-              col = (col + n) & 511;
+                for (int k = 0; k < BK / UMMA_K; ++k)
+                  umma_bf16<2>(tmem_base + col, sw128_desc(a0 + k * UMMA_K * 2),
+                               sw128_desc(b0 + o * 128 + k * UMMA_K * 2), idesc, (kb | k) != 0);
+                o += n >> 1;
+                rem -= n;
+                col = (col + n) & 511;
+              }
+              tc_commit<2>(&empty[stage]);
             }
-            tc_commit<2>(&empty[stage]);
+            __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          tc_commit<2>(&tile_full[tcount & (kTileRing - 1)]);
+          if (elect_one()) tc_commit<2>(&tile_full[tcount & (kTileRing - 1)]);
+          __syncwarp();
           ++tcount;
           pos = (pos + nch) & (kChunks - 1);
         }
       }
-      if (p.prof) {
+      if (p.prof && lane == 0) {
         unsigned long long* pr = p.prof + blockIdx.x * kProf;
         pr[2] = w_full;
         pr[3] = w_chunk;

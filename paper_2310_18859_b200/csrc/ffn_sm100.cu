@@ -713,8 +713,9 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
   };
 
   if (warp == 0) {
-    // ===== TMA producer (both CTAs): own 128 weight rows, own half of the tokens
-    if (lane == 0) {
+    // ===== TMA producer (both CTAs): own 128 weight rows, own half of the
+    // tokens (warp-uniform walk, one elected lane issues)
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (int it = unit; it < total; it += n_units) {
@@ -726,18 +727,22 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           const uint32_t fb = map_rank(smem_u32(&full[stage]), 0);
-          if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBoxBytes));
-          tma_load_3d<2>(sA + stage * kABytes, &tmW, kb * BK, t.f0 + rank * 128, t.slot, fb);
-          for (int b = 0; b < nbox; ++b)
-            tma_load_2d<2>(sB + stage * kBBytes + b * kBoxBytes, &tmX, kb * BK, xrow + b * kTnBox,
-                           fb);
+          if (elect_one()) {
+            if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBoxBytes));
+            tma_load_3d<2>(sA + stage * kABytes, &tmW, kb * BK, t.f0 + rank * 128, t.slot, fb);
+            for (int b = 0; b < nbox; ++b)
+              tma_load_2d<2>(sB + stage * kBBytes + b * kBoxBytes, &tmX, kb * BK,
+                             xrow + b * kTnBox, fb);
+          }
+          __syncwarp();
           if (++stage == kTnStages) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (leader CTA, one lane): M = 256 features x N = nmma tokens
-    if (lane == 0 && leader) {
+    // ===== MMA issuer (leader CTA): M = 256 features x N = nmma tokens;
+    // warp-uniform walk, one elected lane issues
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -745,7 +750,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
       for (int it = unit; it < total; it += n_units) {
         const TnTile t = get_tile(it);
         if (t.slot < 0) {
-          atomicExch(p.err_flag, 1);
+          if (lane == 0) atomicExch(p.err_flag, 1);
           continue;
         }
         const uint32_t idesc = idesc_bf16_rt(256, t.nmma);
@@ -757,14 +762,18 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * kABytes);
           const uint32_t b0 = smem_u32(sB + stage * kBBytes);
+          if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < BK / UMMA_K; ++k)
-            umma_bf16<2>(d_tmem, sw128_desc(a0 + k * UMMA_K * 2), sw128_desc(b0 + k * UMMA_K * 2),
-                         idesc, (kb | k) != 0);
-          tc_commit<2>(&empty[stage]);
+            for (int k = 0; k < BK / UMMA_K; ++k)
+              umma_bf16<2>(d_tmem, sw128_desc(a0 + k * UMMA_K * 2),
+                           sw128_desc(b0 + k * UMMA_K * 2), idesc, (kb | k) != 0);
+            tc_commit<2>(&empty[stage]);
+          }
+          __syncwarp();
           if (++stage == kTnStages) { stage = 0; phase ^= 1; }
         }
-        tc_commit<2>(&tmem_full[acc]);
+        if (elect_one()) tc_commit<2>(&tmem_full[acc]);
+        __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
