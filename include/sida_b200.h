@@ -152,7 +152,8 @@ int sida_debug_gemm_prof(unsigned long long* out);
 /* Observability: collect the counters above from now on (on = 1) or stop. */
 int sida_set_gemm_prof(int on);
 
-/* Expert-FFN tile family for sida_grouped_ffn_bf16: -1 auto, 0 token-M
+/* Expert-FFN tile family for sida_grouped_ffn_bf16: -1 auto (token-N for both
+ * GEMMs when d, h % 256 == 0, else token-M), 0 token-M
  * tiles for both GEMMs (128/256 token rows x BN features), 1 token-N tiles
  * for both (swap-AB: 256 features x 16..256 token rows in steps of 16),
  * 2 token-M GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2,

@@ -631,6 +631,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int unit = blockIdx.x >> 1, n_units = gridDim.x >> 1;
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 8] = gtime();
 
   if (warp == 2) {
     // token-tile prefix over the listed experts: one warp, 32 experts per step
@@ -685,6 +686,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
   const uint32_t tmem_base = *s_tmem;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 9] = gtime();
 
   const int n_ft = p.ndim / 256;  // feature tiles per expert (M = 256 per pair)
   const int total = s_prefix[n_list] * n_ft;
@@ -747,6 +749,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      const unsigned long long m0 = p.prof ? clk() : 0;
       for (int it = unit; it < total; it += n_units) {
         const TnTile t = get_tile(it);
         if (t.slot < 0) {
@@ -776,6 +779,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
         __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
+      if (p.prof && lane == 0) p.prof[blockIdx.x * kProfSlots + 3] = clk() - m0;
     }
   } else {
     // ===== epilogue: warp owns TMEM lanes 32*(w%4).. (32 features of this
@@ -784,6 +788,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
     const int half = (warp - 2) >> 2;
     int acc = 0;
     uint32_t acc_phase = 0;
+    const unsigned long long e0 = p.prof ? clk() : 0;
     for (int it = unit; it < total; it += n_units) {
       const TnTile t = get_tile(it);
       if (t.slot < 0) continue;
@@ -850,10 +855,12 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
       if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(&tmem_empty[acc]), 0));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (p.prof && warp == 2 && lane == 0) p.prof[blockIdx.x * kProfSlots + 5] = clk() - e0;
   }
 
   tc_fence_before();
   cluster_sync();
+  if (p.prof && threadIdx.x == 0) p.prof[blockIdx.x * kProfSlots + 10] = gtime();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -1095,33 +1102,30 @@ static int choose_cg(int gemm, int n_rows, int listed) {
 // Tile family per expert GEMM (sida_set_ffn_tiles, or SIDA_FFN_SWAP at load):
 // -1 auto, 0 token-M for both GEMMs, 1 token-N (swap-AB) for both, 2 token-M
 // GEMM1 + token-N GEMM2, 3 token-N GEMM1 + token-M GEMM2, 5 the one-launch
-// FFN of expert_ffn.cu (4, a per-token-tile fused kernel, was retired). Auto is
-// token-M with the per-GEMM CTA-group choice above, which measured fastest
-// everywhere (profiles/r1/ffn_tile_families.txt); token-N is used in auto
-// mode only inside [SIDA_FFN_SWAP_LO, SIDA_FFN_SWAP_HI) rows per expert for
-// GEMM2 (empty by default).
+// FFN of expert_ffn.cu (4, a per-token-tile fused kernel, was retired). Auto
+// is token-N for both GEMMs wherever d, h % 256 == 0 -- measured fastest or
+// equal at every expert count once the MMA issue is warp-uniform (one B200,
+// tools/ffn_probe.py, 32K rows: base-128 0.400 vs 0.425 ms token-M, base-64
+// 0.341 vs 0.352, base-256 0.530 vs 0.570, base-8 0.281 both; 131K rows at
+// base-128 1.194 vs 1.211) -- and token-M with the CTA-group choice above
+// otherwise. SIDA_FFN_SWAP sets the initial mode.
 static int g_tn_mode = -2;
-static int g_tn_lo = 0, g_tn_hi = 0;
 
 static void tn_init() {
   if (g_tn_mode != -2) return;
   const char* e = getenv("SIDA_FFN_SWAP");
   g_tn_mode = e ? atoi(e) : -1;
-  if (const char* r = getenv("SIDA_FFN_SWAP_LO")) g_tn_lo = atoi(r);
-  if (const char* r = getenv("SIDA_FFN_SWAP_HI")) g_tn_hi = atoi(r);
 }
 
-static bool choose_tn(int gemm, int n_rows, int listed, int d, int h) {
+static bool choose_tn(int gemm, int d, int h) {
   tn_init();
   if (d % 256 != 0 || h % 256 != 0) return false;
   switch (g_tn_mode) {
     case 0: return false;
-    case 1: return true;
     case 2: return gemm == 2;
     case 3: return gemm == 1;
-    default: break;
+    default: return true;  // 1, and auto
   }
-  return gemm == 2 && n_rows >= g_tn_lo * listed && n_rows < g_tn_hi * listed;
 }
 
 extern "C" int sida_set_ffn_tiles(int mode) {
@@ -1197,7 +1201,7 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   p1.arena = ar; p1.slot_stride = slot_stride; p1.bias_off = b1_off;
   p1.hidden = hidden; p1.err_flag = err_flag; p1.prof = prof_buffer(0);
   p1.half_tiles = 1;
-  int st = choose_tn(1, n_rows, listed, d, h) ? sm100::launch_tn<1>(x_perm, ar, n_slots, p1, listed, s)
+  int st = choose_tn(1, d, h) ? sm100::launch_tn<1>(x_perm, ar, n_slots, p1, listed, s)
               : sm100::dispatch_gemm<1>(x_perm, ar, n_slots, p1, listed,
                                         choose_cg(1, n_rows, listed), s);
   if (st) return st;
@@ -1207,7 +1211,7 @@ extern "C" int sida_grouped_ffn_bf16(const uint16_t* x_perm, int n_rows, int d, 
   p2.row_map = row_map; p2.alpha = alpha; p2.resid = resid; p2.out = out;
   p2.out_bf16 = out_bf16;
   p2.prof = prof_buffer(1);
-  if (choose_tn(2, n_rows, listed, d, h)) return sm100::launch_tn<2>(hidden, ar + w2_off, n_slots, p2, listed, s);
+  if (choose_tn(2, d, h)) return sm100::launch_tn<2>(hidden, ar + w2_off, n_slots, p2, listed, s);
   return sm100::dispatch_gemm<2>(hidden, ar + w2_off, n_slots, p2, listed,
                                  choose_cg(2, n_rows, listed), s);
 }
