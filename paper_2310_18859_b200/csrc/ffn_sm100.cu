@@ -720,6 +720,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
     {
       int stage = 0;
       uint32_t phase = 0;
+      unsigned long long w_empty = 0;
       for (int it = unit; it < total; it += n_units) {
         const TnTile t = get_tile(it);
         if (t.slot < 0) continue;
@@ -727,7 +728,9 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
         const int nbox = ceil_div(half_rows, kTnBox);
         const int xrow = t.row0 + static_cast<int>(rank) * half_rows;
         for (int kb = 0; kb < nkb; ++kb) {
+          const unsigned long long c0 = p.prof ? clk() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (p.prof) w_empty += clk() - c0;
           const uint32_t fb = map_rank(smem_u32(&full[stage]), 0);
           if (elect_one()) {
             if (leader) mbar_expect_tx(&full[stage], 2 * (kABytes + nbox * kBoxBytes));
@@ -740,6 +743,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
           if (++stage == kTnStages) { stage = 0; phase ^= 1; }
         }
       }
+      if (p.prof && lane == 0) p.prof[blockIdx.x * kProfSlots + 0] = w_empty;
     }
   } else if (warp == 1) {
     // ===== MMA issuer (leader CTA): M = 256 features x N = nmma tokens;
@@ -750,6 +754,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
       int acc = 0;
       uint32_t acc_phase = 0;
       const unsigned long long m0 = p.prof ? clk() : 0;
+      unsigned long long w_epi = 0, w_tma = 0, n_tiles = 0;
       for (int it = unit; it < total; it += n_units) {
         const TnTile t = get_tile(it);
         if (t.slot < 0) {
@@ -757,11 +762,16 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
           continue;
         }
         const uint32_t idesc = idesc_bf16_rt(256, t.nmma);
+        ++n_tiles;
+        const unsigned long long c1 = p.prof ? clk() : 0;
         mbar_wait_cluster(&tmem_empty[acc], acc_phase ^ 1);
+        if (p.prof) w_epi += clk() - c1;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kTnMax;
         for (int kb = 0; kb < nkb; ++kb) {
+          const unsigned long long c2 = p.prof ? clk() : 0;
           mbar_wait(&full[stage], phase);
+          if (p.prof) w_tma += clk() - c2;
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + stage * kABytes);
           const uint32_t b0 = smem_u32(sB + stage * kBBytes);
@@ -779,7 +789,13 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
         __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
-      if (p.prof && lane == 0) p.prof[blockIdx.x * kProfSlots + 3] = clk() - m0;
+      if (p.prof && lane == 0) {
+        unsigned long long* pr = p.prof + blockIdx.x * kProfSlots;
+        pr[1] = w_epi;
+        pr[2] = w_tma;
+        pr[3] = clk() - m0;
+        pr[6] = n_tiles;
+      }
     }
   } else {
     // ===== epilogue: warp owns TMEM lanes 32*(w%4).. (32 features of this
@@ -789,6 +805,7 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
     int acc = 0;
     uint32_t acc_phase = 0;
     const unsigned long long e0 = p.prof ? clk() : 0;
+    unsigned long long w_full = 0;
     for (int it = unit; it < total; it += n_units) {
       const TnTile t = get_tile(it);
       if (t.slot < 0) continue;
@@ -797,7 +814,9 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
           p.arena + static_cast<size_t>(t.slot) * p.slot_stride + p.bias_off);
       const float b = bf16_to_f32(bias[f]);
       const int nch = ceil_div(t.nrows, 32);
+      const unsigned long long c3 = p.prof ? clk() : 0;
       mbar_wait(&tmem_full[acc], acc_phase);
+      if (p.prof) w_full += clk() - c3;
       tc_fence_after();
       const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kTnMax;
       for (int c = half; c < nch; c += 2) {
@@ -855,7 +874,10 @@ grouped_gemm_tn_kernel(const __grid_constant__ CUtensorMap tmW,  // (k, feature,
       if (lane == 0) mbar_arrive_cluster(map_rank(smem_u32(&tmem_empty[acc]), 0));
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (p.prof && warp == 2 && lane == 0) p.prof[blockIdx.x * kProfSlots + 5] = clk() - e0;
+    if (p.prof && warp == 2 && lane == 0) {
+      p.prof[blockIdx.x * kProfSlots + 4] = w_full;
+      p.prof[blockIdx.x * kProfSlots + 5] = clk() - e0;
+    }
   }
 
   tc_fence_before();
