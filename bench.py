@@ -33,6 +33,7 @@ independent replicas instead.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import sys
@@ -241,7 +242,7 @@ class ClockSampler:
             self._nvml = None
 
     def __enter__(self):
-        if self._nvml is not None:
+        if self._nvml is not None and os.environ.get("SIDA_BENCH_NVML", "1") != "0":
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         return self
@@ -404,7 +405,16 @@ def budget_runs(model, pred, cfg, lengths, runs, steps=4, zipf=False, seed=0):
         slots = max(1, int(round(frac * n_all)))
         eng = SidaEngine(model, pred, MemoryBudget(slots * eb), eval_top_k=1,
                          victim_policy=policy)
-        run_stream(eng, toks, lengths, 2, 1)  # reach the steady residency cycle
+        if slots >= n_all:
+            # calibration run: every expert resident before timing (a table
+            # routing token t to expert t % K in every layer), so rarely used
+            # experts are not first-touch loads inside the timed steps
+            from paper_2310_18859_b200.predictor import ExpertHashTable
+
+            ids = np.tile(np.arange(n_tok) % cfg.num_experts, (cfg.num_layers, 1))[:, :, None]
+            eng.forward(ExpertHashTable(0, list(lengths), ids, np.ones(ids.shape)), lengths,
+                        tokens_dev=toks[0])
+        run_stream(eng, toks, lengths, 3, 1)  # reach the steady residency cycle
         loads0 = eng.store.bytes_loaded
         ms, tabs = run_stream(eng, toks, lengths, steps, 0)
         loaded = (eng.store.bytes_loaded - loads0) / steps
@@ -633,6 +643,12 @@ def run_ours(args):
     n_steps = args.warmup + args.steps
     toks = [synth_tokens(n_tok, cfg.vocab_size, g) for _ in range(n_steps + 1)]
     torch.cuda.synchronize()
+    # a serving process's long-lived host objects (model, predictor, residency
+    # bookkeeping) leave the cyclic GC's generations: full collections
+    # otherwise traverse them and stall the launch loop for 60-100 ms
+    # (measured: first timed steps of 80-100 ms against 7.4 ms)
+    gc.collect()
+    gc.freeze()
     h = _lib.lib()
 
     def barrier():
@@ -657,6 +673,7 @@ def run_ours(args):
     # the timed region carries no per-layer events (an event recorded between
     # two launches ends their programmatic-dependent-launch overlap); the
     # per-layer FFN / attention times come from an instrumented pass after it
+    step_evs = []  # compute-stream events at step boundaries (per-step spread)
     for j in range(n_steps):
         if j == args.warmup:
             barrier()
@@ -665,6 +682,9 @@ def run_ours(args):
             sampler.__enter__()
             ev_start.record(cs)
             t_wall0 = time.perf_counter()
+        if j > args.warmup:
+            step_evs.append(torch.cuda.Event(enable_timing=True))
+            step_evs[-1].record(cs)
         a = j + HASH_AHEAD
         tables[a] = engine.hash_tokens(a, toks[a % len(toks)], lengths)
         engine.forward(tables.pop(j), lengths, tokens_dev=toks[j % len(toks)],
@@ -676,6 +696,8 @@ def run_ours(args):
     launches = h.sida_launch_count() - launches0
     loads_timed = engine.store.n_loads - loads0
     ms = max_over_ranks(ev_start.elapsed_time(ev_end))
+    bounds = [ev_start] + step_evs + [ev_end]
+    step_list = [bounds[i].elapsed_time(bounds[i + 1]) for i in range(len(bounds) - 1)]
     # instrumented pass: CUDA events around every layer's attention and FFN,
     # and the FFN GEMMs' own cycle / %globaltimer counters (the SM clock the
     # dominant kernel actually ran at)
@@ -778,6 +800,7 @@ def run_ours(args):
         "metric": "MoE inference tokens/sec (SiDA serving)",
         "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "step_ms_median": float(np.median(step_list)), "step_ms_max": float(np.max(step_list)),
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic uniform tokens, random-init Switch-shaped weights (GPU RNG)",
         "config": {"workload": workload_name(args, ws, ep), "global_batch": B * ws,
