@@ -229,7 +229,7 @@ class SidaEngine:
         n_layers = model.config.num_layers
         cs = self.compute_stream
         bp = self._pending if (self._pending is not None and self._pending.table is table) \
-            else self._plan_batch(table)
+            else self._plan_batch(table, next_table)
         self._pending = None
         required, plan, waves = bp.required, bp.plan, bp.waves
         dt = table.on_device(model, stream=self.hash_stream)
@@ -403,16 +403,29 @@ class SidaEngine:
         return logits
 
     # -- planning / issue ---------------------------------------------------------------
-    def _plan_batch(self, table) -> _BatchPlan:
+    def _plan_batch(self, table, next_table=None) -> _BatchPlan:
         """ref pipeline.py:217-225: plan against the residency state left by
-        every group issued so far, and do the slot bookkeeping of all groups."""
+        every group issued so far, and do the slot bookkeeping of all groups.
+        The spread policy also reads the next batch's table when it is built
+        (hash-driven victims: experts neither batch needs go first)."""
         n_layers = self.model.config.num_layers
         required = table.required_by_layer()
         if len(required) < n_layers:
             raise ContractError(f"missing hash entry for (layer {len(required)}, token 0)")
-        planner = plan_placement if self.victim_policy == "fifo" else plan_placement_spread
-        plan = planner(table, self.state, self.budget, self.model.expert_bytes_each())
+        if self.victim_policy == "fifo":
+            plan = plan_placement(table, self.state, self.budget, self.model.expert_bytes_each())
+        else:
+            nt = next_table if next_table is not None and self._table_ready(next_table) else None
+            plan = plan_placement_spread(table, self.state, self.budget,
+                                         self.model.expert_bytes_each(), next_table=nt)
         return _BatchPlan(table, required, plan, [None] * len(plan.groups))
+
+    @staticmethod
+    def _table_ready(table) -> bool:
+        """Host tables always; device tables once their hash (and histogram)
+        has completed -- planning never waits on the hash stream."""
+        dt = getattr(table, "_dev", None)
+        return dt is None or (dt.hist is not None and dt.ready.query())
 
     def _issue(self, bp: _BatchPlan, idx: int) -> None:
         """ref pipeline.py:229-235 issue(): apply the group to the residency

@@ -148,7 +148,7 @@ def plan_placement(table, state: ResidencyState, budget: MemoryBudget,
 
 
 def plan_placement_spread(table, state: ResidencyState, budget: MemoryBudget,
-                          expert_bytes: int) -> PlacementPlan:
+                          expert_bytes: int, next_table=None) -> PlacementPlan:
     """Opt-in victim policy (no reference counterpart; ``SidaEngine(...,
     victim_policy="spread")``): the same per-layer groups as
     ``plan_placement`` -- loads are the layer's missing experts in ascending
@@ -165,7 +165,12 @@ def plan_placement_spread(table, state: ResidencyState, budget: MemoryBudget,
     batch, 8/2/6/2 on layers 0-3) and a layer's copies outlast the compute
     they could hide behind. Spread victims settle at one load per layer (12
     per batch) there, and at 1-3 per layer at 72 slots, each within a
-    layer's compute when issued a layer ahead."""
+    layer's compute when issued a layer ahead.
+
+    ``next_table`` (the next batch's hash table, which SiDA has already built
+    while this batch is planned): among the experts this batch does not need,
+    those the next batch does not need either go first -- the hash-driven
+    half of the victim order. Without it the order is as above."""
     if expert_bytes > budget.fast_tier_bytes:
         raise UnservableError(
             f"expert of {expert_bytes} bytes exceeds budget {budget.fast_tier_bytes}")
@@ -191,6 +196,14 @@ def plan_placement_spread(table, state: ResidencyState, budget: MemoryBudget,
     for layer, r in enumerate(required):
         if r:
             req[layer, np.fromiter(r, dtype=np.int64, count=len(r))] = True
+    nxt = None
+    if next_table is not None:
+        nreq = next_table.required_by_layer()
+        nxt = np.zeros_like(req)
+        for layer, r in enumerate(nreq):
+            r = [e for e in r if e < req.shape[1]]
+            if r and layer < req.shape[0]:
+                nxt[layer, np.asarray(r, dtype=np.int64)] = True
     resident = set(keys)
     used = state.used_bytes
     budget_bytes = budget.fast_tier_bytes
@@ -217,10 +230,13 @@ def plan_placement_spread(table, state: ResidencyState, budget: MemoryBudget,
                                    np.where(ll == layer, 4,
                                             np.where(ll < layer - 1, 1,
                                                      np.where(ll > layer, 2, 3))))
+                    # (class 0 split by the next batch's table: its experts
+                    # are evicted after the ones neither batch needs)
+                    nx = nxt[ll, ke[idx]] if nxt is not None else np.zeros(idx.size, bool)
                     dist = np.where(ll < layer, n_layers - layer + ll, ll - layer)
                     # (class, evictions already taken from the layer, furthest
                     # next use, arrival order) as one lexicographic integer key
-                    hi = cls * 4096
+                    hi = (cls * 2 + (nx & (cls == 0))) * 4096
                     lo = (255 - np.clip(dist, 0, 255)) * 65536 + pos_all[idx]
                     free = np.ones(idx.size, dtype=bool)
                     cand = (idx, ll, cls, hi, lo, free)

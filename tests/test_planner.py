@@ -167,3 +167,52 @@ def test_spread_policy_tiny_budgets(slots):
             apply_group_inplace(st, g, slots, 1)
             assert st.used_bytes <= slots
         st.check()
+
+
+def test_spread_policy_uses_the_next_batch_table():
+    """Hash-driven victims (plan_placement_spread(..., next_table=...)): with a
+    skewed stream whose hot experts recur batch after batch and a budget that
+    holds the hot set plus a little, knowing the next batch's table cuts the
+    expert loads, and an expert the next batch needs is never evicted while an
+    expert neither batch needs is resident."""
+    from paper_2310_18859_b200.offload import (MemoryBudget, ResidencyState,
+                                               apply_group_inplace, plan_placement_spread)
+
+    L, K, slots = 6, 32, 6 * 20
+    rng = np.random.default_rng(7)
+    hot = [set(rng.choice(K, 14, replace=False).tolist()) for _ in range(L)]
+    stream = []
+    for _ in range(12):
+        layers = []
+        for layer in range(L):
+            cold = set(rng.choice(K, 6, replace=False).tolist())
+            layers.append(hot[layer] | cold)
+        stream.append(FakeTable(layers))
+
+    def run(aware):
+        st = ResidencyState()
+        loads = 0
+        for j, table in enumerate(stream):
+            nxt = stream[j + 1] if aware and j + 1 < len(stream) else None
+            plan = plan_placement_spread(table, st, MemoryBudget(slots), 1, next_table=nxt)
+            req = table.required_by_layer()
+            for g in plan.groups:
+                if nxt is not None:
+                    nreq = nxt.required_by_layer()
+                    live = set(st.resident)
+                    for op, k in g.steps:
+                        if op == "load":
+                            live.add(k)
+                            continue
+                        live.discard(k)
+                        if k[1] in nreq[k[0]] and k[1] not in req[k[0]]:
+                            # a next-batch expert went while an unneeded one stayed?
+                            assert not any(e not in req[l] and e not in nreq[l]
+                                           for (l, e) in live)
+                apply_group_inplace(st, g, slots, 1)
+                loads += len(g.loads) if j >= 2 else 0
+            st.check()
+        return loads
+
+    blind, aware = run(False), run(True)
+    assert aware < blind, (aware, blind)
