@@ -1,6 +1,7 @@
 """A/B of the hash/compute stream arrangement at the bench shape, in one
 process, modes interleaved and repeated (median ms per step):
-  prio    hash stream at low priority, compute at high (engine default)
+  prio    hash stream at low priority, compute at high
+  hashprio  hash stream at high priority, compute at low
   flat    both streams at the same priority
   serial  hash enqueued on the compute stream (no overlap)
     python tools/pipe_ab.py [--experts 128] [--reps 5] [--steps 8]
@@ -34,6 +35,7 @@ budget = MemoryBudget(model.total_expert_bytes())
 lo, hi = torch.cuda.Stream.priority_range()
 cs_hi = torch.cuda.Stream(priority=hi)
 streams = {"prio": (torch.cuda.Stream(priority=lo), cs_hi),
+           "hashprio": (torch.cuda.Stream(priority=hi), torch.cuda.Stream(priority=lo)),
            "flat": (torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=0)),
            "serial": (cs_hi, cs_hi)}
 modes = a.modes.split(",")
