@@ -65,7 +65,7 @@ def parse():
     p.add_argument("--experts", type=int, default=128)
     p.add_argument("--budget-frac", type=float, default=0.97,
                    help="HBM expert budget as a fraction of all (local) expert bytes")
-    p.add_argument("--victim-policy", default="spread", choices=["fifo", "spread"],
+    p.add_argument("--victim-policy", default="fifo", choices=["fifo", "spread"],
                    help="expert-store victim order: the reference's FIFO classes or the "
                         "opt-in spread order (identical logits)")
     p.add_argument("--parallel", default="auto", choices=["auto", "dp", "ep"],
@@ -864,8 +864,9 @@ def run_ours(args):
                       "marginal): a batch activates a subset of the experts, the regime SiDA "
                       "saves memory in",
             "budgets": budget_runs(model, pred, cfg, lengths,
-                                   [(1.0, "fifo"), (0.9, "spread"), (0.85, "spread"),
-                                    (0.8, "spread"), (0.7, "spread")], zipf=True, seed=1)}
+                                   [(1.0, "fifo"), (0.9, "fifo"), (0.9, "spread"),
+                                    (0.85, "fifo"), (0.85, "spread"), (0.8, "spread"),
+                                    (0.7, "spread")], zipf=True, seed=1)}
         for r in line["memory_regime_zipf"]["budgets"]:
             r["copy_ms_per_step_at_link"] = r["expert_loads_per_step"] * eb / (link * 1e9) * 1e3
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
