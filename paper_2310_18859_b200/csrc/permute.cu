@@ -16,10 +16,11 @@
 //               the row's rank among the tile's rows of its expert. Writes
 //               the tile's per-expert counts and one code per row
 //               (expert | rank << 10), both coalesced.
-//   tile_base   one CTA per layer, threads = (tile chunk, expert): the
-//               exclusive scan of the counts over tiles (each (tile, expert)
-//               run's offset inside its expert), then a block scan of the
-//               expert totals with warp-shuffle prefix sums -> hist, off.
+//   tile_base   one CTA per (32 experts, layer), threads = (tile chunk,
+//               expert): the exclusive scan of the counts over tiles (each
+//               (tile, expert) run's offset inside its expert) -> base, hist.
+//   place_tiles (below) also scans hist over experts with warp-shuffle
+//               prefix sums for the expert offsets (tile 0 publishes off).
 //   place_tiles one CTA per (layer, tile): position of row r = off[e] +
 //               base[tile][e] + rank; inv written row-ordered (coalesced),
 //               the tile's rows staged in shared memory in sorted order so
@@ -147,109 +148,55 @@ rank_tiles_kernel(const int32_t* __restrict__ ids, int n_rows, int K, int n_tile
   }
 }
 
-// Block-wide exclusive scan of v over the block's threads (blockDim.x a
-// multiple of 32, <= 1024); returns the exclusive prefix, *total the sum.
-__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int w = lane < nw ? s_warp[lane] : 0;
-    int wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += t;
-    }
-    if (lane < nw) s_warp[lane] = wi - w;
-    if (lane == 31) s_warp[32] = wi;
-  }
-  __syncthreads();
-  *total = s_warp[32];
-  return s_warp[warp] + incl - v;
-}
-
-// One CTA of 1024 threads per layer: thread (q, e) owns expert e's counts over
-// the q-th of Q contiguous tile chunks (Q = 1024 / K rounded to 32, up to 32):
-// chunk sums, a prefix over the chunks in shared memory, then base[l][t][e] =
-// sum of counts[l][t'][e] over t' < t; hist, off from the expert totals by a
-// block scan with warp-shuffle prefix sums.
+// CTA (32 experts, layer), 1024 threads: thread (q, e) owns expert e's counts
+// over the q-th of 32 contiguous tile chunks: chunk sums, a prefix over the
+// chunks in shared memory, then base[l][t][e] = sum of counts[l][t'][e] over
+// t' < t, and hist[l][e] = the expert's total. Warp = 32 consecutive experts of
+// one chunk, so every counts / base access is a coalesced 128 B row segment.
+// (The expert offsets -- a scan of hist over experts -- are taken by
+// place_tiles, which needs them per CTA anyway.)
 __global__ void __launch_bounds__(1024)
 tile_base_kernel(const int32_t* __restrict__ counts, int K, int n_tiles, int32_t* __restrict__ base,
-                 int32_t* __restrict__ hist, int32_t* __restrict__ off) {
-  __shared__ int s_warp[33];
-  __shared__ int s_part[1024];
-  const int layer = blockIdx.x;
-  const int KP = (K + 31) & ~31;
-  const int Q = blockDim.x / KP;
-  const int e = threadIdx.x % KP, q = threadIdx.x / KP;
+                 int32_t* __restrict__ hist) {
+  __shared__ int s_part[32][33];
+  const int layer = blockIdx.y;
+  const int el = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + el;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // rank_tiles' counts are complete
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int32_t* cl = counts + (size_t)layer * n_tiles * K;
   int32_t* bl = base + (size_t)layer * n_tiles * K;
-  const int t0 = q < Q ? q * n_tiles / Q : n_tiles, t1 = q < Q ? (q + 1) * n_tiles / Q : n_tiles;
-  const bool mine = q < Q && e < K;
+  const int t0 = q * n_tiles / 32, t1 = (q + 1) * n_tiles / 32;
+  const bool mine = e < K;
   int sum = 0;
-  if (mine) {
-    int t = t0;
-    for (; t + 8 <= t1; t += 8) {  // eight loads in flight
-      int v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = cl[(size_t)(t + u) * K + e];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) sum += v[u];
-    }
-    for (; t < t1; ++t) sum += cl[(size_t)t * K + e];
-  }
-  if (q < Q) s_part[threadIdx.x] = sum;
+  if (mine)
+    for (int t = t0; t < t1; ++t) sum += cl[(size_t)t * K + e];
+  s_part[q][el] = sum;
   __syncthreads();
   int run = 0, tot = 0;
+#pragma unroll 8
+  for (int r = 0; r < 32; ++r) {
+    const int v = s_part[r][el];
+    run += r < q ? v : 0;
+    tot += v;
+  }
   if (mine) {
-    for (int r = 0; r < Q; ++r) {
-      const int v = s_part[r * KP + e];
-      run += r < q ? v : 0;
-      tot += v;
-    }
-    int t = t0;
-    for (; t + 8 <= t1; t += 8) {
-      int v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = cl[(size_t)(t + u) * K + e];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        bl[(size_t)(t + u) * K + e] = run;
-        run += v[u];
-      }
-    }
-    for (; t < t1; ++t) {
+    for (int t = t0; t < t1; ++t) {
       const int v = cl[(size_t)t * K + e];
       bl[(size_t)t * K + e] = run;
       run += v;
     }
+    if (q == 0) hist[(size_t)layer * K + e] = tot;
   }
-  // exclusive scan of the expert totals over experts (threads q == 0)
-  int total;
-  const int o = block_exclusive_scan(q == 0 && e < K ? tot : 0, s_warp, &total);
-  if (q == 0 && e < K) {
-    hist[(size_t)layer * K + e] = tot;
-    off[(size_t)layer * (K + 1) + e] = o;
-  }
-  if (threadIdx.x == 0) off[(size_t)layer * (K + 1) + K] = total;
 }
 
 template <int TILE>
 __global__ void __launch_bounds__(kPermThreads)
 place_tiles_kernel(const int32_t* __restrict__ codes, int n_rows, int K, int n_tiles,
                    const int32_t* __restrict__ counts, const int32_t* __restrict__ base,
-                   const int32_t* __restrict__ off, const float* __restrict__ alpha_rows,
-                   int32_t* __restrict__ perm, int32_t* __restrict__ inv,
-                   float* __restrict__ alpha_perm) {
+                   const int32_t* __restrict__ hist, int32_t* __restrict__ off,
+                   const float* __restrict__ alpha_rows, int32_t* __restrict__ perm,
+                   int32_t* __restrict__ inv, float* __restrict__ alpha_perm) {
   extern __shared__ int32_t smem[];
   int32_t* s_code = smem;              // [TILE]
   int32_t* s_ord = s_code + TILE;      // [TILE] tile row of sorted position q
@@ -258,14 +205,35 @@ place_tiles_kernel(const int32_t* __restrict__ codes, int n_rows, int K, int n_t
   const int layer = blockIdx.y, tile = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int r0 = tile * TILE, r1 = min(n_rows, r0 + TILE), n = r1 - r0;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // codes, counts, base, off complete
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // codes, counts, base, hist complete
   stage_ids(codes + (size_t)layer * n_rows, r0, r1, s_code);
   const size_t ct = ((size_t)layer * n_tiles + tile) * K;
   for (int e = threadIdx.x; e < K; e += blockDim.x) {
     s_texc[e] = counts[ct + e];
-    s_pos0[e] = off[(size_t)layer * (K + 1) + e] + base[ct + e];
+    s_pos0[e] = hist[(size_t)layer * K + e];  // -> expert offsets below
   }
   __syncthreads();
+  if (warp == 1) {  // expert offsets: exclusive scan of the layer's histogram
+    int carry = 0;
+    for (int b = 0; b < K; b += 32) {
+      const int e = b + lane;
+      const int v = e < K ? s_pos0[e] : 0;
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (e < K) {
+        s_pos0[e] = carry + incl - v;
+        if (tile == 0) off[(size_t)layer * (K + 1) + e] = carry + incl - v;
+      }
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (tile == 0 && lane == 0) off[(size_t)layer * (K + 1) + K] = carry;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < K; e += blockDim.x) s_pos0[e] += base[ct + e];
   if (warp == 0) {  // exclusive scan of the tile's counts over experts
     int carry = 0;
     for (int b = 0; b < K; b += 32) {
@@ -389,12 +357,16 @@ static int permute_launch(const int32_t* ids, int n_layers, int n_rows, int K, c
     SIDA_CUDA(cudaMemsetAsync(counts, 0, n * sizeof(int32_t), s));
   }
   // tile_base publishes hist / off, so it runs even for zero rows
-  int st = launch_pdl(tile_base_kernel, dim3(n_layers), 1024, 0, s, (const int32_t*)counts, K,
-                      n_tiles, base, hist, off);
-  if (st || n_rows == 0) return st;
+  int st = launch_pdl(tile_base_kernel, dim3(ceil_div(K, 32), n_layers), 1024, 0, s,
+                      (const int32_t*)counts, K, n_tiles, base, hist);
+  if (st) return st;
+  if (n_rows == 0) {  // no tiles to place: publish the (all-zero) offsets
+    SIDA_CUDA(cudaMemsetAsync(off, 0, (size_t)n_layers * (K + 1) * sizeof(int32_t), s));
+    return SIDA_OK;
+  }
   return launch_pdl(place_tiles_kernel<TILE>, grid, kPermThreads, smem3, s, (const int32_t*)codes,
                     n_rows, K, n_tiles, (const int32_t*)counts, (const int32_t*)base,
-                    (const int32_t*)off, alpha_rows, perm, inv, alpha_perm);
+                    (const int32_t*)hist, off, alpha_rows, perm, inv, alpha_perm);
 }
 
 extern "C" int sida_permute_hist(const int32_t* ids, int n_layers, int n_rows, int num_experts,
