@@ -22,6 +22,7 @@ p.add_argument("--experts", type=int, default=128)
 p.add_argument("--batches", type=int, default=10)
 p.add_argument("--reps", type=int, default=4)
 p.add_argument("--budget-frac", type=float, default=0.97)
+p.add_argument("--victim-policy", default="fifo", choices=["fifo", "spread"])
 a = p.parse_args()
 cfg = MoEConfig(vocab_size=32128, d_model=768, num_layers=12, num_experts=a.experts,
                 expert_hidden=3072, max_seq_len=512, num_classes=2)
@@ -30,7 +31,7 @@ pred = PredictorNet(PredictorConfig(), 768, 12, a.experts, Rng(1))
 eb = model.expert_bytes_each()
 slots = int(round(a.budget_frac * 12 * a.experts))
 budget = MemoryBudget(slots * eb)
-eng = SidaEngine(model, pred, budget, victim_policy="spread")
+eng = SidaEngine(model, pred, budget, victim_policy=a.victim_policy)
 rng = np.random.default_rng(99)
 B, T = 256, 128
 
