@@ -324,6 +324,17 @@ int sida_moe_token_f64(const double* x, int m, const double* alphas, const doubl
 int sida_expert_copy(void* dst_slot, const void* src_pinned, size_t bytes, void* copy_stream,
                      void* wait_event, void* done_event);
 
+/* n int32 values from host memory into device memory, in order on
+ * `stream`, carried in kernel parameter blocks (no copy-engine work: these
+ * small rows never queue behind the expert copies). src may be reused as soon
+ * as the call returns. */
+int sida_poke_i32(int32_t* dst, const int32_t* src, int n, void* stream);
+
+/* bytes from src to dst copied by the SMs on `stream`; either side may be
+ * pinned host memory (mapped under UVA). For the per-batch token rows and
+ * logits: no copy-engine work, so they never wait behind expert copies. */
+int sida_copy_sm(void* dst, const void* src, size_t bytes, void* stream);
+
 /* Pack one expert from the reference layout (float64 w1 (d,h), b1 (h),
  * w2 (h,d), b2 (d)) into the slot image above (host memory, bf16 RNE).
  * dst must hold sida_slot_bytes(d,h) bytes. */

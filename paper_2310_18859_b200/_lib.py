@@ -75,6 +75,8 @@ SIGNATURES = {
     "sida_router_scores_f64": (_i, [_vp, _i, _i, _vp, _i, _vp, _vp]),
     "sida_moe_token_f64": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp]),
     "sida_expert_copy": (_i, [_vp, _vp, _sz, _vp, _vp, _vp]),
+    "sida_poke_i32": (_i, [_vp, _vp, _i, _vp]),
+    "sida_copy_sm": (_i, [_vp, _vp, _sz, _vp]),
     "sida_pack_expert_host": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp]),
     "sida_plan_placement": (_i, [_vp, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp]),
 }

@@ -126,3 +126,64 @@ extern "C" int sida_combine_ranks(const float* y, const float* resid, int n_toke
   SIDA_LAUNCH_CHECK();
   return SIDA_OK;
 }
+
+// Small int32 rows (expert -> slot maps, sequence offsets) host -> HBM as
+// kernel parameters instead of an H2D memcpy: a memcpy on the compute or hash
+// stream shares the copy engines with the multi-MB expert copies in flight
+// on the copy stream and can wait behind them for milliseconds; a launch
+// carrying the values in its parameter block does not touch the copy engines.
+namespace {
+constexpr int kPokeMax = 1000;  // 4 KB parameter block
+struct PokeArgs {
+  int n;
+  int32_t v[kPokeMax];
+};
+__global__ void poke_i32_kernel(int32_t* __restrict__ dst, const PokeArgs a) {
+  for (int i = threadIdx.x; i < a.n; i += blockDim.x) dst[i] = a.v[i];
+}
+}  // namespace
+
+extern "C" int sida_poke_i32(int32_t* dst, const int32_t* src, int n, void* stream) {
+  SIDA_REQUIRE(n >= 0 && (n == 0 || (dst && src)), SIDA_ERR_CONTRACT,
+               "bad sida_poke_i32 arguments (n=%d)", n);
+  for (int off = 0; off < n; off += kPokeMax) {
+    PokeArgs a;
+    a.n = n - off < kPokeMax ? n - off : kPokeMax;
+    memcpy(a.v, src + off, sizeof(int32_t) * a.n);
+    poke_i32_kernel<<<1, 256, 0, sida::as_stream(stream)>>>(dst + off, a);
+    SIDA_LAUNCH_CHECK();
+  }
+  return SIDA_OK;
+}
+
+// Byte copy by the SMs between device memory and pinned (mapped, UVA) host
+// memory: for the per-batch token rows up and the logits down, which as
+// cudaMemcpyAsync on the hash / compute stream would queue on the copy
+// engines behind the expert copies the planner has already enqueued.
+namespace {
+__global__ void copy_sm_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                               size_t bytes) {
+  const size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+  if (vec) {
+    const size_t n16 = bytes / 16;
+    for (size_t i = t; i < n16; i += stride)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (size_t i = n16 * 16 + t; i < bytes; i += stride) dst[i] = src[i];
+  } else {
+    for (size_t i = t; i < bytes; i += stride) dst[i] = src[i];
+  }
+}
+}  // namespace
+
+extern "C" int sida_copy_sm(void* dst, const void* src, size_t bytes, void* stream) {
+  SIDA_REQUIRE(bytes == 0 || (dst && src), SIDA_ERR_CONTRACT, "null pointer passed to sida_copy_sm");
+  if (bytes == 0) return SIDA_OK;
+  const size_t chunks = (bytes + 16 * 256 - 1) / (16 * 256);
+  const int blocks = static_cast<int>(chunks < 148 ? chunks : 148);
+  copy_sm_kernel<<<blocks, 256, 0, sida::as_stream(stream)>>>(static_cast<uint8_t*>(dst),
+                                                              static_cast<const uint8_t*>(src), bytes);
+  SIDA_LAUNCH_CHECK();
+  return SIDA_OK;
+}

@@ -383,31 +383,24 @@ class Wave:
 
 
 class RowUploader:
-    """Small int32 rows (expert -> slot maps, expert lists) to the device
-    through a pinned ring, without a pinned allocation per call: slot i's host
-    row is rewritten only after the copy that last used it has completed."""
+    """Small int32 rows (expert -> slot maps, expert lists) to the device: a
+    ring of device rows written in stream order by `sida_poke_i32` (values in
+    the kernel's parameter block), so they never wait behind expert copies on
+    the copy engines the way a pinned H2D memcpy on the compute stream does."""
 
     def __init__(self, device, width: int, slots: int = 64):
-        self.host = torch.empty((slots, max(width, 1)), dtype=torch.int32).pin_memory()
-        self.host_np = self.host.numpy()
         self.dev = torch.empty((slots, max(width, 1)), dtype=torch.int32, device=device)
-        self.events: list = [None] * slots
+        self.slots = slots
         self.i = 0
 
     def upload(self, arr: np.ndarray, stream) -> torch.Tensor:
         i = self.i
-        self.i = (i + 1) % len(self.events)
-        ev = self.events[i]
-        if ev is not None and not ev.query():
-            ev.synchronize()
+        self.i = (i + 1) % self.slots
         n = len(arr)
-        self.host_np[i, :n] = arr
-        with torch.cuda.stream(stream):
-            self.dev[i, :n].copy_(self.host[i, :n], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(stream)
-        self.events[i] = ev
-        return self.dev[i, :n]
+        src = np.ascontiguousarray(arr, dtype=np.int32)
+        dst = self.dev[i, :n]
+        _lib.check(_lib.lib().sida_poke_i32(dst.data_ptr(), src.ctypes.data, n, stream.cuda_stream))
+        return dst
 
 
 class ExpertStore:

@@ -177,7 +177,9 @@ class TableSlot:
         st[:n].numpy()[:] = toks
         dev = self.get("tokens", (n,), torch.int32)
         with torch.cuda.stream(stream):
-            dev.copy_(st[:n], non_blocking=True)
+            # SM copy from pinned memory: no copy-engine queueing behind expert copies
+            _lib.check(_lib.lib().sida_copy_sm(dev.data_ptr(), st.data_ptr(), 4 * n,
+                                               stream.cuda_stream))
             self._stage_ev = torch.cuda.Event()
             self._stage_ev.record(stream)
         return dev
@@ -536,7 +538,10 @@ def hash_device(predictor: PredictorNet, model: MoEModel | None, tokens, lengths
     use_tables = model is not None
     with torch.cuda.stream(st):
         new = slot.get if slot is not None else _fresh(device)
-        seq_off = torch.from_numpy(off).pin_memory().to(device, non_blocking=True)
+        # as a kernel-parameter write, not an H2D memcpy: it must not queue
+        # behind expert copies on the copy engines (sida_poke_i32)
+        seq_off = new("seq_off", (n_seq + 1,), torch.int32)
+        _lib.check(h.sida_poke_i32(seq_off.data_ptr(), off.ctypes.data, n_seq + 1, st.cuda_stream))
         ids = new("ids", (L, n_tok, eval_top_k), torch.int32)
         alpha = new("alpha", (L, n_tok, eval_top_k), torch.float64)
         alpha_f32 = new("alpha_f32", (L, n_tok, eval_top_k), torch.float32)

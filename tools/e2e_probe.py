@@ -59,3 +59,4 @@ prof.enable()
 serve_sida(model, pred, bs, budget, engine=eng, compute_hit_rate=False)
 prof.disable()
 pstats.Stats(prof).sort_stats("tottime").print_stats(15)
+pstats.Stats(prof).sort_stats("cumulative").print_stats(25)
