@@ -417,6 +417,25 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       const int cbase = ti.half ? ti.ncol0 + (quarter >> 1) * kHalfCols + half * (kHalfCols / 2)
                                 : ti.ncol0 + half * kHalfCols;
       const int nchunks = ti.half ? kChunks / 2 : kChunks;
+      // GEMM2 residual rows, one chunk ahead: chunk c + 1's loads are in
+      // flight while chunk c is stored (chunk 0's while the MMAs finish), so
+      // the epilogue keeps two chunks of residual reads outstanding
+      float4 xa[8], xb[8];
+      auto load_x = [&](int c, float4 (&x)[8]) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 4 + (lane >> 3), q = lane & 7;
+          const int orow_r = __shfl_sync(0xffffffffu, orow, r);
+          x[i] = (gp.resid && qrow0 + r < ti.row_end)
+                     ? __ldg(reinterpret_cast<const float4*>(
+                           gp.resid + static_cast<size_t>(orow_r) * gp.ndim + cbase + c * 32 + q * 4))
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      // (BN = 256: four chunks per warp leave no registers for a second
+      // chunk of residual, so it loads each chunk at the chunk's start)
+      constexpr bool kAhead = BN <= 192;
+      if (st2 && kAhead) load_x(0, xa);
       const unsigned long long c2 = p.prof ? clk() : 0;
       mbar_wait(&tmem_full[acc], acc_phase);
       if (p.prof) w_full += clk() - c2;
@@ -428,6 +447,8 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
       for (int c = 0; c < kChunks; ++c) {
         if (kChunks % 2 == 0 && c == kChunks / 2 && nchunks == kChunks / 2) break;
+        if (st2 && kAhead && c + 1 < nchunks) load_x(c + 1, (c & 1) ? xa : xb);
+        if (st2 && !kAhead) load_x(c, (c & 1) ? xb : xa);
         const int col0 = cbase + c * 32;
         const uint4* bvec = reinterpret_cast<const uint4*>(bias + col0);
         uint4 braw[4];
@@ -484,33 +505,21 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
           }
           __syncwarp();
           // read back: lane -> (row = i*4 + lane/8, chunk = lane%8); residual
-          // and unpermute (row_map) applied per row segment
-          // all eight residual loads in flight before any store (MLP 8)
-          size_t at8[8];
-          float4 x8[8];
-          int brow8[8][kMaxBf16K];
+          // (loaded one chunk ahead, load_x) and unpermute (row_map) per row segment
+          const float4 (&x8)[8] = (c & 1) ? xb : xa;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), q = lane & 7;
             const int orow_r = __shfl_sync(0xffffffffu, orow, r);
+            int brow8[kMaxBf16K];
             if (gp.bf16_map) {
 #pragma unroll
-              for (int j = 0; j < kMaxBf16K; ++j)
-                brow8[i][j] = __shfl_sync(0xffffffffu, brow[j], r);
+              for (int j = 0; j < kMaxBf16K; ++j) brow8[j] = __shfl_sync(0xffffffffu, brow[j], r);
             }
-            at8[i] = static_cast<size_t>(orow_r) * gp.ndim + col0 + q * 4;
-            x8[i] = (gp.resid && qrow0 + r < ti.row_end)
-                        ? __ldg(reinterpret_cast<const float4*>(gp.resid + at8[i]))
-                        : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = i * 4 + (lane >> 3), q = lane & 7;
-            const int orow_r = gp.peer_bf16 ? __shfl_sync(0xffffffffu, orow, r) : 0;
             const uint4 raw = lds128(stile + r * 128 + ((q ^ (r & 7)) << 4));
             if (qrow0 + r < ti.row_end) {
               float4 o = *reinterpret_cast<const float4*>(&raw);
-              const size_t at = at8[i];
+              const size_t at = static_cast<size_t>(orow_r) * gp.ndim + col0 + q * 4;
               if (gp.resid) {
                 const float4 x = x8[i];
                 o.x = x.x + o.x; o.y = x.y + o.y; o.z = x.z + o.z; o.w = x.w + o.w;
@@ -531,7 +540,7 @@ grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
                   for (int j = 0; j < kMaxBf16K; ++j)
                     if (j < gp.bf16_k)
-                      *reinterpret_cast<uint2*>(bf16_row(gp, brow8[i][j]) + col) = ob;
+                      *reinterpret_cast<uint2*>(bf16_row(gp, brow8[j]) + col) = ob;
                 }
               }
             }
