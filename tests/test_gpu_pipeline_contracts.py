@@ -171,3 +171,27 @@ def test_engine_ring_reused_across_calls_and_after_a_failed_call(cuda_device):
     for r in runs[1:]:
         for a, b in zip(runs[0].logits, r.logits):
             assert np.array_equal(a, b)
+
+
+def test_engine_token_pool_grows_across_calls(cuda_device):
+    """serve_sida's per-engine token pool (tokens uploaded one iteration ahead
+    on their own stream, SM-copied from pinned staging) is reallocated when a
+    later call brings larger batches and reused when it brings smaller ones:
+    every call matches a fresh engine's logits."""
+    from paper_2310_18859_b200 import MemoryBudget, PredictorConfig, PredictorNet, Rng, serve_sida
+    from paper_2310_18859_b200.engine import SidaEngine
+
+    model = make_model()
+    pred = PredictorNet(PredictorConfig(), BASE["d_model"], BASE["num_layers"],
+                        BASE["num_experts"], Rng(1))
+    budget = MemoryBudget(3 * model.expert_bytes_each())
+    small = make_stream(model, 4, seed=3)
+    big = make_stream(model, 7, seed=4, batch_size=9, t_len=(10, 13))
+    want = {name: serve_sida(model, pred, b, budget, compute_hit_rate=False).logits
+            for name, b in (("small", small), ("big", big))}
+    eng = SidaEngine(model, pred, budget)
+    for name, b in (("small", small), ("big", big), ("small", small), ("big", big)):
+        got = serve_sida(model, pred, b, budget, engine=eng, compute_hit_rate=False).logits
+        assert len(got) == len(want[name])
+        for a, c in zip(want[name], got):
+            assert np.array_equal(a, c)
